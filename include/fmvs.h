@@ -1,0 +1,262 @@
+/*
+ * fmvs.h — C ABI of the B200-native FaSS-MVS per-frame depth/normal path.
+ *
+ * This is the drop-in boundary for the reference's C++ API in
+ * /root/reference/proj/include/fassmvs/ (SURVEY.md §8b). Plain C types only:
+ * pointers, sizes, POD structs. Every entry point cites the reference
+ * interface it replaces. Host code above this ABI (the C++ adapter
+ * include/fassmvs_b200.hpp, the Python binding paper_2112_00821_b200/) maps
+ * return codes back to the reference's exception types (errors.hpp:10-24).
+ *
+ * Conventions
+ *   - images are 8-bit grayscale, row-major, width*height bytes
+ *     (ImageU8 = Raster<uint8_t>, raster.hpp:13-58)
+ *   - float maps are row-major width*height (DepthMap/ConfidenceMap,
+ *     raster.hpp:60-61); normal maps are interleaved xyz, 3*width*height
+ *     floats (NormalMap = Raster<Eigen::Vector3f>, raster.hpp:62)
+ *   - 3x3 matrices are row-major double[9]
+ *   - return code: FMVS_OK or one of the FMVS_ERR_* codes; the message of the
+ *     last failure on the calling thread is fmvs_last_error()
+ *   - a context owns one CUDA stream and its device arenas; it is not
+ *     reentrant, distinct contexts are fully concurrent (README.md:160-162)
+ */
+#ifndef FMVS_H
+#define FMVS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMVS_ABI_VERSION 1
+
+/* Return codes. 1..3 mirror the reference exception types (errors.hpp:10-24)
+ * whose CLI exit codes are 1/2/1 (tools/fassmvs.cpp:338-353). */
+enum {
+    FMVS_OK = 0,
+    FMVS_ERR_INVALID_INPUT = 1, /* fassmvs::InvalidInputError */
+    FMVS_ERR_CONFIG = 2,        /* fassmvs::ConfigError */
+    FMVS_ERR_GEOMETRY = 3,      /* fassmvs::GeometryError */
+    FMVS_ERR_CUDA = 4,          /* CUDA runtime / device failure (no reference analogue) */
+    FMVS_ERR_CAPACITY = 5       /* caller-provided output buffer too small */
+};
+
+/* Intrinsics (geometry.hpp:19-39). */
+typedef struct fmvs_intrinsics {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} fmvs_intrinsics;
+
+/* Pose (geometry.hpp:44-55): rotation maps reference-frame vectors into the
+ * camera frame (row-major), center in the reference frame. */
+typedef struct fmvs_pose {
+    double rotation[9];
+    double center[3];
+} fmvs_pose;
+
+/* CalibratedView (geometry.hpp:57-63). */
+typedef struct fmvs_view {
+    const uint8_t* image; /* width*height bytes, row-major */
+    fmvs_intrinsics intrinsics;
+    fmvs_pose pose;
+} fmvs_view;
+
+/* PlaneStack (geometry.hpp:75-94): shared normal + strictly decreasing
+ * distances. */
+typedef struct fmvs_plane_stack {
+    double normal[3];
+    const double* distances;
+    int32_t count;
+} fmvs_plane_stack;
+
+enum { FMVS_COST_CENSUS = 0, FMVS_COST_NCC = 1 };              /* CostKind, matching.hpp:12 */
+enum { FMVS_SGM_PLANE = 0, FMVS_SGM_SURFACE_NORMAL = 1,
+       FMVS_SGM_PATH_GRADIENT = 2 };                            /* SgmVariant, sgm.hpp:13-17 */
+enum { FMVS_RANGE_FULL = 0, FMVS_RANGE_FIXED = 1,
+       FMVS_RANGE_SPACING_MULTIPLE = 2 };                       /* RangePolicy::Kind, pipeline.hpp:13-18 */
+
+/* SgmConfig (sgm.hpp:19-32). */
+typedef struct fmvs_sgm_config {
+    int32_t variant;
+    int32_t paths; /* 8 or 4 */
+    double phi1;
+    int32_t phi2_adaptive;
+    double phi2_fixed;
+    double alpha;
+    double beta;
+    int32_t penalty_scale;
+} fmvs_sgm_config;
+
+/* CostFunctionSpec (matching.hpp:14-23). */
+typedef struct fmvs_cost_spec {
+    int32_t kind;
+    int32_t window_w;
+    int32_t window_h;
+} fmvs_cost_spec;
+
+/* PipelineConfig (pipeline.hpp:22-35) incl. DepthBounds and RangePolicy. */
+typedef struct fmvs_config {
+    int32_t bundle_size;
+    int32_t pyramid_levels;
+    double d_min, d_max;
+    double sweep_normal[3];
+    int32_t range_kind;
+    double range_value;
+    int32_t max_planes;
+    fmvs_sgm_config sgm;
+    fmvs_cost_spec cost;
+    int32_t normal_smoothing_radius;
+} fmvs_config;
+
+/* Per-level statistics of the last estimate on a context. */
+typedef struct fmvs_level_stats {
+    int32_t width, height;
+    int32_t planes;        /* global plane-stack size of the level */
+    uint64_t entries;      /* sum over pixels of CostVolume::count */
+} fmvs_level_stats;
+
+typedef struct fmvs_ctx fmvs_ctx;
+
+/* ---------------------------------------------------------------- misc -- */
+int32_t fmvs_abi_version(void);
+const char* fmvs_last_error(void);
+/* Fills the reference defaults (PipelineConfig ctor, pipeline.hpp:22-35;
+ * SgmConfig sgm.hpp:19-32; CostFunctionSpec matching.hpp:14-23). */
+void fmvs_config_default(fmvs_config* cfg, double d_min, double d_max);
+
+/* ------------------------------------------------------------- context -- */
+int fmvs_ctx_create(int32_t device, fmvs_ctx** out);
+void fmvs_ctx_destroy(fmvs_ctx* ctx);
+int fmvs_ctx_synchronize(fmvs_ctx* ctx);
+/* Per-level statistics of the last estimate_bundle on this context; returns
+ * the number of levels written (<= capacity). */
+int32_t fmvs_ctx_level_stats(fmvs_ctx* ctx, fmvs_level_stats* out, int32_t capacity);
+/* Number of kernels the last estimate enqueued. */
+int64_t fmvs_ctx_last_launch_count(fmvs_ctx* ctx);
+
+/* ------------------------------------------------------------ hot path -- */
+/* fassmvs::estimate_bundle (pipeline.hpp:79-80, pipeline.cpp:200-309).
+ * Host buffers in and out: depth/confidence width*height floats, normals
+ * 3*width*height floats, all at the reference view's full resolution.
+ * Blocking: returns when the outputs are written. */
+int fmvs_estimate_bundle(fmvs_ctx* ctx, const fmvs_view* views, int32_t n_views,
+                         const fmvs_config* cfg, float* depth, float* normals_xyz,
+                         float* confidence);
+
+/* Device-resident variant: views[k].image are DEVICE pointers, outputs are
+ * DEVICE pointers; enqueued on the context stream and returns without
+ * waiting (fmvs_ctx_synchronize to wait). Same validation and results. */
+int fmvs_estimate_bundle_device(fmvs_ctx* ctx, const fmvs_view* views, int32_t n_views,
+                                const fmvs_config* cfg, float* d_depth, float* d_normals_xyz,
+                                float* d_confidence);
+
+/* ------------------------------------------------- host-side geometry -- */
+/* plane_homography (geometry.hpp:100-103, geometry.cpp:100-114). */
+int fmvs_plane_homography(const double normal[3], double distance,
+                          const fmvs_intrinsics* ref_intr, const fmvs_pose* ref_pose,
+                          const fmvs_intrinsics* other_intr, const fmvs_pose* other_pose,
+                          double out_h[9]);
+/* bounding_distances (geometry.hpp:110-112, geometry.cpp:121-145). */
+int fmvs_bounding_distances(double d_min, double d_max, const double normal[3],
+                            const fmvs_intrinsics* ref_intr, double* delta_min,
+                            double* delta_max);
+/* plane_distances (geometry.hpp:132-135, geometry.cpp:183-297). Writes at
+ * most capacity distances; *count receives the full count
+ * (FMVS_ERR_CAPACITY when it exceeds capacity). */
+int fmvs_plane_distances(const fmvs_intrinsics* ref_intr, const fmvs_pose* ref_pose,
+                         const fmvs_intrinsics* other_intr, const fmvs_pose* other_pose,
+                         double delta_min, double delta_max, const double normal[3],
+                         int32_t max_planes, double* out, int32_t capacity, int32_t* count);
+/* depth_from_plane (geometry.hpp:140, geometry.cpp:299-306). */
+double fmvs_depth_from_plane(double x, double y, const double normal[3], double distance,
+                             const fmvs_intrinsics* intr);
+/* adaptive_phi2 (sgm.hpp:36, sgm.cpp:22-24). */
+double fmvs_adaptive_phi2(double phi1, double alpha, double beta, double intensity_delta);
+/* parabola_refine (sgm.hpp:98-101, sgm.cpp:351-363). */
+int fmvs_parabola_refine(double d_prev, double d_win, double d_next, double c_prev,
+                         double c_win, double c_next, double* out);
+
+/* -------------------------------------------- device stages (host I/O) -- */
+/* build_pyramids (pipeline.hpp:50, pipeline.cpp:79-126): out_images holds
+ * levels x n_views images back to back (level-major, each level's size from
+ * out_intr[level*n_views + k]); capacity in bytes. */
+int fmvs_build_pyramids(fmvs_ctx* ctx, const fmvs_view* views, int32_t n_views,
+                        int32_t levels, uint8_t* out_images, uint64_t capacity,
+                        fmvs_intrinsics* out_intr);
+
+/* refine_range (pipeline.hpp:63-65, pipeline.cpp:136-173). coarser and intr
+ * may be NULL (required by the spacing policy). */
+int fmvs_refine_range(fmvs_ctx* ctx, const float* prior, int32_t width, int32_t height,
+                      int32_t range_kind, double range_value, double d_min, double d_max,
+                      const fmvs_plane_stack* coarser, const fmvs_intrinsics* intr, float* lo,
+                      float* hi);
+
+/* sweep_cost_volume (matching.hpp:74-76, matching.cpp:116-294). Outputs the
+ * dynamic CostVolume (matching.hpp:36-53): first/count/offset per pixel and
+ * costs (capacity entries; *total receives the entry count, FMVS_ERR_CAPACITY
+ * when it exceeds capacity). */
+int fmvs_sweep_cost_volume(fmvs_ctx* ctx, const fmvs_view* views, int32_t n_views,
+                           int32_t ref_index, const fmvs_plane_stack* planes, const float* lo,
+                           const float* hi, const fmvs_cost_spec* cost, int32_t* first,
+                           int32_t* count, uint64_t* offset, uint16_t* costs, uint64_t capacity,
+                           uint64_t* total, int32_t* per_side);
+
+/* compute_normal_offsets (sgm.hpp:66-68, sgm.cpp:252-299): out holds 4
+ * int16 shifts per pixel (canonical dirs, sgm.hpp:55-56). */
+int fmvs_compute_normal_offsets(fmvs_ctx* ctx, const float* prior_normals_xyz,
+                                const float* prior_depth, int32_t width, int32_t height,
+                                const fmvs_plane_stack* planes, const fmvs_intrinsics* intr,
+                                int16_t* out);
+
+/* aggregate / aggregate_single_path (sgm.hpp:86-96, sgm.cpp:301-331). The
+ * volume is given as the reference's ragged layout. dir_x = dir_y = 0 runs
+ * all cfg->paths directions; otherwise the single path (dir_x, dir_y).
+ * prior_* may be NULL unless the variant is SurfaceNormal. */
+int fmvs_aggregate(fmvs_ctx* ctx, int32_t width, int32_t height, const fmvs_plane_stack* planes,
+                   const int32_t* first, const int32_t* count, const uint64_t* offset,
+                   const uint16_t* costs, uint64_t total, const uint8_t* image,
+                   const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
+                   const float* prior_normals_xyz, const float* prior_depth, int32_t dir_x,
+                   int32_t dir_y, uint32_t* out_values);
+
+/* wta (sgm.hpp:93, sgm.cpp:333-349). */
+int fmvs_wta(fmvs_ctx* ctx, int32_t width, int32_t height, const int32_t* first,
+             const int32_t* count, const uint64_t* offset, const uint32_t* values,
+             uint64_t total, int32_t* winners);
+
+/* median_filter_5x5 (pipeline.hpp:70, pipeline.cpp:175-198). */
+int fmvs_median_filter_5x5(fmvs_ctx* ctx, const float* depth, int32_t width, int32_t height,
+                           float* out);
+
+/* normals_from_depth / smooth_normals / confidence_map (surface.hpp:11-24,
+ * surface.cpp:9-104). */
+int fmvs_normals_from_depth(fmvs_ctx* ctx, const float* depth, int32_t width, int32_t height,
+                            const fmvs_intrinsics* intr, float* out_xyz);
+int fmvs_smooth_normals(fmvs_ctx* ctx, const float* raw_xyz, const uint8_t* image,
+                        int32_t width, int32_t height, int32_t radius, float* out_xyz);
+int fmvs_confidence_map(fmvs_ctx* ctx, const float* normals_xyz, int32_t width, int32_t height,
+                        const double sweep_normal[3], double rho_degrees, float* out);
+
+/* upscale_nearest (pipeline.hpp:58-59, pipeline.cpp:91-134); channels = 1
+ * (DepthMap) or 3 (NormalMap). */
+int fmvs_upscale_nearest(fmvs_ctx* ctx, const float* in, int32_t in_width, int32_t in_height,
+                         int32_t channels, int32_t out_width, int32_t out_height, float* out);
+
+/* --------------------------------------------- synthetic input (bench) -- */
+/* render_scene over fronto_scene / slanted_scene (render.hpp:41-62,
+ * render.cpp:52-183) on the device: kind 0 = fronto, 1 = slanted. images:
+ * n_views*width*height bytes; gt_depth / gt_normals_xyz of every view (may be
+ * NULL); intr / poses receive the cameras. */
+int fmvs_render_plane_scene(fmvs_ctx* ctx, int32_t kind, int32_t width, int32_t height,
+                            double focal, double depth, double tilt_deg, int32_t n_views,
+                            double baseline_step, uint64_t seed, double texture_scale,
+                            uint8_t* images, float* gt_depth, float* gt_normals_xyz,
+                            fmvs_intrinsics* intr, fmvs_pose* poses);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FMVS_H */

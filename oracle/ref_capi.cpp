@@ -1,0 +1,480 @@
+// Oracle C ABI: the UNMODIFIED reference library (/root/reference/proj/src,
+// built against oracle/eigen_shim by oracle/Makefile) exposed through the same
+// signatures as include/fmvs.h with a `ref_` prefix, so the parity tests can
+// drive the reference and the B200 library through one Python binding.
+//
+// TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+// CPU-baseline leg load this library. Nothing here is on the product path.
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "fassmvs/errors.hpp"
+#include "fassmvs/geometry.hpp"
+#include "fassmvs/matching.hpp"
+#include "fassmvs/parallel.hpp"
+#include "fassmvs/pipeline.hpp"
+#include "fassmvs/postfilter.hpp"
+#include "fassmvs/render.hpp"
+#include "fassmvs/sgm.hpp"
+#include "fassmvs/surface.hpp"
+#include "fmvs.h"
+
+using namespace fassmvs;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return FMVS_OK;
+    } catch (const InvalidInputError& e) {
+        g_err = e.what();
+        return FMVS_ERR_INVALID_INPUT;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return FMVS_ERR_CONFIG;
+    } catch (const GeometryError& e) {
+        g_err = e.what();
+        return FMVS_ERR_GEOMETRY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FMVS_ERR_CUDA;
+    }
+}
+
+Intrinsics to_intr(const fmvs_intrinsics& i) {
+    Intrinsics r;
+    r.fx = i.fx;
+    r.fy = i.fy;
+    r.cx = i.cx;
+    r.cy = i.cy;
+    r.width = i.width;
+    r.height = i.height;
+    return r;
+}
+
+fmvs_intrinsics from_intr(const Intrinsics& i) {
+    return {i.fx, i.fy, i.cx, i.cy, i.width, i.height};
+}
+
+Pose to_pose(const fmvs_pose& p) {
+    Pose r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r.rotation(i, j) = p.rotation[3 * i + j];
+    r.center = Eigen::Vector3d(p.center[0], p.center[1], p.center[2]);
+    return r;
+}
+
+fmvs_pose from_pose(const Pose& p) {
+    fmvs_pose r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            r.rotation[3 * i + j] = p.rotation(i, j);
+    for (int i = 0; i < 3; ++i)
+        r.center[i] = p.center(i);
+    return r;
+}
+
+ImageU8 to_image(const uint8_t* data, int w, int h) {
+    ImageU8 img(w, h, 0);
+    if (data && w > 0 && h > 0)
+        std::memcpy(img.data(), data, static_cast<std::size_t>(w) * h);
+    return img;
+}
+
+std::vector<CalibratedView> to_bundle(const fmvs_view* views, int n) {
+    std::vector<CalibratedView> b(n);
+    for (int k = 0; k < n; ++k) {
+        b[k].intrinsics = to_intr(views[k].intrinsics);
+        b[k].pose = to_pose(views[k].pose);
+        b[k].image = to_image(views[k].image, views[k].intrinsics.width,
+                              views[k].intrinsics.height);
+    }
+    return b;
+}
+
+Eigen::Vector3d v3(const double* n) { return Eigen::Vector3d(n[0], n[1], n[2]); }
+
+PlaneStack to_stack(const fmvs_plane_stack* s) {
+    PlaneStack p;
+    p.normal = v3(s->normal);
+    p.distances.assign(s->distances, s->distances + s->count);
+    return p;
+}
+
+SgmConfig to_sgm(const fmvs_sgm_config& c) {
+    SgmConfig s;
+    s.variant = static_cast<SgmVariant>(c.variant);
+    s.paths = c.paths;
+    s.phi1 = c.phi1;
+    s.phi2_adaptive = c.phi2_adaptive != 0;
+    s.phi2_fixed = c.phi2_fixed;
+    s.alpha = c.alpha;
+    s.beta = c.beta;
+    s.penalty_scale = c.penalty_scale;
+    return s;
+}
+
+CostFunctionSpec to_cost(const fmvs_cost_spec& c) {
+    CostFunctionSpec s;
+    s.kind = static_cast<CostKind>(c.kind);
+    s.window_w = c.window_w;
+    s.window_h = c.window_h;
+    return s;
+}
+
+PipelineConfig to_config(const fmvs_config& c) {
+    PipelineConfig p(DepthBounds(c.d_min, c.d_max));
+    p.bundle_size = c.bundle_size;
+    p.pyramid_levels = c.pyramid_levels;
+    p.sweep_normal = v3(c.sweep_normal);
+    p.range_policy.kind = static_cast<RangePolicy::Kind>(c.range_kind);
+    p.range_policy.value = c.range_value;
+    p.max_planes = c.max_planes;
+    p.sgm = to_sgm(c.sgm);
+    p.cost = to_cost(c.cost);
+    p.normal_smoothing_radius = c.normal_smoothing_radius;
+    return p;
+}
+
+DepthMap to_depth(const float* d, int w, int h) {
+    DepthMap m(w, h, 0.0f);
+    std::memcpy(m.data(), d, sizeof(float) * static_cast<std::size_t>(w) * h);
+    return m;
+}
+
+NormalMap to_normals(const float* xyz, int w, int h) {
+    NormalMap m = make_normal_map(w, h);
+    for (std::size_t p = 0; p < static_cast<std::size_t>(w) * h; ++p)
+        m.data()[p] = Eigen::Vector3f(xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2]);
+    return m;
+}
+
+void write_normals(const NormalMap& m, float* xyz) {
+    for (std::size_t p = 0; p < m.size(); ++p) {
+        xyz[3 * p] = m.data()[p].x();
+        xyz[3 * p + 1] = m.data()[p].y();
+        xyz[3 * p + 2] = m.data()[p].z();
+    }
+}
+
+CostVolume to_volume(int w, int h, const fmvs_plane_stack* planes, const int32_t* first,
+                     const int32_t* count, const uint64_t* offset, const uint16_t* costs,
+                     uint64_t total) {
+    CostVolume v;
+    v.width = w;
+    v.height = h;
+    v.planes = to_stack(planes);
+    const std::size_t npx = static_cast<std::size_t>(w) * h;
+    v.first.assign(first, first + npx);
+    v.count.assign(count, count + npx);
+    v.offset.assign(offset, offset + npx);
+    v.costs.assign(costs, costs + total);
+    return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ref_abi_version(void) { return FMVS_ABI_VERSION; }
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_worker_count(void) { return worker_count(); }
+
+void ref_config_default(fmvs_config* cfg, double d_min, double d_max) {
+    const PipelineConfig p(DepthBounds(d_min, d_max));
+    cfg->bundle_size = p.bundle_size;
+    cfg->pyramid_levels = p.pyramid_levels;
+    cfg->d_min = d_min;
+    cfg->d_max = d_max;
+    for (int i = 0; i < 3; ++i)
+        cfg->sweep_normal[i] = p.sweep_normal(i);
+    cfg->range_kind = static_cast<int32_t>(p.range_policy.kind);
+    cfg->range_value = p.range_policy.value;
+    cfg->max_planes = p.max_planes;
+    cfg->sgm = {static_cast<int32_t>(p.sgm.variant), p.sgm.paths, p.sgm.phi1,
+                p.sgm.phi2_adaptive ? 1 : 0, p.sgm.phi2_fixed, p.sgm.alpha, p.sgm.beta,
+                p.sgm.penalty_scale};
+    cfg->cost = {static_cast<int32_t>(p.cost.kind), p.cost.window_w, p.cost.window_h};
+    cfg->normal_smoothing_radius = p.normal_smoothing_radius;
+}
+
+int ref_estimate_bundle(void*, const fmvs_view* views, int32_t n_views, const fmvs_config* cfg,
+                        float* depth, float* normals_xyz, float* confidence) {
+    return guard([&] {
+        const BundleResult r = estimate_bundle(to_bundle(views, n_views), to_config(*cfg));
+        std::memcpy(depth, r.depth.data(), sizeof(float) * r.depth.size());
+        write_normals(r.normals, normals_xyz);
+        std::memcpy(confidence, r.confidence.data(), sizeof(float) * r.confidence.size());
+    });
+}
+
+int ref_plane_homography(const double normal[3], double distance, const fmvs_intrinsics* ri,
+                         const fmvs_pose* rp, const fmvs_intrinsics* oi, const fmvs_pose* op,
+                         double out_h[9]) {
+    return guard([&] {
+        const Eigen::Matrix3d h = plane_homography(SweepPlane{v3(normal), distance}, to_intr(*ri),
+                                                   to_pose(*rp), to_intr(*oi), to_pose(*op));
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                out_h[3 * i + j] = h(i, j);
+    });
+}
+
+int ref_bounding_distances(double d_min, double d_max, const double normal[3],
+                           const fmvs_intrinsics* ri, double* dmin, double* dmax) {
+    return guard([&] {
+        const auto [a, b] = bounding_distances(DepthBounds(d_min, d_max), v3(normal), to_intr(*ri));
+        *dmin = a;
+        *dmax = b;
+    });
+}
+
+int ref_plane_distances(const fmvs_intrinsics* ri, const fmvs_pose* rp, const fmvs_intrinsics* oi,
+                        const fmvs_pose* op, double delta_min, double delta_max,
+                        const double normal[3], int32_t max_planes, double* out,
+                        int32_t capacity, int32_t* count) {
+    int rc = guard([&] {
+        const std::vector<double> d = plane_distances(to_intr(*ri), to_pose(*rp), to_intr(*oi),
+                                                      to_pose(*op), delta_min, delta_max,
+                                                      v3(normal), max_planes);
+        *count = static_cast<int32_t>(d.size());
+        for (int i = 0; i < static_cast<int>(d.size()) && i < capacity; ++i)
+            out[i] = d[i];
+    });
+    if (rc == FMVS_OK && *count > capacity) {
+        g_err = "plane distances: output capacity too small";
+        return FMVS_ERR_CAPACITY;
+    }
+    return rc;
+}
+
+double ref_depth_from_plane(double x, double y, const double normal[3], double distance,
+                            const fmvs_intrinsics* intr) {
+    return depth_from_plane(Eigen::Vector2d(x, y), SweepPlane{v3(normal), distance},
+                            to_intr(*intr));
+}
+
+double ref_adaptive_phi2(double phi1, double alpha, double beta, double di) {
+    return adaptive_phi2(phi1, alpha, beta, di);
+}
+
+int ref_parabola_refine(double a, double b, double c, double ca, double cb, double cc,
+                        double* out) {
+    return guard([&] { *out = parabola_refine(a, b, c, ca, cb, cc); });
+}
+
+int ref_build_pyramids(void*, const fmvs_view* views, int32_t n_views, int32_t levels,
+                       uint8_t* out_images, uint64_t capacity, fmvs_intrinsics* out_intr) {
+    return guard([&] {
+        const PyramidLevelSet set = build_pyramids(to_bundle(views, n_views), levels);
+        uint64_t pos = 0;
+        for (int l = 0; l < levels; ++l)
+            for (int k = 0; k < n_views; ++k) {
+                const CalibratedView& v = set.levels[l][k];
+                out_intr[l * n_views + k] = from_intr(v.intrinsics);
+                if (pos + v.image.size() > capacity)
+                    throw std::runtime_error("pyramid output capacity too small");
+                std::memcpy(out_images + pos, v.image.data(), v.image.size());
+                pos += v.image.size();
+            }
+    });
+}
+
+int ref_gaussian_blur(const uint8_t* image, int32_t w, int32_t h, int32_t radius, double sigma,
+                      float* out) {
+    return guard([&] {
+        const Raster<float> r = gaussian_blur(to_image(image, w, h), radius, sigma);
+        std::memcpy(out, r.data(), sizeof(float) * r.size());
+    });
+}
+
+int ref_refine_range(void*, const float* prior, int32_t w, int32_t h, int32_t kind, double value,
+                     double d_min, double d_max, const fmvs_plane_stack* coarser,
+                     const fmvs_intrinsics* intr, float* lo, float* hi) {
+    return guard([&] {
+        RangePolicy pol;
+        pol.kind = static_cast<RangePolicy::Kind>(kind);
+        pol.value = value;
+        PlaneStack stack;
+        if (coarser)
+            stack = to_stack(coarser);
+        Intrinsics in;
+        if (intr)
+            in = to_intr(*intr);
+        const SamplingRange r = refine_range(to_depth(prior, w, h), pol, DepthBounds(d_min, d_max),
+                                             coarser ? &stack : nullptr, intr ? &in : nullptr);
+        std::memcpy(lo, r.lo.data(), sizeof(float) * r.lo.size());
+        std::memcpy(hi, r.hi.data(), sizeof(float) * r.hi.size());
+    });
+}
+
+int ref_sweep_cost_volume(void*, const fmvs_view* views, int32_t n_views, int32_t ref_index,
+                          const fmvs_plane_stack* planes, const float* lo, const float* hi,
+                          const fmvs_cost_spec* cost, int32_t* first, int32_t* count,
+                          uint64_t* offset, uint16_t* costs, uint64_t capacity, uint64_t* total,
+                          int32_t* per_side) {
+    int rc = guard([&] {
+        const std::vector<CalibratedView> b = to_bundle(views, n_views);
+        const int w = b[ref_index < 0 || ref_index >= n_views ? 0 : ref_index].intrinsics.width;
+        const int h = b[ref_index < 0 || ref_index >= n_views ? 0 : ref_index].intrinsics.height;
+        SamplingRange r;
+        r.lo = to_depth(lo, w, h);
+        r.hi = to_depth(hi, w, h);
+        const CostVolume v = sweep_cost_volume(b, ref_index, to_stack(planes), r, to_cost(*cost));
+        const std::size_t npx = static_cast<std::size_t>(w) * h;
+        std::memcpy(first, v.first.data(), 4 * npx);
+        std::memcpy(count, v.count.data(), 4 * npx);
+        for (std::size_t p = 0; p < npx; ++p)
+            offset[p] = v.offset[p];
+        *total = v.costs.size();
+        *per_side = v.per_side;
+        if (v.costs.size() <= capacity)
+            std::memcpy(costs, v.costs.data(), 2 * v.costs.size());
+    });
+    if (rc == FMVS_OK && *total > capacity) {
+        g_err = "sweep: cost capacity too small";
+        return FMVS_ERR_CAPACITY;
+    }
+    return rc;
+}
+
+int ref_compute_normal_offsets(void*, const float* prior_normals_xyz, const float* prior_depth,
+                               int32_t w, int32_t h, const fmvs_plane_stack* planes,
+                               const fmvs_intrinsics* intr, int16_t* out) {
+    return guard([&] {
+        const NormalOffsets o = compute_normal_offsets(to_normals(prior_normals_xyz, w, h),
+                                                       to_depth(prior_depth, w, h),
+                                                       to_stack(planes), to_intr(*intr));
+        for (std::size_t p = 0; p < o.size(); ++p)
+            for (int c = 0; c < 4; ++c)
+                out[4 * p + c] = o.data()[p][c];
+    });
+}
+
+int ref_aggregate(void*, int32_t w, int32_t h, const fmvs_plane_stack* planes,
+                  const int32_t* first, const int32_t* count, const uint64_t* offset,
+                  const uint16_t* costs, uint64_t total, const uint8_t* image,
+                  const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
+                  const float* prior_normals_xyz, const float* prior_depth, int32_t dir_x,
+                  int32_t dir_y, uint32_t* out_values) {
+    return guard([&] {
+        const CostVolume v = to_volume(w, h, planes, first, count, offset, costs, total);
+        NormalMap pn;
+        DepthMap pd;
+        if (prior_normals_xyz)
+            pn = to_normals(prior_normals_xyz, w, h);
+        if (prior_depth)
+            pd = to_depth(prior_depth, w, h);
+        const ImageU8 img = to_image(image, w, h);
+        const Intrinsics in = to_intr(*intr);
+        const AggregatedVolume a =
+            (dir_x == 0 && dir_y == 0)
+                ? aggregate(v, img, to_sgm(*cfg), in, prior_normals_xyz ? &pn : nullptr,
+                            prior_depth ? &pd : nullptr)
+                : aggregate_single_path(v, img, to_sgm(*cfg), in, dir_x, dir_y,
+                                        prior_normals_xyz ? &pn : nullptr,
+                                        prior_depth ? &pd : nullptr);
+        std::memcpy(out_values, a.values.data(), 4 * a.values.size());
+    });
+}
+
+int ref_wta(void*, int32_t w, int32_t h, const int32_t* first, const int32_t* count,
+            const uint64_t* offset, const uint32_t* values, uint64_t total, int32_t* winners) {
+    return guard([&] {
+        AggregatedVolume a;
+        a.width = w;
+        a.height = h;
+        const std::size_t npx = static_cast<std::size_t>(w) * h;
+        a.first.assign(first, first + npx);
+        a.count.assign(count, count + npx);
+        a.offset.assign(offset, offset + npx);
+        a.values.assign(values, values + total);
+        const PlaneIndexMap m = wta(a);
+        std::memcpy(winners, m.data(), 4 * npx);
+    });
+}
+
+int ref_median_filter_5x5(void*, const float* depth, int32_t w, int32_t h, float* out) {
+    return guard([&] {
+        const DepthMap m = median_filter_5x5(to_depth(depth, w, h));
+        std::memcpy(out, m.data(), sizeof(float) * m.size());
+    });
+}
+
+int ref_normals_from_depth(void*, const float* depth, int32_t w, int32_t h,
+                           const fmvs_intrinsics* intr, float* out_xyz) {
+    return guard([&] { write_normals(normals_from_depth(to_depth(depth, w, h), to_intr(*intr)), out_xyz); });
+}
+
+int ref_smooth_normals(void*, const float* raw_xyz, const uint8_t* image, int32_t w, int32_t h,
+                       int32_t radius, float* out_xyz) {
+    return guard([&] {
+        write_normals(smooth_normals(to_normals(raw_xyz, w, h), to_image(image, w, h), radius),
+                      out_xyz);
+    });
+}
+
+int ref_confidence_map(void*, const float* normals_xyz, int32_t w, int32_t h,
+                       const double sweep_normal[3], double rho_degrees, float* out) {
+    return guard([&] {
+        const ConfidenceMap c = confidence_map(to_normals(normals_xyz, w, h), v3(sweep_normal),
+                                               rho_degrees);
+        std::memcpy(out, c.data(), sizeof(float) * c.size());
+    });
+}
+
+int ref_upscale_nearest(void*, const float* in, int32_t iw, int32_t ih, int32_t channels,
+                        int32_t ow, int32_t oh, float* out) {
+    return guard([&] {
+        if (channels == 1) {
+            const DepthMap m = upscale_nearest(to_depth(in, iw, ih), ow, oh);
+            std::memcpy(out, m.data(), sizeof(float) * m.size());
+        } else {
+            write_normals(upscale_nearest(to_normals(in, iw, ih), ow, oh), out);
+        }
+    });
+}
+
+int ref_render_plane_scene(void*, int32_t kind, int32_t w, int32_t h, double focal, double depth,
+                           double tilt_deg, int32_t n_views, double step, uint64_t seed,
+                           double texture_scale, uint8_t* images, float* gt_depth,
+                           float* gt_normals_xyz, fmvs_intrinsics* intr, fmvs_pose* poses) {
+    return guard([&] {
+        SyntheticScene s = kind == 0
+                               ? fronto_scene(w, h, focal, depth, n_views, step, seed)
+                               : slanted_scene(w, h, focal, depth, tilt_deg, n_views, step, seed);
+        s.texture_scale = texture_scale;
+        const std::vector<RenderedView> r = render_scene(s);
+        const std::size_t npx = static_cast<std::size_t>(w) * h;
+        for (int k = 0; k < n_views; ++k) {
+            std::memcpy(images + k * npx, r[k].view.image.data(), npx);
+            if (gt_depth)
+                std::memcpy(gt_depth + k * npx, r[k].gt_depth.data(), 4 * npx);
+            if (gt_normals_xyz)
+                write_normals(r[k].gt_normals, gt_normals_xyz + 3 * k * npx);
+            if (intr)
+                intr[k] = from_intr(r[k].view.intrinsics);
+            if (poses)
+                poses[k] = from_pose(r[k].view.pose);
+        }
+    });
+}
+
+// DoG texture mask (postfilter.hpp:18-48), used by the accuracy criteria.
+int ref_dog_mask(const uint8_t* image, int32_t w, int32_t h, uint8_t* out) {
+    return guard([&] {
+        const TextureMask m = dog_mask(to_image(image, w, h));
+        for (std::size_t p = 0; p < m.size(); ++p)
+            out[p] = m.data()[p] ? 1 : 0;
+    });
+}
+
+}  // extern "C"
