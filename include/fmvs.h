@@ -135,6 +135,18 @@ int fmvs_ctx_synchronize(fmvs_ctx* ctx);
 int32_t fmvs_ctx_level_stats(fmvs_ctx* ctx, fmvs_level_stats* out, int32_t capacity);
 /* Number of kernels the last estimate enqueued. */
 int64_t fmvs_ctx_last_launch_count(fmvs_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for event timing by callers. */
+void* fmvs_ctx_stream(fmvs_ctx* ctx);
+/* Optional per-stage CUDA-event timing on the context stream (stage times
+ * accumulate over calls until fmvs_ctx_stage_reset). */
+void fmvs_ctx_set_timing(fmvs_ctx* ctx, int32_t enable);
+int32_t fmvs_ctx_stage_count(fmvs_ctx* ctx);
+const char* fmvs_ctx_stage_name(fmvs_ctx* ctx, int32_t index);
+int fmvs_ctx_stage_time(fmvs_ctx* ctx, int32_t index, double* ms, int64_t* calls);
+void fmvs_ctx_stage_reset(fmvs_ctx* ctx);
+/* Pinned host memory for zero-staging H2D/D2H of bundles and maps. */
+void* fmvs_host_alloc(uint64_t bytes);
+void fmvs_host_free(void* ptr);
 
 /* ------------------------------------------------------------ hot path -- */
 /* fassmvs::estimate_bundle (pipeline.hpp:79-80, pipeline.cpp:200-309).

@@ -1,0 +1,20 @@
+"""B200-native FaSS-MVS per-frame depth/normal/confidence pipeline.
+
+The product is ``_lib/libfmvs.so``: hand-written sm_100a CUDA kernels and a
+C++ host driver behind the C ABI in ``include/fmvs.h``. This package is the
+Python binding of that ABI, mirroring the reference API names
+(``fassmvs::estimate_bundle`` etc.). There is no CPU fallback: importing the
+binding when the library is not built raises.
+"""
+from .fassmvs import (  # noqa: F401
+    AggregatedVolume, Backend, BundleResult, CalibratedView, ConfigError, CostFunctionSpec,
+    CostKind, CostVolume, CudaError, GeometryError, Intrinsics, InvalidInputError,
+    PipelineConfig, PlaneStack, Pose, RangeKind, RangePolicy, SgmConfig, SgmVariant,
+    default_backend, estimate_bundle)
+
+__all__ = [
+    "AggregatedVolume", "Backend", "BundleResult", "CalibratedView", "ConfigError",
+    "CostFunctionSpec", "CostKind", "CostVolume", "CudaError", "GeometryError", "Intrinsics",
+    "InvalidInputError", "PipelineConfig", "PlaneStack", "Pose", "RangeKind", "RangePolicy",
+    "SgmConfig", "SgmVariant", "default_backend", "estimate_bundle",
+]

@@ -1,0 +1,1367 @@
+// Host driver and C ABI (include/fmvs.h) of the B200 FaSS-MVS library.
+//
+// estimate_bundle (pipeline.cpp:200-309) is split into
+//   1. a host plan: validation in the reference's order and every
+//      data-independent quantity for ALL levels (plane stacks, homographies,
+//      lookup tables), uploaded in one H2D copy;
+//   2. a fixed device launch sequence on the context stream: pyramid, then per
+//      level range -> scan -> sweep -> [SN offsets] -> SGM -> WTA/depth ->
+//      median -> normals/smoothing/confidence. The ragged cost volume lives in
+//      worst-case arenas, so the sequence never synchronises with the host.
+// The stage entry points (fmvs_sweep_cost_volume, fmvs_aggregate, ...) run the
+// same kernels on host-provided inputs for stage-wise parity tests.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace k = fmvs::k;
+using fmvs::Error;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FMVS_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return FMVS_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FMVS_ERR_CUDA;
+    }
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (ptr)
+                cudaFree(ptr);
+            ptr = nullptr;
+            cap = 0;
+            const size_t want = std::max<size_t>(bytes, 256);
+            FMVS_CUDA_CHECK(cudaMalloc(&ptr, want));
+            cap = want;
+        }
+        return ptr;
+    }
+    template <typename T>
+    T* as(size_t count) {
+        return static_cast<T*>(get(count * sizeof(T)));
+    }
+    ~DevBuf() {
+        if (ptr)
+            cudaFree(ptr);
+    }
+};
+
+// Grow-only pinned host buffer.
+struct HostBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (ptr)
+                cudaFreeHost(ptr);
+            ptr = nullptr;
+            cap = 0;
+            FMVS_CUDA_CHECK(cudaMallocHost(&ptr, std::max<size_t>(bytes, 256)));
+            cap = std::max<size_t>(bytes, 256);
+        }
+        return ptr;
+    }
+    ~HostBuf() {
+        if (ptr)
+            cudaFreeHost(ptr);
+    }
+};
+
+// Scratch device memory for the stage API (freed on scope exit).
+struct Tmp {
+    std::vector<void*> ptrs;
+    template <typename T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        FMVS_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <typename T>
+    T* upload(const T* host, size_t count, cudaStream_t s) {
+        T* d = alloc<T>(count);
+        if (count)
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+        return d;
+    }
+    ~Tmp() {
+        for (void* p : ptrs)
+            cudaFree(p);
+    }
+};
+
+fmvs::V3 v3(const double* n) { return {n[0], n[1], n[2]}; }
+
+fmvs::dev::Intr intr_of(const fmvs_intrinsics& k) { return fmvs::dev::make_intr(k); }
+
+// Host plan of one level (everything data-independent).
+struct LevelPlan {
+    int w = 0, h = 0;
+    std::vector<fmvs_intrinsics> intr;  // per view
+    std::vector<double> planes;
+    std::vector<double> homs;           // [nmatch][P][9]
+    // offsets into the uploaded plan blob (in doubles)
+    size_t off_planes = 0, off_homs = 0;
+    size_t img_off = 0;                 // per-level byte offset of the image block
+    size_t quad_off = 0;                // per-level u32 offset of the quad block
+};
+
+// Validation + geometry for a whole bundle (pipeline.cpp:202-242,
+// matching.cpp:119-142), evaluated before any launch.
+std::vector<LevelPlan> plan_bundle(const fmvs_view* views, int n, const fmvs_config& cfg) {
+    fmvs::validate_config(cfg);
+    if (n < 3 || n % 2 == 0)
+        fmvs::fail_input("estimate: bundle must hold an odd number (>= 3) of views");
+    if (!views)
+        fmvs::fail_input("estimate: no views");
+    for (int i = 0; i < n; ++i)
+        fmvs::validate_view(views[i]);
+    const int ref = n / 2;
+    const int L = cfg.pyramid_levels;
+    const fmvs::V3 normal = v3(cfg.sweep_normal);
+
+    std::vector<LevelPlan> lv(L);
+    for (int l = 0; l < L; ++l) {
+        lv[l].intr.resize(n);
+        for (int k = 0; k < n; ++k)
+            lv[l].intr[k] = l == 0 ? views[k].intrinsics : fmvs::halved(lv[l - 1].intr[k]);
+        lv[l].w = lv[l].intr[ref].width;
+        lv[l].h = lv[l].intr[ref].height;
+    }
+    for (int l = L - 1; l >= 0; --l) {
+        LevelPlan& P = lv[l];
+        std::vector<fmvs::Camera> cams(n);
+        for (int k = 0; k < n; ++k)
+            cams[k] = fmvs::camera_of(P.intr[k], views[k].pose);
+        double dmin = 0, dmax = 0;
+        fmvs::bounding_distances(cfg.d_min, cfg.d_max, normal, P.intr[ref], &dmin, &dmax);
+        int far_view = ref == 0 ? 1 : 0;
+        double far_dist = -1.0;
+        for (int k = 0; k < n; ++k) {
+            if (k == ref)
+                continue;
+            const double dist = fmvs::norm(fmvs::sub(cams[k].center, cams[ref].center));
+            if (dist > far_dist) {
+                far_dist = dist;
+                far_view = k;
+            }
+        }
+        const int cap = l == L - 1 ? cfg.max_planes : std::numeric_limits<int>::max();
+        P.planes = fmvs::plane_distances(cams[ref], cams[far_view], dmin, dmax, normal, cap);
+        if (l < L - 1 && cfg.range_kind == FMVS_RANGE_SPACING_MULTIPLE && lv[l + 1].planes.size() < 2)
+            fmvs::fail_config("refine range: spacing policy needs the coarser plane stack");
+        if (P.planes.size() > 65535)
+            fmvs::fail_config("b200: more than 65535 sweep planes in one level is unsupported");
+        // sweep_cost_volume checks (matching.cpp:126-142)
+        for (size_t i = 1; i < P.planes.size(); ++i)
+            if (!(P.planes[i] < P.planes[i - 1]))
+                fmvs::fail_input("sweep: plane distances must be strictly decreasing");
+        std::vector<fmvs::V3> centers;
+        for (int k = 0; k < n; ++k)
+            centers.push_back(fmvs::mul(cams[ref].rot, fmvs::sub(cams[k].center, cams[ref].center)));
+        fmvs::require_centers_in_front(normal, P.planes.back(), centers);
+        const int np = static_cast<int>(P.planes.size());
+        P.homs.resize(static_cast<size_t>(n - 1) * np * 9);
+        int m = 0;
+        for (int k = 0; k < n; ++k) {
+            if (k == ref)
+                continue;
+            for (int i = 0; i < np; ++i) {
+                const fmvs::M3 H = fmvs::plane_homography(normal, P.planes[i], cams[ref], cams[k]);
+                double* o = &P.homs[(static_cast<size_t>(m) * np + i) * 9];
+                for (int r = 0; r < 3; ++r)
+                    for (int c = 0; c < 3; ++c)
+                        o[3 * r + c] = H.a[r][c];
+            }
+            ++m;
+        }
+    }
+    fmvs_sgm_config sc = cfg.sgm;
+    sc.penalty_scale = n / 2;
+    fmvs::validate_sgm(sc);
+    return lv;
+}
+
+}  // namespace
+
+struct fmvs_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t staged = nullptr;   // plan upload finished reading the pinned blob
+    HostBuf pinned_plan;
+    HostBuf pinned_stats;
+    std::map<std::string, std::unique_ptr<DevBuf>> bufs;
+    std::vector<fmvs_level_stats> stats;
+    int64_t launches = 0;
+    // optional per-stage CUDA-event timing (bench.py roofline numbers)
+    bool timing = false;
+    struct Span {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Span> spans;
+    std::vector<cudaEvent_t> event_pool;
+    std::vector<std::string> stage_names;
+    std::vector<double> stage_ms;
+    std::vector<int64_t> stage_calls;
+
+    cudaEvent_t event() {
+        if (!event_pool.empty()) {
+            cudaEvent_t e = event_pool.back();
+            event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        FMVS_CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+    int stage_id(const char* name) {
+        for (size_t i = 0; i < stage_names.size(); ++i)
+            if (stage_names[i] == name)
+                return static_cast<int>(i);
+        stage_names.push_back(name);
+        stage_ms.push_back(0.0);
+        stage_calls.push_back(0);
+        return static_cast<int>(stage_names.size() - 1);
+    }
+    // Runs launch() bracketed by events on the context stream when timing.
+    template <typename F>
+    void timed(const char* name, F&& launch) {
+        if (!timing) {
+            launch();
+            return;
+        }
+        Span sp{stage_id(name), event(), event()};
+        FMVS_CUDA_CHECK(cudaEventRecord(sp.a, stream));
+        launch();
+        FMVS_CUDA_CHECK(cudaEventRecord(sp.b, stream));
+        spans.push_back(sp);
+    }
+    // After a stream synchronisation: fold finished spans into the totals.
+    void collect() {
+        for (const Span& sp : spans) {
+            float ms = 0.0f;
+            FMVS_CUDA_CHECK(cudaEventElapsedTime(&ms, sp.a, sp.b));
+            stage_ms[sp.stage] += ms;
+            stage_calls[sp.stage] += 1;
+            event_pool.push_back(sp.a);
+            event_pool.push_back(sp.b);
+        }
+        spans.clear();
+    }
+
+    DevBuf& buf(const std::string& name) {
+        auto& b = bufs[name];
+        if (!b)
+            b = std::make_unique<DevBuf>();
+        return *b;
+    }
+    void use() { FMVS_CUDA_CHECK(cudaSetDevice(device)); }
+};
+
+namespace {
+
+// The per-bundle device pipeline. d_images[k] are level-0 device images;
+// outputs are device pointers of the reference view's level-0 maps.
+void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config& cfg,
+                const uint8_t* const* d_images, float* d_depth, float* d_normals, float* d_conf) {
+    std::vector<LevelPlan> lv = plan_bundle(views, n, cfg);
+    const int L = cfg.pyramid_levels;
+    const int ref = n / 2;
+    const int nmatch = n - 1;
+    cudaStream_t s = ctx->stream;
+    int64_t launches = 0;
+
+    // ---- plan blob: per level planes + homs, LUTs, quad pointers ----------
+    const fmvs_sgm_config sgm_base = cfg.sgm;
+    fmvs_sgm_config sc = sgm_base;
+    sc.penalty_scale = n / 2;  // pipeline.cpp:252-253
+    const std::vector<long long> phi2 = fmvs::phi2_table(sc);
+    const int census_bits = cfg.cost.window_w * cfg.cost.window_h - 1;
+    const std::vector<uint16_t> clut = fmvs::census_cost_table(census_bits);
+    const std::vector<double> swt = fmvs::smoothing_table(cfg.normal_smoothing_radius);
+    double k3[3];
+    fmvs::blur3_kernel(k3);
+
+    size_t nd = 0;  // doubles
+    for (auto& P : lv) {
+        P.off_planes = nd;
+        nd += P.planes.size();
+        P.off_homs = nd;
+        nd += P.homs.size();
+    }
+    const size_t off_swt = nd;
+    nd += swt.size();
+    const size_t off_phi2 = nd;  // long long, same width as double
+    nd += 256;
+    size_t img_bytes = 0, quad_words = 0;
+    for (auto& P : lv) {
+        P.img_off = img_bytes;
+        P.quad_off = quad_words;
+        size_t px = 0;
+        for (int k2 = 0; k2 < n; ++k2)
+            px += static_cast<size_t>(P.intr[k2].width) * P.intr[k2].height;
+        img_bytes += px;
+        quad_words += px;
+    }
+    const size_t off_ptrs = nd;  // quad pointers (per level, nmatch), as 8-byte words
+    nd += static_cast<size_t>(L) * nmatch;
+    const size_t off_sizes = nd;  // int2 per level/match (8 bytes)
+    nd += static_cast<size_t>(L) * nmatch;
+    const size_t off_clut = nd;
+    nd += (clut.size() * 2 + 7) / 8;
+
+    double* d_blob = ctx->buf("plan").as<double>(nd);
+    uint8_t* d_img = ctx->buf("images").as<uint8_t>(img_bytes);
+    uint32_t* d_quad = ctx->buf("quads").as<uint32_t>(quad_words);
+
+    FMVS_CUDA_CHECK(cudaEventSynchronize(ctx->staged));
+    double* h_blob = static_cast<double*>(ctx->pinned_plan.get(nd * sizeof(double)));
+    for (auto& P : lv) {
+        std::memcpy(h_blob + P.off_planes, P.planes.data(), P.planes.size() * 8);
+        std::memcpy(h_blob + P.off_homs, P.homs.data(), P.homs.size() * 8);
+    }
+    std::memcpy(h_blob + off_swt, swt.data(), swt.size() * 8);
+    std::memcpy(h_blob + off_phi2, phi2.data(), 256 * 8);
+    std::memcpy(h_blob + off_clut, clut.data(), clut.size() * 2);
+    std::vector<const uint8_t*> img_ptr(static_cast<size_t>(L) * n);
+    for (int l = 0; l < L; ++l) {
+        size_t o = lv[l].img_off, q = lv[l].quad_off;
+        int m = 0;
+        for (int k2 = 0; k2 < n; ++k2) {
+            const size_t px = static_cast<size_t>(lv[l].intr[k2].width) * lv[l].intr[k2].height;
+            img_ptr[l * n + k2] = l == 0 ? d_images[k2] : d_img + o;
+            if (k2 != ref) {
+                const uint32_t* qp = d_quad + q;
+                std::memcpy(h_blob + off_ptrs + l * nmatch + m, &qp, 8);
+                const int2 sz = make_int2(lv[l].intr[k2].width, lv[l].intr[k2].height);
+                std::memcpy(h_blob + off_sizes + l * nmatch + m, &sz, 8);
+                ++m;
+            }
+            o += px;
+            q += px;
+        }
+    }
+    FMVS_CUDA_CHECK(cudaMemcpyAsync(d_blob, h_blob, nd * sizeof(double), cudaMemcpyHostToDevice, s));
+    FMVS_CUDA_CHECK(cudaEventRecord(ctx->staged, s));
+    const long long* d_phi2 = reinterpret_cast<const long long*>(d_blob + off_phi2);
+    const double* d_swt = d_blob + off_swt;
+    const uint16_t* d_clut = reinterpret_cast<const uint16_t*>(d_blob + off_clut);
+
+    // ---- K1: pyramid + quads ------------------------------------------------
+    for (int l = 1; l < L; ++l)
+        for (int k2 = 0; k2 < n; ++k2) {
+            const fmvs_intrinsics& a = lv[l - 1].intr[k2];
+            const fmvs_intrinsics& b = lv[l].intr[k2];
+            ctx->timed("pyramid", [&] {
+                k::blur_halve(img_ptr[(l - 1) * n + k2], a.width, a.height,
+                              const_cast<uint8_t*>(img_ptr[l * n + k2]), b.width, b.height, k3, s);
+            });
+            ++launches;
+        }
+    for (int l = 0; l < L; ++l) {
+        size_t q = lv[l].quad_off;
+        for (int k2 = 0; k2 < n; ++k2) {
+            const fmvs_intrinsics& a = lv[l].intr[k2];
+            if (k2 != ref) {
+                ctx->timed("quads", [&] { k::pack_quads(img_ptr[l * n + k2], a.width, a.height, d_quad + q, s); });
+                ++launches;
+            }
+            q += static_cast<size_t>(a.width) * a.height;
+        }
+    }
+
+    // ---- per-level buffers ---------------------------------------------------
+    size_t max_px = 0, max_entries = 0;
+    int max_h = 0, max_p = 0;
+    for (auto& P : lv) {
+        const size_t px = static_cast<size_t>(P.w) * P.h;
+        max_px = std::max(max_px, px);
+        max_entries = std::max(max_entries, px * P.planes.size());
+        max_h = std::max(max_h, P.h);
+        max_p = std::max(max_p, static_cast<int>(P.planes.size()));
+    }
+    auto* meta = ctx->buf("meta").as<fmvs::dev::VolMeta>(max_px);
+    auto* row_total = ctx->buf("row_total").as<uint32_t>(max_h);
+    auto* row_base = ctx->buf("row_base").as<uint64_t>(static_cast<size_t>(L) * (max_h + 1));
+    auto* costs = ctx->buf("costs").as<uint16_t>(max_entries);
+    auto* agg = ctx->buf("agg").as<uint32_t>(max_entries);
+    auto* offs = ctx->buf("offsets").as<int16_t>(4 * max_px);
+    auto* depth_raw = ctx->buf("depth_raw").as<float>(max_px);
+    auto* nraw = ctx->buf("normals_raw").as<float>(3 * max_px);
+    size_t lvl_px = 0;
+    for (auto& P : lv)
+        lvl_px += static_cast<size_t>(P.w) * P.h;
+    float* depth_all = ctx->buf("depth_levels").as<float>(lvl_px);
+    float* normals_all = ctx->buf("normal_levels").as<float>(3 * lvl_px);
+    std::vector<float*> depth_l(L), normals_l(L);
+    {
+        size_t o = 0;
+        for (int l = 0; l < L; ++l) {
+            depth_l[l] = depth_all + o;
+            normals_l[l] = normals_all + 3 * o;
+            o += static_cast<size_t>(lv[l].w) * lv[l].h;
+        }
+        depth_l[0] = d_depth;
+        normals_l[0] = d_normals;
+    }
+    int pmax_smem_limit = (200 * 1024) / (4 * 2 * 4);
+    uint32_t* sgm_scratch = nullptr;
+    if (max_p > pmax_smem_limit) {
+        size_t lines = 0;
+        for (auto& P : lv)
+            lines = std::max(lines, static_cast<size_t>(4 * (P.w + P.h) + 4 * (P.w + P.h - 1)));
+        sgm_scratch = ctx->buf("sgm_scratch").as<uint32_t>(lines * 2 * max_p);
+    }
+
+    const double cos_rho = std::cos(60.0 * M_PI / 180.0);
+    const double pdv = (cfg.sweep_normal[0] * 0.0 + cfg.sweep_normal[1] * 0.0) +
+                       cfg.sweep_normal[2] * -1.0;
+    const double nx = cfg.sweep_normal[0], ny = cfg.sweep_normal[1], nz = cfg.sweep_normal[2];
+
+    ctx->stats.assign(L, fmvs_level_stats{});
+    for (int l = L - 1; l >= 0; --l) {
+        const LevelPlan& P = lv[l];
+        const int np = static_cast<int>(P.planes.size());
+        const double* d_planes = d_blob + P.off_planes;
+        const fmvs::dev::Intr intr = intr_of(P.intr[ref]);
+        uint64_t* rb = row_base + static_cast<size_t>(l) * (max_h + 1);
+        const bool have_prior = l < L - 1;
+
+        k::RangeArgs ra{};
+        ra.intr = intr;
+        ra.nx = nx;
+        ra.ny = ny;
+        ra.nz = nz;
+        ra.planes = d_planes;
+        ra.nplanes = np;
+        ra.d_min = cfg.d_min;
+        ra.d_max = cfg.d_max;
+        ra.mode = have_prior ? 1 : 0;
+        if (have_prior) {
+            ra.prior = depth_l[l + 1];
+            ra.prior_w = lv[l + 1].w;
+            ra.prior_h = lv[l + 1].h;
+            ra.policy = cfg.range_kind;
+            ra.policy_value = cfg.range_value;
+            ra.coarser = d_blob + lv[l + 1].off_planes;
+            ra.ncoarser = static_cast<int>(lv[l + 1].planes.size());
+        }
+        ra.meta = meta;
+        ra.row_total = row_total;
+        ctx->timed("range", [&] {
+            k::range_rows(ra, s);
+            k::scan_rows(row_total, P.h, rb, s);
+        });
+        launches += 2;
+
+        k::SweepArgs sa{};
+        sa.w = P.w;
+        sa.h = P.h;
+        sa.ref_img = img_ptr[l * n + ref];
+        sa.nmatch = nmatch;
+        sa.quads = reinterpret_cast<const uint32_t* const*>(d_blob + off_ptrs + l * nmatch);
+        sa.sizes = reinterpret_cast<const int2*>(d_blob + off_sizes + l * nmatch);
+        sa.homs = d_blob + P.off_homs;
+        sa.nplanes = np;
+        sa.nleft = ref;
+        sa.meta = meta;
+        sa.row_base = rb;
+        sa.costs = costs;
+        sa.agg_zero = agg;
+        sa.kind = cfg.cost.kind;
+        sa.ww = cfg.cost.window_w;
+        sa.wh = cfg.cost.window_h;
+        sa.census_lut = d_clut;
+        ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { k::sweep(sa, s); });
+        ++launches;
+
+        int variant = cfg.sgm.variant;
+        if (variant == FMVS_SGM_SURFACE_NORMAL && !have_prior)
+            variant = FMVS_SGM_PLANE;  // pipeline.cpp:254-255
+        if (variant == FMVS_SGM_SURFACE_NORMAL) {
+            k::OffsetArgs oa{};
+            oa.intr = intr;
+            oa.w = P.w;
+            oa.h = P.h;
+            oa.prior_depth = depth_l[l + 1];
+            oa.prior_normals = normals_l[l + 1];
+            oa.prior_w = lv[l + 1].w;
+            oa.prior_h = lv[l + 1].h;
+            oa.nx = nx;
+            oa.ny = ny;
+            oa.nz = nz;
+            oa.planes = d_planes;
+            oa.nplanes = np;
+            oa.out = offs;
+            ctx->timed("offsets", [&] { k::normal_offsets(oa, s); });
+            ++launches;
+        }
+
+        k::SgmArgs ga{};
+        ga.w = P.w;
+        ga.h = P.h;
+        ga.meta = meta;
+        ga.row_base = rb;
+        ga.costs = costs;
+        ga.agg = agg;
+        ga.image = img_ptr[l * n + ref];
+        ga.variant = variant;
+        ga.phi1 = std::llround(sc.phi1 * sc.penalty_scale);
+        ga.phi2_lut = d_phi2;
+        ga.offsets = variant == FMVS_SGM_SURFACE_NORMAL ? offs : nullptr;
+        ga.intr = intr;
+        ga.nx = nx;
+        ga.ny = ny;
+        ga.nz = nz;
+        ga.planes = d_planes;
+        ga.nplanes = np;
+        static const int kDirs[8][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1},
+                                        {1, 1}, {-1, -1}, {1, -1}, {-1, 1}};
+        ga.ndirs = cfg.sgm.paths == 8 ? 8 : 4;
+        for (int d = 0; d < 8; ++d) {
+            ga.dirs[d][0] = kDirs[d][0];
+            ga.dirs[d][1] = kDirs[d][1];
+        }
+        ga.pmax = np;
+        ga.scratch = np > pmax_smem_limit ? sgm_scratch : nullptr;
+        ctx->timed(l == 0 ? "sgm_l0" : "sgm", [&] { k::sgm(ga, s); });
+        ++launches;
+
+        k::WtaArgs wa{};
+        wa.w = P.w;
+        wa.h = P.h;
+        wa.meta = meta;
+        wa.row_base = rb;
+        wa.agg = agg;
+        wa.depth = depth_raw;
+        wa.intr = intr;
+        wa.nx = nx;
+        wa.ny = ny;
+        wa.nz = nz;
+        wa.planes = d_planes;
+        wa.nplanes = np;
+        ctx->timed("wta", [&] { k::wta_depth(wa, s); });
+        ctx->timed("median", [&] { k::median5(depth_raw, P.w, P.h, depth_l[l], s); });
+        launches += 2;
+
+        // Normals are consumed only by SN below level 0 and by the result at
+        // level 0 (pipeline.cpp:292-306); confidence only at level 0.
+        const bool need_normals = l == 0 || cfg.sgm.variant == FMVS_SGM_SURFACE_NORMAL;
+        if (need_normals) {
+            ctx->timed("normals", [&] { k::normals_raw(depth_l[l], P.w, P.h, intr, nraw, s); });
+            ctx->timed("smooth_conf", [&] {
+                k::smooth_conf(nraw, img_ptr[l * n + ref], P.w, P.h, cfg.normal_smoothing_radius,
+                               d_swt, normals_l[l], l == 0 ? d_conf : nullptr, cos_rho, pdv, nx, ny,
+                               nz, s);
+            });
+            launches += 2;
+        }
+        ctx->stats[l] = fmvs_level_stats{P.w, P.h, np, 0};
+    }
+    // entry totals per level (read back after the caller synchronises)
+    auto* h_stats = static_cast<uint64_t*>(ctx->pinned_stats.get(sizeof(uint64_t) * L));
+    for (int l = 0; l < L; ++l)
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(h_stats + l, row_base + static_cast<size_t>(l) * (max_h + 1) + lv[l].h,
+                                        sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    ctx->launches = launches;
+}
+
+void finish_stats(fmvs_ctx* ctx) {
+    auto* h = static_cast<uint64_t*>(ctx->pinned_stats.ptr);
+    if (!h)
+        return;
+    for (size_t l = 0; l < ctx->stats.size(); ++l)
+        ctx->stats[l].entries = h[l];
+}
+
+void copy_views_to_device(fmvs_ctx* ctx, const fmvs_view* views, int n,
+                          std::vector<const uint8_t*>* d_images) {
+    size_t total = 0;
+    for (int k2 = 0; k2 < n; ++k2)
+        total += static_cast<size_t>(views[k2].intrinsics.width) * views[k2].intrinsics.height;
+    uint8_t* d = ctx->buf("input_images").as<uint8_t>(total);
+    d_images->resize(n);
+    size_t o = 0;
+    for (int k2 = 0; k2 < n; ++k2) {
+        const size_t px = static_cast<size_t>(views[k2].intrinsics.width) * views[k2].intrinsics.height;
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(d + o, views[k2].image, px, cudaMemcpyHostToDevice, ctx->stream));
+        (*d_images)[k2] = d + o;
+        o += px;
+    }
+}
+
+// Converts the reference ragged layout (first, count, offset) to meta +
+// row bases; offsets must be the exclusive prefix sum of counts.
+void host_layout(int w, int h, const int32_t* first, const int32_t* count, const uint64_t* offset,
+                 uint64_t total, std::vector<fmvs::dev::VolMeta>* meta, std::vector<uint64_t>* rb) {
+    meta->resize(static_cast<size_t>(w) * h);
+    rb->resize(h + 1);
+    uint64_t run = 0;
+    for (int y = 0; y < h; ++y) {
+        const size_t row = static_cast<size_t>(y) * w;
+        (*rb)[y] = w > 0 ? offset[row] : run;
+        for (int x = 0; x < w; ++x) {
+            const size_t p = row + x;
+            if (offset[p] != run)
+                fmvs::fail_input("b200 layout: offsets must be the prefix sum of counts");
+            if (first[p] < 0 || first[p] > 65535 || count[p] < 0 || count[p] > 65535)
+                fmvs::fail_input("b200 layout: first/count out of the supported range");
+            (*meta)[p] = fmvs::dev::VolMeta{static_cast<uint32_t>(offset[p] - (*rb)[y]),
+                                            static_cast<uint32_t>(first[p]) |
+                                                (static_cast<uint32_t>(count[p]) << 16)};
+            run += static_cast<uint64_t>(count[p]);
+        }
+    }
+    (*rb)[h] = run;
+    if (run != total)
+        fmvs::fail_input("b200 layout: counts do not sum to the cost count");
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+
+extern "C" {
+
+int32_t fmvs_abi_version(void) { return FMVS_ABI_VERSION; }
+
+const char* fmvs_last_error(void) { return g_last_error.c_str(); }
+
+void fmvs_config_default(fmvs_config* c, double d_min, double d_max) {
+    c->bundle_size = 5;
+    c->pyramid_levels = 3;
+    c->d_min = d_min;
+    c->d_max = d_max;
+    c->sweep_normal[0] = 0;
+    c->sweep_normal[1] = 0;
+    c->sweep_normal[2] = -1;
+    c->range_kind = FMVS_RANGE_SPACING_MULTIPLE;
+    c->range_value = 3.0;
+    c->max_planes = 256;
+    c->sgm = {FMVS_SGM_PLANE, 8, 100.0, 1, 0.0, 8.0, 10.0, 1};
+    c->cost = {FMVS_COST_NCC, 5, 5};
+    c->normal_smoothing_radius = 2;
+}
+
+int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
+    return guarded([&] {
+        if (!out)
+            fmvs::fail_input("ctx: null output");
+        auto ctx = std::make_unique<fmvs_ctx>();
+        ctx->device = device;
+        ctx->use();
+        FMVS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        FMVS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->staged, cudaEventDisableTiming));
+        FMVS_CUDA_CHECK(cudaEventRecord(ctx->staged, ctx->stream));
+        *out = ctx.release();
+    });
+}
+
+void fmvs_ctx_destroy(fmvs_ctx* ctx) {
+    if (!ctx)
+        return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->bufs.clear();
+    for (auto& sp : ctx->spans) {
+        cudaEventDestroy(sp.a);
+        cudaEventDestroy(sp.b);
+    }
+    for (cudaEvent_t e : ctx->event_pool)
+        cudaEventDestroy(e);
+    cudaEventDestroy(ctx->staged);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int fmvs_ctx_synchronize(fmvs_ctx* ctx) {
+    return guarded([&] {
+        ctx->use();
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        finish_stats(ctx);
+        ctx->collect();
+    });
+}
+
+void fmvs_ctx_set_timing(fmvs_ctx* ctx, int32_t enable) { ctx->timing = enable != 0; }
+
+int32_t fmvs_ctx_stage_count(fmvs_ctx* ctx) { return static_cast<int32_t>(ctx->stage_names.size()); }
+
+const char* fmvs_ctx_stage_name(fmvs_ctx* ctx, int32_t i) {
+    return i >= 0 && i < static_cast<int32_t>(ctx->stage_names.size()) ? ctx->stage_names[i].c_str() : "";
+}
+
+int fmvs_ctx_stage_time(fmvs_ctx* ctx, int32_t i, double* ms, int64_t* calls) {
+    if (i < 0 || i >= static_cast<int32_t>(ctx->stage_names.size()))
+        return FMVS_ERR_INVALID_INPUT;
+    *ms = ctx->stage_ms[i];
+    *calls = ctx->stage_calls[i];
+    return FMVS_OK;
+}
+
+void fmvs_ctx_stage_reset(fmvs_ctx* ctx) {
+    std::fill(ctx->stage_ms.begin(), ctx->stage_ms.end(), 0.0);
+    std::fill(ctx->stage_calls.begin(), ctx->stage_calls.end(), 0);
+}
+
+int32_t fmvs_ctx_level_stats(fmvs_ctx* ctx, fmvs_level_stats* out, int32_t capacity) {
+    const int32_t n = std::min<int32_t>(capacity, static_cast<int32_t>(ctx->stats.size()));
+    for (int32_t i = 0; i < n; ++i)
+        out[i] = ctx->stats[i];
+    return n;
+}
+
+int64_t fmvs_ctx_last_launch_count(fmvs_ctx* ctx) { return ctx->launches; }
+
+void* fmvs_ctx_stream(fmvs_ctx* ctx) { return ctx->stream; }
+
+void* fmvs_host_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess)
+        return nullptr;
+    return p;
+}
+
+void fmvs_host_free(void* p) {
+    if (p)
+        cudaFreeHost(p);
+}
+
+int fmvs_estimate_bundle(fmvs_ctx* ctx, const fmvs_view* views, int32_t n, const fmvs_config* cfg,
+                         float* depth, float* normals_xyz, float* confidence) {
+    return guarded([&] {
+        ctx->use();
+        if (!cfg)
+            fmvs::fail_config("estimate: null config");
+        fmvs::validate_config(*cfg);
+        if (n < 3 || n % 2 == 0)
+            fmvs::fail_input("estimate: bundle must hold an odd number (>= 3) of views");
+        for (int i = 0; i < n; ++i)
+            fmvs::validate_view(views[i]);
+        std::vector<const uint8_t*> d_images;
+        copy_views_to_device(ctx, views, n, &d_images);
+        const fmvs_intrinsics& k0 = views[n / 2].intrinsics;
+        const size_t px = static_cast<size_t>(k0.width) * k0.height;
+        float* d_out = ctx->buf("host_out").as<float>(5 * px);
+        run_bundle(ctx, views, n, *cfg, d_images.data(), d_out, d_out + px, d_out + 4 * px);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(depth, d_out, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(normals_xyz, d_out + px, 3 * px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(confidence, d_out + 4 * px, px * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        finish_stats(ctx);
+        ctx->collect();
+    });
+}
+
+int fmvs_estimate_bundle_device(fmvs_ctx* ctx, const fmvs_view* views, int32_t n,
+                                const fmvs_config* cfg, float* d_depth, float* d_normals_xyz,
+                                float* d_confidence) {
+    return guarded([&] {
+        ctx->use();
+        if (!cfg)
+            fmvs::fail_config("estimate: null config");
+        std::vector<const uint8_t*> d_images(std::max(n, 0));
+        for (int i = 0; i < n; ++i)
+            d_images[i] = views[i].image;
+        run_bundle(ctx, views, n, *cfg, d_images.data(), d_depth, d_normals_xyz, d_confidence);
+    });
+}
+
+// -------------------------------------------------------- host geometry --
+
+int fmvs_plane_homography(const double normal[3], double distance, const fmvs_intrinsics* ri,
+                          const fmvs_pose* rp, const fmvs_intrinsics* oi, const fmvs_pose* op,
+                          double out_h[9]) {
+    return guarded([&] {
+        const fmvs::M3 H = fmvs::plane_homography(v3(normal), distance, fmvs::camera_of(*ri, *rp),
+                                                  fmvs::camera_of(*oi, *op));
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)
+                out_h[3 * r + c] = H.a[r][c];
+    });
+}
+
+int fmvs_bounding_distances(double d_min, double d_max, const double normal[3],
+                            const fmvs_intrinsics* ri, double* lo, double* hi) {
+    return guarded([&] { fmvs::bounding_distances(d_min, d_max, v3(normal), *ri, lo, hi); });
+}
+
+int fmvs_plane_distances(const fmvs_intrinsics* ri, const fmvs_pose* rp, const fmvs_intrinsics* oi,
+                         const fmvs_pose* op, double delta_min, double delta_max,
+                         const double normal[3], int32_t max_planes, double* out, int32_t capacity,
+                         int32_t* count) {
+    int rc = guarded([&] {
+        const std::vector<double> d =
+            fmvs::plane_distances(fmvs::camera_of(*ri, *rp), fmvs::camera_of(*oi, *op), delta_min,
+                                  delta_max, v3(normal), max_planes);
+        *count = static_cast<int32_t>(d.size());
+        for (int i = 0; i < static_cast<int>(d.size()) && i < capacity; ++i)
+            out[i] = d[i];
+    });
+    if (rc == FMVS_OK && *count > capacity) {
+        g_last_error = "plane distances: output capacity too small";
+        return FMVS_ERR_CAPACITY;
+    }
+    return rc;
+}
+
+double fmvs_depth_from_plane(double x, double y, const double normal[3], double distance,
+                             const fmvs_intrinsics* intr) {
+    return fmvs::depth_from_plane(x, y, v3(normal), distance, *intr);
+}
+
+double fmvs_adaptive_phi2(double phi1, double alpha, double beta, double di) {
+    return fmvs::adaptive_phi2(phi1, alpha, beta, di);
+}
+
+int fmvs_parabola_refine(double a, double b, double c, double ca, double cb, double cc,
+                         double* out) {
+    return guarded([&] { *out = fmvs::parabola_refine(a, b, c, ca, cb, cc); });
+}
+
+// --------------------------------------------------------- device stages --
+
+int fmvs_build_pyramids(fmvs_ctx* ctx, const fmvs_view* views, int32_t n, int32_t levels,
+                        uint8_t* out_images, uint64_t capacity, fmvs_intrinsics* out_intr) {
+    return guarded([&] {
+        ctx->use();
+        if (levels < 1)
+            fmvs::fail_config("pyramids: need at least one level");
+        for (int i = 0; i < n; ++i)
+            fmvs::validate_view(views[i]);
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        std::vector<fmvs_intrinsics> intr(static_cast<size_t>(levels) * n);
+        std::vector<uint8_t*> d(static_cast<size_t>(levels) * n);
+        uint64_t need = 0;
+        for (int l = 0; l < levels; ++l)
+            for (int k2 = 0; k2 < n; ++k2) {
+                intr[l * n + k2] = l == 0 ? views[k2].intrinsics : fmvs::halved(intr[(l - 1) * n + k2]);
+                const size_t px = static_cast<size_t>(intr[l * n + k2].width) * intr[l * n + k2].height;
+                need += px;
+                d[l * n + k2] = l == 0 ? t.upload(views[k2].image, px, s) : t.alloc<uint8_t>(px);
+            }
+        if (need > capacity)
+            throw fmvs::Error(FMVS_ERR_CAPACITY, "pyramids: output capacity too small");
+        double k3[3];
+        fmvs::blur3_kernel(k3);
+        for (int l = 1; l < levels; ++l)
+            for (int k2 = 0; k2 < n; ++k2) {
+                const auto& a = intr[(l - 1) * n + k2];
+                const auto& b = intr[l * n + k2];
+                k::blur_halve(d[(l - 1) * n + k2], a.width, a.height, d[l * n + k2], b.width,
+                              b.height, k3, s);
+            }
+        uint64_t pos = 0;
+        for (int l = 0; l < levels; ++l)
+            for (int k2 = 0; k2 < n; ++k2) {
+                const size_t px = static_cast<size_t>(intr[l * n + k2].width) * intr[l * n + k2].height;
+                FMVS_CUDA_CHECK(cudaMemcpyAsync(out_images + pos, d[l * n + k2], px, cudaMemcpyDeviceToHost, s));
+                pos += px;
+                out_intr[l * n + k2] = intr[l * n + k2];
+            }
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_refine_range(fmvs_ctx* ctx, const float* prior, int32_t w, int32_t h, int32_t kind,
+                      double value, double d_min, double d_max, const fmvs_plane_stack* coarser,
+                      const fmvs_intrinsics* intr, float* lo, float* hi) {
+    return guarded([&] {
+        ctx->use();
+        fmvs::validate_depth_bounds(d_min, d_max);
+        if (kind == FMVS_RANGE_SPACING_MULTIPLE && (!coarser || !intr || coarser->count < 2))
+            fmvs::fail_config("refine range: spacing policy needs the coarser plane stack");
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        k::RangeArgs ra{};
+        fmvs_intrinsics k0 = intr ? *intr : fmvs_intrinsics{1, 1, 0, 0, w, h};
+        k0.width = w;
+        k0.height = h;
+        ra.intr = intr_of(k0);
+        ra.nx = coarser ? coarser->normal[0] : 0;
+        ra.ny = coarser ? coarser->normal[1] : 0;
+        ra.nz = coarser ? coarser->normal[2] : -1;
+        const double one = 1.0;
+        ra.planes = t.upload(&one, 1, s);
+        ra.nplanes = 1;
+        ra.mode = 1;
+        ra.d_min = d_min;
+        ra.d_max = d_max;
+        ra.prior = t.upload(prior, px, s);
+        ra.prior_w = w;
+        ra.prior_h = h;
+        ra.policy = kind;
+        ra.policy_value = value;
+        if (coarser) {
+            ra.coarser = t.upload(coarser->distances, coarser->count, s);
+            ra.ncoarser = coarser->count;
+        }
+        ra.lo_out = t.alloc<float>(px);
+        ra.hi_out = t.alloc<float>(px);
+        ra.meta = t.alloc<fmvs::dev::VolMeta>(px);
+        ra.row_total = t.alloc<uint32_t>(h);
+        k::range_rows(ra, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(lo, ra.lo_out, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(hi, ra.hi_out, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_sweep_cost_volume(fmvs_ctx* ctx, const fmvs_view* views, int32_t n, int32_t ref_index,
+                           const fmvs_plane_stack* planes, const float* lo, const float* hi,
+                           const fmvs_cost_spec* cost, int32_t* first, int32_t* count,
+                           uint64_t* offset, uint16_t* costs, uint64_t capacity, uint64_t* total,
+                           int32_t* per_side) {
+    int rc = guarded([&] {
+        ctx->use();
+        fmvs::validate_cost(*cost);  // matching.cpp:119-142
+        if (ref_index < 0 || ref_index >= n)
+            fmvs::fail_input("sweep: reference index out of range");
+        if (ref_index < 1 || ref_index > n - 2)
+            fmvs::fail_input("sweep: need at least one matching image on each side");
+        for (int i = 0; i < n; ++i)
+            fmvs::validate_view(views[i]);
+        if (planes->count < 1)
+            fmvs::fail_input("sweep: empty plane list");
+        for (int i = 1; i < planes->count; ++i)
+            if (!(planes->distances[i] < planes->distances[i - 1]))
+                fmvs::fail_input("sweep: plane distances must be strictly decreasing");
+        if (planes->count > 65535)
+            fmvs::fail_config("b200: more than 65535 sweep planes in one level is unsupported");
+        const fmvs::Camera cref = fmvs::camera_of(views[ref_index]);
+        std::vector<fmvs::V3> centers;
+        for (int k2 = 0; k2 < n; ++k2)
+            centers.push_back(fmvs::mul(cref.rot, fmvs::sub(fmvs::camera_of(views[k2]).center, cref.center)));
+        const fmvs::V3 normal = v3(planes->normal);
+        fmvs::require_centers_in_front(normal, planes->distances[planes->count - 1], centers);
+        *per_side = std::max(ref_index, n - 1 - ref_index);
+
+        const int w = views[ref_index].intrinsics.width, h = views[ref_index].intrinsics.height;
+        const size_t px = static_cast<size_t>(w) * h;
+        const int np = planes->count;
+        std::vector<double> homs(static_cast<size_t>(n - 1) * np * 9);
+        std::vector<const uint32_t*> qptr;
+        std::vector<int2> sizes;
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        int m = 0;
+        for (int k2 = 0; k2 < n; ++k2) {
+            if (k2 == ref_index)
+                continue;
+            const fmvs::Camera ck = fmvs::camera_of(views[k2]);
+            for (int i = 0; i < np; ++i) {
+                const fmvs::M3 H = fmvs::plane_homography(normal, planes->distances[i], cref, ck);
+                for (int r = 0; r < 3; ++r)
+                    for (int c = 0; c < 3; ++c)
+                        homs[(static_cast<size_t>(m) * np + i) * 9 + 3 * r + c] = H.a[r][c];
+            }
+            const int vw = views[k2].intrinsics.width, vh = views[k2].intrinsics.height;
+            const size_t vpx = static_cast<size_t>(vw) * vh;
+            uint8_t* di = t.upload(views[k2].image, vpx, s);
+            uint32_t* dq = t.alloc<uint32_t>(vpx);
+            k::pack_quads(di, vw, vh, dq, s);
+            qptr.push_back(dq);
+            sizes.push_back(make_int2(vw, vh));
+            ++m;
+        }
+        k::RangeArgs ra{};
+        ra.intr = intr_of(views[ref_index].intrinsics);
+        ra.nx = normal.x;
+        ra.ny = normal.y;
+        ra.nz = normal.z;
+        ra.planes = t.upload(planes->distances, np, s);
+        ra.nplanes = np;
+        ra.mode = 2;
+        ra.lo_in = t.upload(lo, px, s);
+        ra.hi_in = t.upload(hi, px, s);
+        ra.meta = t.alloc<fmvs::dev::VolMeta>(px);
+        ra.row_total = t.alloc<uint32_t>(h);
+        k::range_rows(ra, s);
+        uint64_t* rb = t.alloc<uint64_t>(h + 1);
+        k::scan_rows(ra.row_total, h, rb, s);
+        std::vector<uint64_t> h_rb(h + 1);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(h_rb.data(), rb, (h + 1) * 8, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+        *total = h_rb[h];
+        const uint64_t ne = h_rb[h];
+        k::SweepArgs sa{};
+        sa.w = w;
+        sa.h = h;
+        sa.ref_img = t.upload(views[ref_index].image, px, s);
+        sa.nmatch = n - 1;
+        sa.quads = t.upload(qptr.data(), qptr.size(), s);
+        sa.sizes = t.upload(sizes.data(), sizes.size(), s);
+        sa.homs = t.upload(homs.data(), homs.size(), s);
+        sa.nplanes = np;
+        sa.nleft = ref_index;
+        sa.meta = ra.meta;
+        sa.row_base = rb;
+        sa.costs = t.alloc<uint16_t>(ne);
+        sa.kind = cost->kind;
+        sa.ww = cost->window_w;
+        sa.wh = cost->window_h;
+        const std::vector<uint16_t> clut = fmvs::census_cost_table(cost->window_w * cost->window_h - 1);
+        sa.census_lut = t.upload(clut.data(), clut.size(), s);
+        k::sweep(sa, s);
+        std::vector<fmvs::dev::VolMeta> meta(px);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(meta.data(), ra.meta, px * 8, cudaMemcpyDeviceToHost, s));
+        if (ne <= capacity && ne > 0)
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(costs, sa.costs, ne * 2, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                const size_t p = static_cast<size_t>(y) * w + x;
+                first[p] = static_cast<int32_t>(meta[p].fc & 0xFFFFu);
+                count[p] = static_cast<int32_t>(meta[p].fc >> 16);
+                offset[p] = h_rb[y] + meta[p].rel;
+            }
+    });
+    if (rc == FMVS_OK && *total > capacity) {
+        g_last_error = "sweep: cost capacity too small";
+        return FMVS_ERR_CAPACITY;
+    }
+    return rc;
+}
+
+int fmvs_compute_normal_offsets(fmvs_ctx* ctx, const float* prior_normals_xyz,
+                                const float* prior_depth, int32_t w, int32_t h,
+                                const fmvs_plane_stack* planes, const fmvs_intrinsics* intr,
+                                int16_t* out) {
+    return guarded([&] {
+        ctx->use();
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        k::OffsetArgs oa{};
+        fmvs_intrinsics k0 = *intr;
+        oa.intr = intr_of(k0);
+        oa.w = w;
+        oa.h = h;
+        oa.prior_depth = t.upload(prior_depth, px, s);
+        oa.prior_normals = t.upload(prior_normals_xyz, 3 * px, s);
+        oa.prior_w = w;
+        oa.prior_h = h;
+        oa.nx = planes->normal[0];
+        oa.ny = planes->normal[1];
+        oa.nz = planes->normal[2];
+        oa.planes = t.upload(planes->distances, planes->count, s);
+        oa.nplanes = planes->count;
+        oa.out = t.alloc<int16_t>(4 * px);
+        k::normal_offsets(oa, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out, oa.out, px * 8, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* planes,
+                   const int32_t* first, const int32_t* count, const uint64_t* offset,
+                   const uint16_t* costs, uint64_t total, const uint8_t* image,
+                   const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
+                   const float* prior_normals_xyz, const float* prior_depth, int32_t dir_x,
+                   int32_t dir_y, uint32_t* out_values) {
+    return guarded([&] {
+        ctx->use();
+        fmvs::validate_sgm(*cfg);  // check_aggregate_inputs, sgm.cpp:241-248
+        if (cfg->variant == FMVS_SGM_SURFACE_NORMAL && (!prior_normals_xyz || !prior_depth))
+            fmvs::fail_config("sgm: surface-normal variant requires a prior normal and depth map");
+        static const int kDirs[8][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1},
+                                        {1, 1}, {-1, -1}, {1, -1}, {-1, 1}};
+        k::SgmArgs ga{};
+        if (dir_x == 0 && dir_y == 0) {
+            ga.ndirs = cfg->paths == 8 ? 8 : 4;
+            for (int d = 0; d < 8; ++d) {
+                ga.dirs[d][0] = kDirs[d][0];
+                ga.dirs[d][1] = kDirs[d][1];
+            }
+        } else {
+            if (dir_x < -1 || dir_x > 1 || dir_y < -1 || dir_y > 1)
+                fmvs::fail_config("sgm: unsupported path direction");
+            ga.ndirs = 1;
+            ga.dirs[0][0] = dir_x;
+            ga.dirs[0][1] = dir_y;
+        }
+        std::vector<fmvs::dev::VolMeta> meta;
+        std::vector<uint64_t> rb;
+        host_layout(w, h, first, count, offset, total, &meta, &rb);
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        int pmax = 1;
+        for (size_t p = 0; p < px; ++p)
+            pmax = std::max(pmax, static_cast<int>(count[p]));
+        ga.w = w;
+        ga.h = h;
+        ga.meta = t.upload(meta.data(), px, s);
+        ga.row_base = t.upload(rb.data(), rb.size(), s);
+        ga.costs = t.upload(costs, total, s);
+        ga.agg = t.alloc<uint32_t>(total);
+        FMVS_CUDA_CHECK(cudaMemsetAsync(ga.agg, 0, std::max<uint64_t>(total, 1) * 4, s));
+        ga.image = t.upload(image, px, s);
+        ga.variant = cfg->variant;
+        ga.phi1 = std::llround(cfg->phi1 * cfg->penalty_scale);
+        const std::vector<long long> lut = fmvs::phi2_table(*cfg);
+        ga.phi2_lut = t.upload(lut.data(), lut.size(), s);
+        ga.intr = intr_of(*intr);
+        ga.nx = planes->normal[0];
+        ga.ny = planes->normal[1];
+        ga.nz = planes->normal[2];
+        ga.planes = t.upload(planes->distances, planes->count, s);
+        ga.nplanes = planes->count;
+        if (cfg->variant == FMVS_SGM_SURFACE_NORMAL) {
+            k::OffsetArgs oa{};
+            oa.intr = ga.intr;
+            oa.w = w;
+            oa.h = h;
+            oa.prior_depth = t.upload(prior_depth, px, s);
+            oa.prior_normals = t.upload(prior_normals_xyz, 3 * px, s);
+            oa.prior_w = w;
+            oa.prior_h = h;
+            oa.nx = ga.nx;
+            oa.ny = ga.ny;
+            oa.nz = ga.nz;
+            oa.planes = ga.planes;
+            oa.nplanes = ga.nplanes;
+            oa.out = t.alloc<int16_t>(4 * px);
+            k::normal_offsets(oa, s);
+            ga.offsets = oa.out;
+        }
+        ga.pmax = pmax;
+        const int limit = (200 * 1024) / (4 * 2 * 4);
+        if (pmax > limit) {
+            const size_t lines = 8 * static_cast<size_t>(w + h);
+            ga.scratch = t.alloc<uint32_t>(lines * 2 * pmax);
+        }
+        if (total > 0)
+            k::sgm(ga, s);
+        if (total > 0)
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(out_values, ga.agg, total * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_wta(fmvs_ctx* ctx, int32_t w, int32_t h, const int32_t* first, const int32_t* count,
+             const uint64_t* offset, const uint32_t* values, uint64_t total, int32_t* winners) {
+    return guarded([&] {
+        ctx->use();
+        std::vector<fmvs::dev::VolMeta> meta;
+        std::vector<uint64_t> rb;
+        host_layout(w, h, first, count, offset, total, &meta, &rb);
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        k::WtaArgs wa{};
+        wa.w = w;
+        wa.h = h;
+        wa.meta = t.upload(meta.data(), px, s);
+        wa.row_base = t.upload(rb.data(), rb.size(), s);
+        wa.agg = t.upload(values, total, s);
+        wa.winners = t.alloc<int32_t>(px);
+        if (px > 0)
+            k::wta_depth(wa, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(winners, wa.winners, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_median_filter_5x5(fmvs_ctx* ctx, const float* depth, int32_t w, int32_t h, float* out) {
+    return guarded([&] {
+        ctx->use();
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        const float* din = t.upload(depth, px, s);
+        float* dout = t.alloc<float>(px);
+        if (px > 0)
+            k::median5(din, w, h, dout, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out, dout, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_normals_from_depth(fmvs_ctx* ctx, const float* depth, int32_t w, int32_t h,
+                            const fmvs_intrinsics* intr, float* out_xyz) {
+    return guarded([&] {
+        ctx->use();
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        const float* din = t.upload(depth, px, s);
+        float* dout = t.alloc<float>(3 * px);
+        if (px > 0)
+            k::normals_raw(din, w, h, intr_of(*intr), dout, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out_xyz, dout, 3 * px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_smooth_normals(fmvs_ctx* ctx, const float* raw_xyz, const uint8_t* image, int32_t w,
+                        int32_t h, int32_t radius, float* out_xyz) {
+    return guarded([&] {
+        ctx->use();
+        if (radius < 1)  // surface.cpp:42-45
+            fmvs::fail_config("smooth normals: radius must be at least 1");
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        const std::vector<double> wt = fmvs::smoothing_table(radius);
+        const float* din = t.upload(raw_xyz, 3 * px, s);
+        const uint8_t* dimg = t.upload(image, px, s);
+        const double* dwt = t.upload(wt.data(), wt.size(), s);
+        float* dout = t.alloc<float>(3 * px);
+        if (px > 0)
+            k::smooth_conf(din, dimg, w, h, radius, dwt, dout, nullptr, 0, 0, 0, 0, 0, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out_xyz, dout, 3 * px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_confidence_map(fmvs_ctx* ctx, const float* normals_xyz, int32_t w, int32_t h,
+                        const double sweep_normal[3], double rho_degrees, float* out) {
+    return guarded([&] {
+        ctx->use();
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        const double cos_rho = std::cos(rho_degrees * M_PI / 180.0);  // surface.cpp:85-87
+        const double pdv = (sweep_normal[0] * 0.0 + sweep_normal[1] * 0.0) + sweep_normal[2] * -1.0;
+        const float* din = t.upload(normals_xyz, 3 * px, s);
+        float* dout = t.alloc<float>(px);
+        if (px > 0)
+            k::confidence(din, w, h, cos_rho, pdv, sweep_normal[0], sweep_normal[1], sweep_normal[2],
+                          dout, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out, dout, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_upscale_nearest(fmvs_ctx* ctx, const float* in, int32_t iw, int32_t ih, int32_t ch,
+                         int32_t ow, int32_t oh, float* out) {
+    return guarded([&] {
+        ctx->use();
+        if (ow == iw && oh == ih) {  // identity (pipeline.cpp:93-94)
+            std::memcpy(out, in, sizeof(float) * ch * static_cast<size_t>(iw) * ih);
+            return;
+        }
+        if ((iw + 1) / 2 > ow || (ih + 1) / 2 > oh)
+            fmvs::fail_input("upscale: target smaller than the source level");
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const float* din = t.upload(in, static_cast<size_t>(ch) * iw * ih, s);
+        float* dout = t.alloc<float>(static_cast<size_t>(ch) * ow * oh);
+        k::upscale(din, iw, ih, ch, dout, ow, oh, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out, dout, sizeof(float) * ch * static_cast<size_t>(ow) * oh,
+                                        cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_render_plane_scene(fmvs_ctx* ctx, int32_t kind, int32_t w, int32_t h, double focal,
+                            double depth, double tilt_deg, int32_t n_views, double step,
+                            uint64_t seed, double texture_scale, uint8_t* images, float* gt_depth,
+                            float* gt_normals_xyz, fmvs_intrinsics* intr, fmvs_pose* poses) {
+    return guarded([&] {
+        ctx->use();
+        // base_scene / fronto_scene / slanted_scene (render.cpp:143-183)
+        const fmvs_intrinsics k0{focal, focal, (w - 1) / 2.0, (h - 1) / 2.0, w, h};
+        fmvs::validate_intrinsics(k0);
+        if (n_views < 1)
+            fmvs::fail_input("render: scene needs at least one plane and one pose");
+        if (!(texture_scale > 0.0))
+            fmvs::fail_input("render: texture scale must be positive");
+        fmvs::V3 pn{0, 0, -1};
+        if (kind == 1) {
+            const double rad = tilt_deg * M_PI / 180.0;
+            pn = {0.0, -std::sin(rad), -std::cos(rad)};
+        }
+        // PlaneFrame (render.cpp:64-72)
+        const double len = fmvs::norm(pn);
+        fmvs::V3 fn = pn;
+        if (fmvs::dot(pn, pn) > 0.0)
+            fn = fmvs::divs(pn, len);
+        const fmvs::V3 u0{1, 0, 0};
+        const fmvs::V3 ur = fmvs::sub(u0, fmvs::scale(fmvs::dot(u0, fn), fn));
+        fmvs::V3 fu = ur;
+        if (fmvs::dot(ur, ur) > 0.0)
+            fu = fmvs::divs(ur, fmvs::norm(ur));
+        const fmvs::V3 fv = fmvs::cross(fn, fu);
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const size_t px = static_cast<size_t>(w) * h;
+        uint8_t* dimg = t.alloc<uint8_t>(px * n_views);
+        float* dd = gt_depth ? t.alloc<float>(px * n_views) : nullptr;
+        float* dn = gt_normals_xyz ? t.alloc<float>(3 * px * n_views) : nullptr;
+        for (int v = 0; v < n_views; ++v) {
+            fmvs_pose pose{};
+            pose.rotation[0] = pose.rotation[4] = pose.rotation[8] = 1.0;
+            pose.center[0] = (v - (n_views - 1) / 2.0) * step;  // lateral_trajectory
+            k::RenderArgs ra{};
+            ra.w = w;
+            ra.h = h;
+            ra.intr = intr_of(k0);
+            std::memcpy(ra.rot, pose.rotation, sizeof(ra.rot));
+            std::memcpy(ra.center, pose.center, sizeof(ra.center));
+            ra.pn[0] = fn.x;
+            ra.pn[1] = fn.y;
+            ra.pn[2] = fn.z;
+            ra.pp[0] = 0;
+            ra.pp[1] = 0;
+            ra.pp[2] = depth;
+            ra.pu[0] = fu.x;
+            ra.pu[1] = fu.y;
+            ra.pu[2] = fu.z;
+            ra.pv[0] = fv.x;
+            ra.pv[1] = fv.y;
+            ra.pv[2] = fv.z;
+            ra.texture_scale = texture_scale;
+            ra.seed = seed;
+            ra.image = dimg + v * px;
+            ra.gt_depth = dd ? dd + v * px : nullptr;
+            ra.gt_normals = dn ? dn + 3 * v * px : nullptr;
+            k::render_plane(ra, s);
+            if (intr)
+                intr[v] = k0;
+            if (poses)
+                poses[v] = pose;
+        }
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(images, dimg, px * n_views, cudaMemcpyDeviceToHost, s));
+        if (dd)
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(gt_depth, dd, 4 * px * n_views, cudaMemcpyDeviceToHost, s));
+        if (dn)
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(gt_normals_xyz, dn, 12 * px * n_views, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+// K7-K9: per-pixel map kernels of the level tail (pipeline.cpp:260-301):
+// winner-take-all + depth conversion + parabola refinement, the valid-only
+// 5x5 median, central-difference normals, appearance-weighted normal
+// smoothing with the geometric confidence fused in, and NN upscaling.
+// All FP64 expression trees follow the cited reference lines; exp() is
+// replaced by host-computed tables (bit-identical by construction).
+// Roofline: HBM-bound map traffic (a few bytes per pixel in and out).
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace fmvs {
+namespace k {
+
+namespace {
+
+__device__ __forceinline__ double depth_from_plane_dev(double denom, double dist) {
+    using namespace dev;  // geometry.cpp:299-306 with the per-pixel denominator
+    if (fabs(denom) < 1e-12)
+        return 0.0;
+    const double d = div(-dist, denom);
+    return d > 0.0 ? d : 0.0;
+}
+
+__device__ double parabola_dev(double d_prev, double d_win, double d_next, double c_prev,
+                               double c_win, double c_next) {
+    using namespace dev;  // sgm.cpp:351-363 (callers guarantee d_prev < d_win < d_next)
+    const double num = add(add(mul(sub(mul(d_win, d_win), mul(d_next, d_next)), c_prev),
+                               mul(sub(mul(d_next, d_next), mul(d_prev, d_prev)), c_win)),
+                           mul(sub(mul(d_prev, d_prev), mul(d_win, d_win)), c_next));
+    const double den = add(add(mul(sub(d_win, d_next), c_prev), mul(sub(d_next, d_prev), c_win)),
+                           mul(sub(d_prev, d_win), c_next));
+    double m = fabs(c_prev);
+    if (m < fabs(c_win))
+        m = fabs(c_win);
+    if (m < fabs(c_next))
+        m = fabs(c_next);
+    if (m < 1.0)
+        m = 1.0;
+    if (fabs(den) < mul(1e-12, m))
+        return d_win;
+    const double v = div(mul(0.5, num), den);
+    return v < d_prev ? d_prev : (d_next < v ? d_next : v);
+}
+
+__global__ void wta_depth_kernel(WtaArgs a) {
+    using namespace dev;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= a.w)
+        return;
+    const size_t p = static_cast<size_t>(y) * a.w + x;
+    const VolMeta m = a.meta[p];
+    const int f = meta_first(m.fc), c = meta_count(m.fc);
+    if (c == 0) {
+        if (a.winners)
+            a.winners[p] = -1;
+        if (a.depth)
+            a.depth[p] = 0.0f;
+        return;
+    }
+    const uint32_t* v = a.agg + a.row_base[y] + m.rel;
+    int best = 0;
+    uint32_t bv = v[0];
+    for (int i = 1; i < c; ++i) {
+        const uint32_t vi = v[i];
+        if (vi < bv) {
+            bv = vi;
+            best = i;
+        }
+    }
+    const int win = f + best;
+    if (a.winners)
+        a.winners[p] = win;
+    if (!a.depth)
+        return;
+    // pipeline.cpp:263-288
+    const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject(a.intr, double(x), double(y)));
+    const double d_win = depth_from_plane_dev(denom, a.planes[win]);
+    float out = 0.0f;
+    if (d_win > 0.0) {
+        double d = d_win;
+        if (win - 1 >= f && win + 1 < f + c) {
+            const double d_lo = depth_from_plane_dev(denom, a.planes[win + 1]);
+            const double d_hi = depth_from_plane_dev(denom, a.planes[win - 1]);
+            if (d_lo > 0.0 && d_hi > 0.0 && d_lo < d_win && d_win < d_hi)
+                d = parabola_dev(d_lo, d_win, d_hi, double(v[best + 1]), double(v[best]),
+                                 double(v[best - 1]));
+        }
+        out = __double2float_rn(d);
+    }
+    a.depth[p] = out;
+}
+
+// median_filter_5x5 (pipeline.cpp:175-198): element valid/2 of the sorted
+// valid window, by exact rank selection (no sort).
+__global__ void median5_kernel(const float* __restrict__ in, int w, int h,
+                               float* __restrict__ out) {
+    using namespace dev;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    float win[25];
+    int in_image = 0, valid = 0;
+#pragma unroll
+    for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll
+        for (int dx = -2; dx <= 2; ++dx) {
+            const int xx = x + dx, yy = y + dy;
+            if (xx < 0 || yy < 0 || xx >= w || yy >= h)
+                continue;
+            ++in_image;
+            const float d = __ldg(in + static_cast<size_t>(yy) * w + xx);
+            if (depth_ok(d))
+                win[valid++] = d;
+        }
+    float res = 0.0f;
+    if (!(2 * valid < in_image)) {
+        const int k = valid / 2;
+        for (int i = 0; i < valid; ++i) {
+            int less = 0, leq = 0;
+            for (int j = 0; j < valid; ++j) {
+                less += win[j] < win[i];
+                leq += win[j] <= win[i];
+            }
+            if (less <= k && k < leq) {
+                res = win[i];
+                break;
+            }
+        }
+    }
+    out[static_cast<size_t>(y) * w + x] = res;
+}
+
+// normals_from_depth (surface.cpp:9-39)
+__global__ void normals_raw_kernel(const float* __restrict__ depth, int w, int h, dev::Intr k,
+                                   float* __restrict__ out) {
+    using namespace dev;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    const size_t p = static_cast<size_t>(y) * w + x;
+    float3 r = make_float3(0.0f, 0.0f, 0.0f);
+    if (x >= 1 && y >= 1 && x < w - 1 && y < h - 1) {
+        const float dc = depth[p];
+        const float dl = depth[p - 1], dr = depth[p + 1];
+        const float du = depth[p - w], dd = depth[p + w];
+        if (depth_ok(dc) && depth_ok(dl) && depth_ok(dr) && depth_ok(du) && depth_ok(dd)) {
+            const D3 pr = scale3(double(dr), unproject(k, double(x + 1), double(y)));
+            const D3 pl = scale3(double(dl), unproject(k, double(x - 1), double(y)));
+            const D3 pd = scale3(double(dd), unproject(k, double(x), double(y + 1)));
+            const D3 pu = scale3(double(du), unproject(k, double(x), double(y - 1)));
+            const D3 hv = sub3(pr, pl);
+            const D3 vv = sub3(pd, pu);
+            D3 n = cross3(hv, vv);
+            const double len = norm3(n);
+            if (!(len < 1e-15)) {
+                n = {div(n.x, len), div(n.y, len), div(n.z, len)};
+                if (n.z > 0.0)
+                    n = {-n.x, -n.y, -n.z};
+                r = make_float3(__double2float_rn(n.x), __double2float_rn(n.y),
+                                __double2float_rn(n.z));
+            }
+        }
+    }
+    out[3 * p] = r.x;
+    out[3 * p + 1] = r.y;
+    out[3 * p + 2] = r.z;
+}
+
+__device__ __forceinline__ float conf_of(float nx, float ny, float nz, double cos_rho,
+                                         double pdv, double sx, double sy, double sz) {
+    using namespace dev;  // confidence_map (surface.cpp:83-104)
+    if (!normal_ok(nx, ny, nz))
+        return 0.0f;
+    const double ndp = dot3(D3{double(nx), double(ny), double(nz)}, D3{sx, sy, sz});
+    if (ndp < cos_rho || pdv < cos_rho)
+        return 0.0f;
+    double score = div(sub(mul(ndp, pdv), cos_rho), sub(1.0, cos_rho));
+    score = score < 0.0 ? 0.0 : (1.0 < score ? 1.0 : score);
+    return __double2float_rn(score);
+}
+
+// smooth_normals (surface.cpp:41-81) + confidence_map of the smoothed normal.
+__global__ void smooth_conf_kernel(const float* __restrict__ raw, const uint8_t* __restrict__ img,
+                                   int w, int h, int radius, const double* __restrict__ wt,
+                                   float* __restrict__ out, float* __restrict__ conf,
+                                   double cos_rho, double pdv, double sx, double sy, double sz) {
+    using namespace dev;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    const size_t p = static_cast<size_t>(y) * w + x;
+    const float cx = raw[3 * p], cy = raw[3 * p + 1], cz = raw[3 * p + 2];
+    float ox = 0.0f, oy = 0.0f, oz = 0.0f;
+    if (normal_ok(cx, cy, cz)) {
+        double sx_ = double(cx), sy_ = double(cy), sz_ = double(cz);
+        const int ic = img[p];
+        for (int dy = -radius; dy <= radius; ++dy)
+            for (int dx = -radius; dx <= radius; ++dx) {
+                if (dx == 0 && dy == 0)
+                    continue;
+                const int qx = x + dx, qy = y + dy;
+                if (qx < 0 || qy < 0 || qx >= w || qy >= h)
+                    continue;
+                const size_t q = static_cast<size_t>(qy) * w + qx;
+                const float nx = raw[3 * q], ny = raw[3 * q + 1], nz = raw[3 * q + 2];
+                if (!normal_ok(nx, ny, nz))
+                    continue;
+                const int di = abs(int(img[q]) - ic);
+                const double wq = __ldg(wt + (dx * dx + dy * dy) * 256 + di);
+                sx_ = add(sx_, mul(wq, double(nx)));
+                sy_ = add(sy_, mul(wq, double(ny)));
+                sz_ = add(sz_, mul(wq, double(nz)));
+            }
+        const double len = norm3(D3{sx_, sy_, sz_});
+        if (len > 1e-15) {
+            ox = __double2float_rn(div(sx_, len));
+            oy = __double2float_rn(div(sy_, len));
+            oz = __double2float_rn(div(sz_, len));
+        } else {
+            ox = cx;
+            oy = cy;
+            oz = cz;
+        }
+    }
+    out[3 * p] = ox;
+    out[3 * p + 1] = oy;
+    out[3 * p + 2] = oz;
+    if (conf)
+        conf[p] = conf_of(ox, oy, oz, cos_rho, pdv, sx, sy, sz);
+}
+
+__global__ void confidence_kernel(const float* __restrict__ n, int w, int h, double cos_rho,
+                                  double pdv, double sx, double sy, double sz,
+                                  float* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    const size_t p = static_cast<size_t>(y) * w + x;
+    out[p] = conf_of(n[3 * p], n[3 * p + 1], n[3 * p + 2], cos_rho, pdv, sx, sy, sz);
+}
+
+__global__ void upscale_kernel(const float* __restrict__ in, int iw, int ih, int ch,
+                               float* __restrict__ out, int ow, int oh) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= ow || y >= oh)
+        return;
+    const int sx = min(x / 2, iw - 1), sy = min(y / 2, ih - 1);  // pipeline.cpp:97-101
+    const size_t s = static_cast<size_t>(sy) * iw + sx, d = static_cast<size_t>(y) * ow + x;
+    for (int c = 0; c < ch; ++c)
+        out[ch * d + c] = in[ch * s + c];
+}
+
+inline dim3 grid2(int w, int h) { return dim3((w + 31) / 32, (h + 7) / 8); }
+
+}  // namespace
+
+void wta_depth(const WtaArgs& a, cudaStream_t s) {
+    wta_depth_kernel<<<dim3((a.w + 127) / 128, a.h), 128, 0, s>>>(a);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void median5(const float* in, int w, int h, float* out, cudaStream_t s) {
+    median5_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(in, w, h, out);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void normals_raw(const float* depth, int w, int h, dev::Intr intr, float* out_xyz,
+                 cudaStream_t s) {
+    normals_raw_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(depth, w, h, intr, out_xyz);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void smooth_conf(const float* raw_xyz, const uint8_t* img, int w, int h, int radius,
+                 const double* weights, float* out_xyz, float* conf, double cos_rho,
+                 double plane_dot_view, double nx, double ny, double nz, cudaStream_t s) {
+    smooth_conf_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(raw_xyz, img, w, h, radius, weights,
+                                                            out_xyz, conf, cos_rho,
+                                                            plane_dot_view, nx, ny, nz);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void confidence(const float* normals_xyz, int w, int h, double cos_rho, double plane_dot_view,
+                double nx, double ny, double nz, float* out, cudaStream_t s) {
+    confidence_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(normals_xyz, w, h, cos_rho,
+                                                           plane_dot_view, nx, ny, nz, out);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void upscale(const float* in, int iw, int ih, int ch, float* out, int ow, int oh,
+             cudaStream_t s) {
+    upscale_kernel<<<grid2(ow, oh), dim3(32, 8), 0, s>>>(in, iw, ih, ch, out, ow, oh);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace k
+}  // namespace fmvs

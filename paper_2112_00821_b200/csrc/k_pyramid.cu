@@ -1,0 +1,94 @@
+// K1: image pyramid (blur_and_halve, pipeline.cpp:79-89 over gaussian_blur,
+// pipeline.cpp:32-75) and the quad-packed sampling images for the sweep.
+//
+// blur_and_halve only keeps the blurred image at even (2x, 2y), so each
+// output pixel evaluates the three horizontal passes it needs (rows 2y-1..2y+1,
+// column 2x, each stored as float like the reference's tmp raster) and the
+// vertical pass, all in the reference's FP64 accumulation order
+// (acc = 0; acc += k[i] * v for i = -1..1), then lround -> clamp -> u8.
+// HBM-bound: 4 B read (L1/L2 reuse) + 1 B written per output pixel.
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace fmvs {
+namespace k {
+
+namespace {
+
+__device__ __forceinline__ int reflect(int i, int n) {  // pipeline.cpp:44-54
+    if (n == 1)
+        return 0;
+    while (i < 0 || i >= n) {
+        if (i < 0)
+            i = -i;
+        if (i >= n)
+            i = 2 * (n - 1) - i;
+    }
+    return i;
+}
+
+__global__ void blur_halve_kernel(const uint8_t* __restrict__ in, int win, int hin,
+                                  uint8_t* __restrict__ out, int wout, int hout, double k0,
+                                  double k1, double k2) {
+    using namespace dev;
+    const double c_k3[3] = {k0, k1, k2};
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= wout || y >= hout)
+        return;
+    const int X = 2 * x, Y = 2 * y;
+    const int xm = reflect(X - 1, win), xp = reflect(X + 1, win);
+    float tmp[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const int yy = reflect(Y + j - 1, hin);
+        const uint8_t* row = in + static_cast<size_t>(yy) * win;
+        double acc = 0.0;
+        acc = add(acc, mul(c_k3[0], double(__ldg(row + xm))));
+        acc = add(acc, mul(c_k3[1], double(__ldg(row + X))));
+        acc = add(acc, mul(c_k3[2], double(__ldg(row + xp))));
+        tmp[j] = __double2float_rn(acc);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+        acc = add(acc, mul(c_k3[j], double(tmp[j])));
+    const float blurred = __double2float_rn(acc);
+    long v = lroundf(blurred);
+    v = v < 0 ? 0 : (v > 255 ? 255 : v);
+    out[static_cast<size_t>(y) * wout + x] = static_cast<uint8_t>(v);
+}
+
+__global__ void pack_quads_kernel(const uint8_t* __restrict__ img, int w, int h,
+                                  uint32_t* __restrict__ quad) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    const int x1 = min(x + 1, w - 1), y1 = min(y + 1, h - 1);
+    const uint8_t* r0 = img + static_cast<size_t>(y) * w;
+    const uint8_t* r1 = img + static_cast<size_t>(y1) * w;
+    quad[static_cast<size_t>(y) * w + x] = uint32_t(__ldg(r0 + x)) | (uint32_t(__ldg(r0 + x1)) << 8) |
+                                           (uint32_t(__ldg(r1 + x)) << 16) |
+                                           (uint32_t(__ldg(r1 + x1)) << 24);
+}
+
+}  // namespace
+
+void blur_halve(const uint8_t* in, int win, int hin, uint8_t* out, int wout, int hout,
+                const double k3[3], cudaStream_t s) {
+    const dim3 block(32, 8);
+    const dim3 grid((wout + 31) / 32, (hout + 7) / 8);
+    blur_halve_kernel<<<grid, block, 0, s>>>(in, win, hin, out, wout, hout, k3[0], k3[1], k3[2]);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void pack_quads(const uint8_t* img, int w, int h, uint32_t* quad, cudaStream_t s) {
+    const dim3 block(32, 8);
+    const dim3 grid((w + 31) / 32, (h + 7) / 8);
+    pack_quads_kernel<<<grid, block, 0, s>>>(img, w, h, quad);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace k
+}  // namespace fmvs

@@ -1,0 +1,181 @@
+// K3: per-pixel sampling range, plane interval and the ragged-volume layout.
+//
+// One CTA per image row. Each pixel evaluates
+//   - its sampling range: uniform (SamplingRange::uniform, matching.cpp:20-26)
+//     or refine_range of the upscaled prior (pipeline.cpp:136-173, with the
+//     nearest-neighbour upscale of pipeline.cpp:91-103 folded into the read),
+//     stored as float exactly like the reference's Raster<float>;
+//   - its plane interval [first, last] (plane_interval, matching.cpp:95-107),
+//     found by two binary searches instead of the reference's linear scans
+//     (valid because scale*delta_i is monotone in i under round-to-nearest);
+// then the row's counts are exclusive-scanned into row-relative offsets.
+// scan_rows turns the per-row totals into 64-bit row bases, so the whole
+// layout is produced on device with no host synchronisation.
+#include <cub/block/block_scan.cuh>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace fmvs {
+namespace k {
+
+namespace {
+
+constexpr int kRangeThreads = 256;
+
+__device__ __forceinline__ void pixel_range(const RangeArgs& a, int x, int y, float* lo_f,
+                                            float* hi_f) {
+    using namespace dev;
+    float lo = __double2float_rn(a.d_min);
+    float hi = __double2float_rn(a.d_max);
+    if (a.mode == 2) {
+        const size_t p = static_cast<size_t>(y) * a.intr.w + x;
+        lo = a.lo_in[p];
+        hi = a.hi_in[p];
+    } else if (a.mode == 1 && a.policy != FMVS_RANGE_FULL) {
+        int sx = x, sy = y;
+        if (!(a.prior_w == a.intr.w && a.prior_h == a.intr.h)) {
+            sx = min(x / 2, a.prior_w - 1);
+            sy = min(y / 2, a.prior_h - 1);
+        }
+        const float d = a.prior[static_cast<size_t>(sy) * a.prior_w + sx];
+        if (depth_ok(d)) {
+            double dd = a.policy_value;
+            bool keep = true;
+            if (a.policy == FMVS_RANGE_SPACING_MULTIPLE) {
+                const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject(a.intr, double(x), double(y)));
+                if (fabs(denom) < 1e-12) {
+                    keep = false;
+                } else {
+                    const double scale = div(-1.0, denom);
+                    if (scale <= 0.0) {
+                        keep = false;
+                    } else {
+                        const int i = dev::nearest_index(a.coarser, a.ncoarser, div(double(d), scale));
+                        const int j = min(i, a.ncoarser - 2);
+                        const double gap = sub(a.coarser[j], a.coarser[j + 1]);
+                        dd = mul(mul(a.policy_value, scale), gap);
+                    }
+                }
+            }
+            if (keep) {
+                const double lo_d = sub(double(d), dd);
+                const double hi_d = add(double(d), dd);
+                lo = __double2float_rn(a.d_min < lo_d ? lo_d : a.d_min);   // std::max
+                hi = __double2float_rn(hi_d < a.d_max ? hi_d : a.d_max);   // std::min
+            }
+        }
+    }
+    *lo_f = lo;
+    *hi_f = hi;
+}
+
+__global__ void __launch_bounds__(kRangeThreads) range_rows_kernel(RangeArgs a) {
+    using namespace dev;
+    using Scan = cub::BlockScan<uint32_t, kRangeThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ uint32_t carry;
+    const int y = blockIdx.x;
+    const int w = a.intr.w;
+    if (threadIdx.x == 0)
+        carry = 0;
+    __syncthreads();
+    for (int x0 = 0; x0 < w; x0 += kRangeThreads) {
+        const int x = x0 + threadIdx.x;
+        uint32_t first = 0, count = 0;
+        if (x < w) {
+            float lo, hi;
+            pixel_range(a, x, y, &lo, &hi);
+            const size_t p = static_cast<size_t>(y) * w + x;
+            if (a.lo_out) {
+                a.lo_out[p] = lo;
+                a.hi_out[p] = hi;
+            }
+            // pixel_depth_scale (matching.cpp:84-90)
+            const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject(a.intr, double(x), double(y)));
+            double scale = 0.0;
+            if (!(fabs(denom) < 1e-12)) {
+                const double s = div(-1.0, denom);
+                scale = s > 0.0 ? s : 0.0;
+            }
+            const double lod = double(lo), hid = double(hi);
+            if (scale > 0.0 && lod <= hid) {
+                const int n = a.nplanes;
+                // first = #{i : scale*delta_i > hi} (a prefix)
+                int l = 0, r = n;
+                while (l < r) {
+                    const int m = (l + r) >> 1;
+                    if (mul(scale, __ldg(a.planes + m)) > hid)
+                        l = m + 1;
+                    else
+                        r = m;
+                }
+                const int f = l;
+                // s = first i with scale*delta_i < lo (a suffix)
+                l = 0;
+                r = n;
+                while (l < r) {
+                    const int m = (l + r) >> 1;
+                    if (mul(scale, __ldg(a.planes + m)) < lod)
+                        r = m;
+                    else
+                        l = m + 1;
+                }
+                const int last = max(l - 1, f - 1);
+                first = static_cast<uint32_t>(f);
+                count = static_cast<uint32_t>(max(0, last - f + 1));
+            }
+        }
+        uint32_t excl, agg;
+        Scan(scan_tmp).ExclusiveSum(count, excl, agg);
+        if (x < w) {
+            const size_t p = static_cast<size_t>(y) * w + x;
+            a.meta[p] = VolMeta{carry + excl, first | (count << 16)};
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        a.row_total[y] = carry;
+}
+
+__global__ void __launch_bounds__(1024) scan_rows_kernel(const uint32_t* __restrict__ totals, int h,
+                                                        uint64_t* __restrict__ base) {
+    using Scan = cub::BlockScan<uint64_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0)
+        carry = 0;
+    __syncthreads();
+    for (int y0 = 0; y0 < h; y0 += 1024) {
+        const int y = y0 + threadIdx.x;
+        const uint64_t v = y < h ? totals[y] : 0;
+        uint64_t excl, agg;
+        Scan(tmp).ExclusiveSum(v, excl, agg);
+        if (y < h)
+            base[y] = carry + excl;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        base[h] = carry;
+}
+
+}  // namespace
+
+void range_rows(const RangeArgs& a, cudaStream_t s) {
+    range_rows_kernel<<<a.intr.h, kRangeThreads, 0, s>>>(a);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void scan_rows(const uint32_t* row_total, int h, uint64_t* row_base, cudaStream_t s) {
+    scan_rows_kernel<<<1, 1024, 0, s>>>(row_total, h, row_base);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace k
+}  // namespace fmvs

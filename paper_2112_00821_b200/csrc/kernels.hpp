@@ -1,0 +1,152 @@
+// Host-callable launchers for the sm_100a kernels (one .cu per stage). All
+// launchers enqueue on the given stream and never synchronise; the driver
+// (driver.cpp) owns buffers and ordering.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace fmvs {
+namespace k {
+
+// ---- K1: pyramid (pipeline.cpp:32-126) + quad packing for the sweep ------
+// out(x,y) = clamp(lround(blur3x3(in)(2x,2y))) with reflected borders.
+void blur_halve(const uint8_t* in, int win, int hin, uint8_t* out, int wout, int hout,
+                const double k3[3], cudaStream_t s);
+// quad[p] = I(x0,y0) | I(x1,y0)<<8 | I(x0,y1)<<16 | I(x1,y1)<<24, x1/y1 clamped:
+// the four bilinear taps of raster.hpp:71-84 in one 32-bit load.
+void pack_quads(const uint8_t* img, int w, int h, uint32_t* quad, cudaStream_t s);
+
+// ---- K3: per-pixel sampling range + plane interval + row prefix sums -----
+struct RangeArgs {
+    dev::Intr intr;
+    double nx, ny, nz;           // sweep normal
+    const double* planes;        // current level stack (device)
+    int nplanes;
+    int mode;                    // 0 uniform, 1 refine from prior, 2 explicit lo/hi
+    double d_min, d_max;
+    // mode 1 (refine_range, pipeline.cpp:136-173)
+    const float* prior;          // coarser-level depth (device)
+    int prior_w, prior_h;
+    int policy;                  // FMVS_RANGE_*
+    double policy_value;
+    const double* coarser;       // coarser stack (device)
+    int ncoarser;
+    // mode 2
+    const float* lo_in;
+    const float* hi_in;
+    // optional outputs of refine_range
+    float* lo_out;
+    float* hi_out;
+    // outputs
+    dev::VolMeta* meta;
+    uint32_t* row_total;         // H entries
+};
+void range_rows(const RangeArgs& a, cudaStream_t s);
+// row_base[y] = sum of row_total[0..y), row_base[H] = total entries.
+void scan_rows(const uint32_t* row_total, int h, uint64_t* row_base, cudaStream_t s);
+
+// ---- K4: plane-sweep cost volume (matching.cpp:116-294) ------------------
+struct SweepArgs {
+    int w, h;                        // reference (level) size
+    const uint8_t* ref_img;
+    int nmatch;                      // matching views
+    const uint32_t* const* quads;    // [nmatch] device pointers (device array)
+    const int2* sizes;               // [nmatch] (w, h) (device array)
+    const double* homs;              // [nmatch][nplanes][9] row-major (device)
+    int nplanes;
+    int nleft;                       // matching views left of the reference
+    const dev::VolMeta* meta;
+    const uint64_t* row_base;
+    uint16_t* costs;
+    uint32_t* agg_zero;              // optional: zeroed at the same entries
+    int kind, ww, wh;
+    const uint16_t* census_lut;      // [bits+1]
+};
+void sweep(const SweepArgs& a, cudaStream_t s);
+
+// ---- K5: surface-normal SGM shifts (sgm.cpp:252-299) ---------------------
+struct OffsetArgs {
+    dev::Intr intr;
+    int w, h;
+    const float* prior_depth;        // coarser level (upscaled on the fly) or same size
+    const float* prior_normals;      // xyz
+    int prior_w, prior_h;
+    double nx, ny, nz;
+    const double* planes;
+    int nplanes;
+    int16_t* out;                    // 4 per pixel
+};
+void normal_offsets(const OffsetArgs& a, cudaStream_t s);
+
+// ---- K6: SGM path aggregation (sgm.cpp:91-239) ---------------------------
+struct SgmArgs {
+    int w, h;
+    const dev::VolMeta* meta;
+    const uint64_t* row_base;
+    const uint16_t* costs;
+    uint32_t* agg;
+    const uint8_t* image;
+    int variant;
+    long long phi1;
+    const long long* phi2_lut;       // [256] device
+    const int16_t* offsets;          // SN shifts (4 per pixel) or null
+    // PG (scene points)
+    dev::Intr intr;
+    double nx, ny, nz;
+    const double* planes;
+    int nplanes;
+    int ndirs;
+    int dirs[8][2];
+    int pmax;                        // per-warp path buffer length
+    uint32_t* scratch;               // global path buffers when pmax is too large for smem
+};
+void sgm(const SgmArgs& a, cudaStream_t s);
+
+// ---- K7: WTA + depth + parabola (sgm.cpp:333-363, pipeline.cpp:263-288) ---
+struct WtaArgs {
+    int w, h;
+    const dev::VolMeta* meta;
+    const uint64_t* row_base;
+    const uint32_t* agg;
+    int32_t* winners;                // optional
+    float* depth;                    // optional (needs intr/planes)
+    dev::Intr intr;
+    double nx, ny, nz;
+    const double* planes;
+    int nplanes;
+};
+void wta_depth(const WtaArgs& a, cudaStream_t s);
+
+// ---- K8/K9: per-pixel map kernels -----------------------------------------
+void median5(const float* in, int w, int h, float* out, cudaStream_t s);
+void normals_raw(const float* depth, int w, int h, dev::Intr intr, float* out_xyz,
+                 cudaStream_t s);
+// smooth_normals (+ confidence_map when conf != nullptr)
+void smooth_conf(const float* raw_xyz, const uint8_t* img, int w, int h, int radius,
+                 const double* weights, float* out_xyz, float* conf, double cos_rho,
+                 double plane_dot_view, double nx, double ny, double nz, cudaStream_t s);
+void confidence(const float* normals_xyz, int w, int h, double cos_rho, double plane_dot_view,
+                double nx, double ny, double nz, float* out, cudaStream_t s);
+void upscale(const float* in, int iw, int ih, int ch, float* out, int ow, int oh,
+             cudaStream_t s);
+
+// ---- synthetic input: render_scene for one textured plane ------------------
+struct RenderArgs {
+    int w, h;
+    dev::Intr intr;
+    double rot[9];                   // world -> camera rotation (row-major)
+    double center[3];
+    double pn[3], pp[3], pu[3], pv[3];  // plane frame (normalised on the host)
+    double texture_scale;
+    uint64_t seed;
+    uint8_t* image;
+    float* gt_depth;
+    float* gt_normals;
+};
+void render_plane(const RenderArgs& a, cudaStream_t s);
+
+}  // namespace k
+}  // namespace fmvs

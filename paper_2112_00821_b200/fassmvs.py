@@ -1,0 +1,577 @@
+"""Python mirror of the reference's public API (proj/include/fassmvs/*.hpp)
+over the C ABI (include/fmvs.h).
+
+Same names, argument meaning and error behaviour as the reference:
+``estimate_bundle(bundle, config) -> BundleResult`` (pipeline.hpp:79-80),
+the stage functions (sweep_cost_volume, aggregate, aggregate_single_path, wta,
+compute_normal_offsets, build_pyramids, refine_range, median_filter_5x5,
+normals_from_depth, smooth_normals, confidence_map, upscale_nearest, the
+host geometry helpers) and the three exception types of errors.hpp:10-24.
+
+A :class:`Backend` binds one shared library. ``Backend.b200()`` is the
+product (the in-tree ``_lib/libfmvs.so``, hand-written sm_100a kernels); the
+tests also bind the reference oracle through the same class.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+
+
+# ------------------------------------------------------------ errors ------
+class FassmvsError(RuntimeError):
+    pass
+
+
+class InvalidInputError(FassmvsError):
+    """fassmvs::InvalidInputError (errors.hpp:10-13), CLI exit code 1."""
+
+
+class ConfigError(FassmvsError):
+    """fassmvs::ConfigError (errors.hpp:15-19), CLI exit code 2."""
+
+
+class GeometryError(FassmvsError):
+    """fassmvs::GeometryError (errors.hpp:21-24), CLI exit code 1."""
+
+
+class CudaError(FassmvsError):
+    """Device failure (no reference analogue)."""
+
+
+class CapacityError(FassmvsError):
+    """Output buffer too small (C ABI only)."""
+
+
+_ERRORS = {
+    _abi.FMVS_ERR_INVALID_INPUT: InvalidInputError,
+    _abi.FMVS_ERR_CONFIG: ConfigError,
+    _abi.FMVS_ERR_GEOMETRY: GeometryError,
+    _abi.FMVS_ERR_CUDA: CudaError,
+    _abi.FMVS_ERR_CAPACITY: CapacityError,
+}
+
+
+# ------------------------------------------------------------- types ------
+class CostKind(enum.IntEnum):
+    CensusHamming = 0
+    NccTruncated = 1
+
+
+class SgmVariant(enum.IntEnum):
+    Plane = 0
+    SurfaceNormal = 1
+    PathGradient = 2
+
+
+class RangeKind(enum.IntEnum):
+    Full = 0
+    Fixed = 1
+    SpacingMultiple = 2
+
+
+@dataclass
+class Intrinsics:  # geometry.hpp:19-39
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+
+    def to_c(self) -> _abi.Intrinsics_c:
+        return _abi.Intrinsics_c(self.fx, self.fy, self.cx, self.cy, self.width, self.height)
+
+    @staticmethod
+    def from_c(c: _abi.Intrinsics_c) -> "Intrinsics":
+        return Intrinsics(c.fx, c.fy, c.cx, c.cy, c.width, c.height)
+
+    def halved(self) -> "Intrinsics":  # geometry.cpp:30-39
+        return Intrinsics(self.fx / 2.0, self.fy / 2.0, self.cx / 2.0, self.cy / 2.0,
+                          (self.width + 1) // 2, (self.height + 1) // 2)
+
+
+@dataclass
+class Pose:  # geometry.hpp:44-55
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    center: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def to_c(self) -> _abi.Pose_c:
+        p = _abi.Pose_c()
+        r = np.asarray(self.rotation, dtype=np.float64).reshape(9)
+        c = np.asarray(self.center, dtype=np.float64).reshape(3)
+        for i in range(9):
+            p.rotation[i] = float(r[i])
+        for i in range(3):
+            p.center[i] = float(c[i])
+        return p
+
+    @staticmethod
+    def from_c(c: _abi.Pose_c) -> "Pose":
+        return Pose(np.array(list(c.rotation), dtype=np.float64).reshape(3, 3),
+                    np.array(list(c.center), dtype=np.float64))
+
+
+@dataclass
+class CalibratedView:  # geometry.hpp:57-63
+    image: np.ndarray  # uint8 (height, width)
+    intrinsics: Intrinsics
+    pose: Pose
+
+
+@dataclass
+class PlaneStack:  # geometry.hpp:75-94
+    distances: np.ndarray
+    normal: tuple = (0.0, 0.0, -1.0)
+
+    def count(self) -> int:
+        return int(len(self.distances))
+
+
+@dataclass
+class SgmConfig:  # sgm.hpp:19-32
+    variant: SgmVariant = SgmVariant.Plane
+    paths: int = 8
+    phi1: float = 100.0
+    phi2_adaptive: bool = True
+    phi2_fixed: float = 0.0
+    alpha: float = 8.0
+    beta: float = 10.0
+    penalty_scale: int = 1
+
+    def to_c(self) -> _abi.SgmConfig_c:
+        return _abi.SgmConfig_c(int(self.variant), self.paths, self.phi1, int(bool(self.phi2_adaptive)),
+                                self.phi2_fixed, self.alpha, self.beta, self.penalty_scale)
+
+
+@dataclass
+class CostFunctionSpec:  # matching.hpp:14-23
+    kind: CostKind = CostKind.NccTruncated
+    window_w: int = 5
+    window_h: int = 5
+
+    def to_c(self) -> _abi.CostSpec_c:
+        return _abi.CostSpec_c(int(self.kind), self.window_w, self.window_h)
+
+    def census_bits(self) -> int:
+        return self.window_w * self.window_h - 1
+
+
+@dataclass
+class RangePolicy:  # pipeline.hpp:12-20
+    kind: RangeKind = RangeKind.SpacingMultiple
+    value: float = 3.0
+
+
+@dataclass
+class PipelineConfig:  # pipeline.hpp:22-35
+    d_min: float
+    d_max: float
+    bundle_size: int = 5
+    pyramid_levels: int = 3
+    sweep_normal: tuple = (0.0, 0.0, -1.0)
+    range_policy: RangePolicy = field(default_factory=RangePolicy)
+    max_planes: int = 256
+    sgm: SgmConfig = field(default_factory=SgmConfig)
+    cost: CostFunctionSpec = field(default_factory=CostFunctionSpec)
+    normal_smoothing_radius: int = 2
+
+    def to_c(self) -> _abi.Config_c:
+        c = _abi.Config_c()
+        c.bundle_size = self.bundle_size
+        c.pyramid_levels = self.pyramid_levels
+        c.d_min = self.d_min
+        c.d_max = self.d_max
+        for i in range(3):
+            c.sweep_normal[i] = float(self.sweep_normal[i])
+        c.range_kind = int(self.range_policy.kind)
+        c.range_value = float(self.range_policy.value)
+        c.max_planes = self.max_planes
+        c.sgm = self.sgm.to_c()
+        c.cost = self.cost.to_c()
+        c.normal_smoothing_radius = self.normal_smoothing_radius
+        return c
+
+
+@dataclass
+class BundleResult:  # pipeline.hpp:37-41
+    depth: np.ndarray       # float32 (h, w)
+    normals: np.ndarray     # float32 (h, w, 3)
+    confidence: np.ndarray  # float32 (h, w)
+
+
+@dataclass
+class CostVolume:  # matching.hpp:36-53
+    width: int
+    height: int
+    planes: PlaneStack
+    per_side: int
+    first: np.ndarray   # int32 (h*w)
+    count: np.ndarray   # int32 (h*w)
+    offset: np.ndarray  # uint64 (h*w)
+    costs: np.ndarray   # uint16 (total)
+
+    def pixel_costs(self, x: int, y: int) -> np.ndarray:
+        p = y * self.width + x
+        return self.costs[int(self.offset[p]):int(self.offset[p]) + int(self.count[p])]
+
+
+@dataclass
+class AggregatedVolume:  # sgm.hpp:39-49
+    width: int
+    height: int
+    planes: PlaneStack
+    first: np.ndarray
+    count: np.ndarray
+    offset: np.ndarray
+    values: np.ndarray  # uint32 (total)
+
+
+# ----------------------------------------------------------- helpers ------
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _pd(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _stack_c(planes: PlaneStack):
+    d = np.ascontiguousarray(planes.distances, dtype=np.float64)
+    s = _abi.PlaneStack_c()
+    for i in range(3):
+        s.normal[i] = float(planes.normal[i])
+    s.distances = d.ctypes.data_as(C.c_void_p)
+    s.count = len(d)
+    return s, d
+
+
+def _views_c(bundle: Sequence[CalibratedView]):
+    arr = (_abi.View_c * max(1, len(bundle)))()
+    keep = []
+    for i, v in enumerate(bundle):
+        img = np.ascontiguousarray(v.image, dtype=np.uint8)
+        keep.append(img)
+        arr[i].image = img.ctypes.data_as(C.c_void_p)
+        arr[i].intrinsics = v.intrinsics.to_c()
+        arr[i].pose = v.pose.to_c()
+    return arr, keep
+
+
+def _f32(a, shape=None) -> np.ndarray:
+    out = np.ascontiguousarray(a, dtype=np.float32)
+    if shape is not None:
+        out = out.reshape(shape)
+    return out
+
+
+# ----------------------------------------------------------- backend ------
+class Backend:
+    """One bound library (the B200 product or, in tests, the oracle)."""
+
+    def __init__(self, lib_path: str, prefix: str, device: int = 0, extras: dict | None = None,
+                 needs_context: bool = True):
+        if not os.path.exists(lib_path):
+            raise FileNotFoundError(lib_path)
+        self.path = lib_path
+        self.lib = C.CDLL(lib_path)
+        self.prefix = prefix
+        self.fn = _abi.bind(self.lib, prefix, extras)
+        self.ctx = C.c_void_p()
+        if needs_context:
+            self._check(self.fn["ctx_create"](device, C.byref(self.ctx)))
+
+    _b200_singleton: "Backend | None" = None
+
+    @classmethod
+    def b200(cls, device: int = 0) -> "Backend":
+        """The product library; fails loudly when the CUDA build is missing."""
+        if device == 0 and cls._b200_singleton is not None:
+            return cls._b200_singleton
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfmvs.so")
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"B200 library not built ({path}); run __graft_entry__.build() or "
+                "make -C paper_2112_00821_b200")
+        b = cls(path, "fmvs_", device)
+        if device == 0:
+            cls._b200_singleton = b
+        return b
+
+    def close(self):
+        if self.ctx and "ctx_destroy" in self.fn:
+            self.fn["ctx_destroy"](self.ctx)
+            self.ctx = C.c_void_p()
+
+    # -- plumbing
+    def _check(self, rc: int):
+        if rc != _abi.FMVS_OK:
+            msg = self.fn["last_error"]().decode(errors="replace")
+            raise _ERRORS.get(rc, FassmvsError)(msg)
+
+    def last_error(self) -> str:
+        return self.fn["last_error"]().decode(errors="replace")
+
+    # ------------------------------------------------------------ hot path
+    def estimate_bundle(self, bundle: Sequence[CalibratedView], config: PipelineConfig) -> BundleResult:
+        """estimate_bundle (pipeline.hpp:79-80)."""
+        views, keep = _views_c(bundle)
+        cfg = config.to_c()
+        n = len(bundle)
+        ref = bundle[n // 2] if n else None
+        w = ref.intrinsics.width if ref is not None else 1
+        h = ref.intrinsics.height if ref is not None else 1
+        w, h = max(w, 1), max(h, 1)
+        depth = np.zeros((h, w), np.float32)
+        normals = np.zeros((h, w, 3), np.float32)
+        conf = np.zeros((h, w), np.float32)
+        self._check(self.fn["estimate_bundle"](self.ctx, views, n, C.byref(cfg), _ptr(depth),
+                                               _ptr(normals), _ptr(conf)))
+        del keep
+        return BundleResult(depth, normals, conf)
+
+    def level_stats(self):
+        out = (_abi.LevelStats_c * 16)()
+        n = self.fn["ctx_level_stats"](self.ctx, out, 16)
+        return [dict(width=out[i].width, height=out[i].height, planes=out[i].planes,
+                     entries=int(out[i].entries)) for i in range(n)]
+
+    def last_launch_count(self) -> int:
+        return int(self.fn["ctx_last_launch_count"](self.ctx))
+
+    # ------------------------------------------------------ host geometry
+    def plane_homography(self, normal, distance, ref_intr: Intrinsics, ref_pose: Pose,
+                         other_intr: Intrinsics, other_pose: Pose) -> np.ndarray:
+        n = np.asarray(normal, np.float64)
+        out = np.zeros(9, np.float64)
+        self._check(self.fn["plane_homography"](_pd(n), float(distance), C.byref(ref_intr.to_c()),
+                                                C.byref(ref_pose.to_c()), C.byref(other_intr.to_c()),
+                                                C.byref(other_pose.to_c()), _pd(out)))
+        return out.reshape(3, 3)
+
+    def bounding_distances(self, d_min, d_max, normal, ref_intr: Intrinsics):
+        n = np.asarray(normal, np.float64)
+        lo, hi = C.c_double(), C.c_double()
+        self._check(self.fn["bounding_distances"](d_min, d_max, _pd(n), C.byref(ref_intr.to_c()),
+                                                  C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def plane_distances(self, ref_intr, ref_pose, other_intr, other_pose, delta_min, delta_max,
+                        normal, max_planes) -> np.ndarray:
+        n = np.asarray(normal, np.float64)
+        cap = 4096
+        while True:
+            out = np.zeros(cap, np.float64)
+            cnt = C.c_int32()
+            rc = self.fn["plane_distances"](C.byref(ref_intr.to_c()), C.byref(ref_pose.to_c()),
+                                            C.byref(other_intr.to_c()), C.byref(other_pose.to_c()),
+                                            delta_min, delta_max, _pd(n), max_planes, _pd(out), cap,
+                                            C.byref(cnt))
+            if rc == _abi.FMVS_ERR_CAPACITY:
+                cap = cnt.value
+                continue
+            self._check(rc)
+            return out[:cnt.value].copy()
+
+    def depth_from_plane(self, x, y, normal, distance, intr: Intrinsics) -> float:
+        n = np.asarray(normal, np.float64)
+        return self.fn["depth_from_plane"](x, y, _pd(n), distance, C.byref(intr.to_c()))
+
+    def adaptive_phi2(self, phi1, alpha, beta, di) -> float:
+        return self.fn["adaptive_phi2"](phi1, alpha, beta, di)
+
+    def parabola_refine(self, d_prev, d_win, d_next, c_prev, c_win, c_next) -> float:
+        out = C.c_double()
+        self._check(self.fn["parabola_refine"](d_prev, d_win, d_next, c_prev, c_win, c_next,
+                                               C.byref(out)))
+        return out.value
+
+    # ------------------------------------------------------------ stages
+    def build_pyramids(self, bundle: Sequence[CalibratedView], levels: int):
+        """build_pyramids (pipeline.hpp:50): list of levels of CalibratedView."""
+        views, keep = _views_c(bundle)
+        n = len(bundle)
+        intr = (_abi.Intrinsics_c * max(1, n * max(levels, 1)))()
+        cap = sum(int(v.image.size) for v in bundle) * 2 + 16
+        out = np.zeros(cap, np.uint8)
+        self._check(self.fn["build_pyramids"](self.ctx, views, n, levels, _ptr(out), cap, intr))
+        res, pos = [], 0
+        for l in range(levels):
+            lvl = []
+            for k in range(n):
+                ki = Intrinsics.from_c(intr[l * n + k])
+                px = ki.width * ki.height
+                lvl.append(CalibratedView(out[pos:pos + px].reshape(ki.height, ki.width).copy(), ki,
+                                          bundle[k].pose))
+                pos += px
+            res.append(lvl)
+        del keep
+        return res
+
+    def refine_range(self, prior: np.ndarray, policy: RangePolicy, d_min: float, d_max: float,
+                     coarser: Optional[PlaneStack] = None, intrinsics: Optional[Intrinsics] = None):
+        prior = _f32(prior)
+        h, w = prior.shape
+        lo = np.zeros((h, w), np.float32)
+        hi = np.zeros((h, w), np.float32)
+        st, keep = (_stack_c(coarser) if coarser is not None else (None, None))
+        self._check(self.fn["refine_range"](self.ctx, _ptr(prior), w, h, int(policy.kind), policy.value,
+                                            d_min, d_max, C.byref(st) if st is not None else None,
+                                            C.byref(intrinsics.to_c()) if intrinsics else None,
+                                            _ptr(lo), _ptr(hi)))
+        return lo, hi
+
+    def sweep_cost_volume(self, bundle: Sequence[CalibratedView], ref_index: int, planes: PlaneStack,
+                          lo: np.ndarray, hi: np.ndarray, costfn: CostFunctionSpec) -> CostVolume:
+        views, keep = _views_c(bundle)
+        n = len(bundle)
+        ref = bundle[min(max(ref_index, 0), max(n - 1, 0))]
+        w, h = ref.intrinsics.width, ref.intrinsics.height
+        px = w * h
+        lo = _f32(lo).reshape(-1)
+        hi = _f32(hi).reshape(-1)
+        first = np.zeros(px, np.int32)
+        count = np.zeros(px, np.int32)
+        offset = np.zeros(px, np.uint64)
+        st, dkeep = _stack_c(planes)
+        cap = max(1, px * planes.count())
+        costs = np.zeros(cap, np.uint16)
+        total = C.c_uint64()
+        per_side = C.c_int32()
+        cs = costfn.to_c()
+        self._check(self.fn["sweep_cost_volume"](self.ctx, views, n, ref_index, C.byref(st), _ptr(lo),
+                                                 _ptr(hi), C.byref(cs), _ptr(first), _ptr(count),
+                                                 _ptr(offset), _ptr(costs), cap, C.byref(total),
+                                                 C.byref(per_side)))
+        return CostVolume(w, h, planes, per_side.value, first, count, offset,
+                          costs[:total.value].copy())
+
+    def compute_normal_offsets(self, prior_normals: np.ndarray, prior_depth: np.ndarray,
+                               planes: PlaneStack, intrinsics: Intrinsics) -> np.ndarray:
+        pn = _f32(prior_normals)
+        pd = _f32(prior_depth)
+        h, w = pd.shape
+        out = np.zeros((h, w, 4), np.int16)
+        st, keep = _stack_c(planes)
+        self._check(self.fn["compute_normal_offsets"](self.ctx, _ptr(pn), _ptr(pd), w, h, C.byref(st),
+                                                      C.byref(intrinsics.to_c()), _ptr(out)))
+        return out
+
+    def _aggregate(self, vol: CostVolume, image: np.ndarray, config: SgmConfig,
+                   intrinsics: Intrinsics, dx: int, dy: int, prior_normals=None, prior_depth=None):
+        st, keep = _stack_c(vol.planes)
+        img = np.ascontiguousarray(image, np.uint8)
+        first = np.ascontiguousarray(vol.first, np.int32)
+        count = np.ascontiguousarray(vol.count, np.int32)
+        offset = np.ascontiguousarray(vol.offset, np.uint64)
+        costs = np.ascontiguousarray(vol.costs, np.uint16)
+        out = np.zeros(max(1, len(costs)), np.uint32)
+        pn = _f32(prior_normals) if prior_normals is not None else None
+        pd = _f32(prior_depth) if prior_depth is not None else None
+        cfg = config.to_c()
+        self._check(self.fn["aggregate"](self.ctx, vol.width, vol.height, C.byref(st), _ptr(first),
+                                         _ptr(count), _ptr(offset), _ptr(costs), len(costs), _ptr(img),
+                                         C.byref(cfg), C.byref(intrinsics.to_c()), _ptr(pn), _ptr(pd),
+                                         dx, dy, _ptr(out)))
+        return AggregatedVolume(vol.width, vol.height, vol.planes, first, count, offset,
+                                out[:len(costs)].copy())
+
+    def aggregate(self, vol: CostVolume, image, config: SgmConfig, intrinsics: Intrinsics,
+                  prior_normals=None, prior_depth=None) -> AggregatedVolume:
+        """aggregate (sgm.hpp:86-89)."""
+        return self._aggregate(vol, image, config, intrinsics, 0, 0, prior_normals, prior_depth)
+
+    def aggregate_single_path(self, vol: CostVolume, image, config: SgmConfig, intrinsics: Intrinsics,
+                              dir_x: int, dir_y: int, prior_normals=None,
+                              prior_depth=None) -> AggregatedVolume:
+        """aggregate_single_path (sgm.hpp:91-96)."""
+        return self._aggregate(vol, image, config, intrinsics, dir_x, dir_y, prior_normals, prior_depth)
+
+    def wta(self, agg: AggregatedVolume) -> np.ndarray:
+        px = agg.width * agg.height
+        out = np.zeros(px, np.int32)
+        first = np.ascontiguousarray(agg.first, np.int32)
+        count = np.ascontiguousarray(agg.count, np.int32)
+        offset = np.ascontiguousarray(agg.offset, np.uint64)
+        vals = np.ascontiguousarray(agg.values, np.uint32)
+        self._check(self.fn["wta"](self.ctx, agg.width, agg.height, _ptr(first), _ptr(count),
+                                   _ptr(offset), _ptr(vals), len(vals), _ptr(out)))
+        return out.reshape(agg.height, agg.width)
+
+    def median_filter_5x5(self, depth: np.ndarray) -> np.ndarray:
+        d = _f32(depth)
+        h, w = d.shape
+        out = np.zeros_like(d)
+        self._check(self.fn["median_filter_5x5"](self.ctx, _ptr(d), w, h, _ptr(out)))
+        return out
+
+    def normals_from_depth(self, depth: np.ndarray, intrinsics: Intrinsics) -> np.ndarray:
+        d = _f32(depth)
+        h, w = d.shape
+        out = np.zeros((h, w, 3), np.float32)
+        self._check(self.fn["normals_from_depth"](self.ctx, _ptr(d), w, h, C.byref(intrinsics.to_c()),
+                                                  _ptr(out)))
+        return out
+
+    def smooth_normals(self, raw: np.ndarray, image: np.ndarray, radius: int) -> np.ndarray:
+        r = _f32(raw)
+        img = np.ascontiguousarray(image, np.uint8)
+        h, w = img.shape
+        out = np.zeros((h, w, 3), np.float32)
+        self._check(self.fn["smooth_normals"](self.ctx, _ptr(r), _ptr(img), w, h, radius, _ptr(out)))
+        return out
+
+    def confidence_map(self, normals: np.ndarray, sweep_normal=(0.0, 0.0, -1.0),
+                       rho_degrees: float = 60.0) -> np.ndarray:
+        nm = _f32(normals)
+        h, w = nm.shape[:2]
+        out = np.zeros((h, w), np.float32)
+        sn = np.asarray(sweep_normal, np.float64)
+        self._check(self.fn["confidence_map"](self.ctx, _ptr(nm), w, h, _pd(sn), rho_degrees, _ptr(out)))
+        return out
+
+    def upscale_nearest(self, m: np.ndarray, width: int, height: int) -> np.ndarray:
+        a = _f32(m)
+        ih, iw = a.shape[:2]
+        ch = 1 if a.ndim == 2 else a.shape[2]
+        out = np.zeros((height, width) + (() if ch == 1 else (ch,)), np.float32)
+        self._check(self.fn["upscale_nearest"](self.ctx, _ptr(a), iw, ih, ch, width, height, _ptr(out)))
+        return out
+
+    # ------------------------------------------------- synthetic scenes
+    def render_plane_scene(self, kind: str, width: int, height: int, focal: float, depth: float,
+                           views: int, baseline_step: float, seed: int = 1, tilt_deg: float = 0.0,
+                           texture_scale: float = 0.5):
+        """fronto_scene / slanted_scene + render_scene (render.hpp:41-62).
+
+        Returns (bundle, gt_depth[views,h,w], gt_normals[views,h,w,3])."""
+        k = 0 if kind == "fronto" else 1
+        px = width * height
+        imgs = np.zeros((views, height, width), np.uint8)
+        gd = np.zeros((views, height, width), np.float32)
+        gn = np.zeros((views, height, width, 3), np.float32)
+        intr = (_abi.Intrinsics_c * views)()
+        poses = (_abi.Pose_c * views)()
+        self._check(self.fn["render_plane_scene"](self.ctx, k, width, height, focal, depth, tilt_deg,
+                                                  views, baseline_step, seed, texture_scale,
+                                                  _ptr(imgs), _ptr(gd), _ptr(gn), intr, poses))
+        bundle = [CalibratedView(imgs[i].copy(), Intrinsics.from_c(intr[i]), Pose.from_c(poses[i]))
+                  for i in range(views)]
+        del px
+        return bundle, gd, gn
+
+
+def default_backend() -> Backend:
+    return Backend.b200()
+
+
+def estimate_bundle(bundle: Sequence[CalibratedView], config: PipelineConfig) -> BundleResult:
+    """Module-level drop-in for fassmvs::estimate_bundle on the B200 library."""
+    return default_backend().estimate_bundle(bundle, config)

@@ -1,0 +1,306 @@
+"""Stage-wise and end-to-end parity of the B200 CUDA path against the oracle
+(the unmodified reference built against the Eigen shim), on identical seeded
+inputs. Integer stages must be bit-exact; the float stages are designed to be
+bit-exact as well (same FP64 expression trees, no FMA), and are asserted so.
+"""
+import numpy as np
+import pytest
+
+from paper_2112_00821_b200 import (ConfigError, CostFunctionSpec, CostKind, CostVolume,
+                                   GeometryError, Intrinsics, InvalidInputError, PlaneStack,
+                                   RangeKind, RangePolicy, SgmConfig, SgmVariant)
+
+from scenes import config, harmonic_stack, random_volume, render
+
+pytestmark = pytest.mark.gpu
+
+COSTS = ["census5", "census97", "ncc5", "ncc9"]
+
+
+def assert_same(a, b, what):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    assert a.shape == b.shape, what
+    if not np.array_equal(a, b, equal_nan=True):
+        bad = np.argwhere(a != b)
+        raise AssertionError(f"{what}: {len(bad)} mismatches, first at {bad[:5].tolist()}: "
+                             f"{a[tuple(bad[0])]} vs {b[tuple(bad[0])]}")
+
+
+# ------------------------------------------------------------- render ----
+def test_render_matches_reference(b200, oracle):
+    for kind, tilt in (("fronto", 0.0), ("slanted", 30.0)):
+        a, ga, na = render(b200, kind, 96, 64, tilt=tilt)
+        b, gb, nb = render(oracle, kind, 96, 64, tilt=tilt)
+        for va, vb in zip(a, b):
+            assert_same(va.image, vb.image, "image")
+        assert_same(ga, gb, "gt depth")
+        assert_same(na, nb, "gt normals")
+
+
+# ------------------------------------------------------------- stages ----
+def test_build_pyramids(b200, oracle):
+    bundle, _, _ = render(oracle, "slanted", 97, 61, tilt=20.0)
+    pa = b200.build_pyramids(bundle, 4)
+    pb = oracle.build_pyramids(bundle, 4)
+    for la, lb in zip(pa, pb):
+        for va, vb in zip(la, lb):
+            assert va.intrinsics == vb.intrinsics
+            assert_same(va.image, vb.image, "pyramid")
+
+
+@pytest.mark.parametrize("kind", [RangeKind.Full, RangeKind.Fixed, RangeKind.SpacingMultiple])
+def test_refine_range(b200, oracle, rng, kind):
+    w, h = 57, 43
+    prior = rng.uniform(3, 12, (h, w)).astype(np.float32)
+    prior[rng.random((h, w)) < 0.1] = 0.0
+    stack = PlaneStack(harmonic_stack(40, fb=200.0, disp0=15.0))
+    intr = Intrinsics(60.0, 60.0, 28.0, 21.0, w, h)
+    pol = RangePolicy(kind, 3.0 if kind != RangeKind.Fixed else 0.7)
+    a = b200.refine_range(prior, pol, 3.2, 13.0, stack, intr)
+    b = oracle.refine_range(prior, pol, 3.2, 13.0, stack, intr)
+    assert_same(a[0], b[0], "lo")
+    assert_same(a[1], b[1], "hi")
+
+
+def _level_inputs(oracle, kind="slanted", w=80, h=60, tilt=25.0, views=5, step=0.5):
+    bundle, _, _ = render(oracle, kind, w, h, tilt=tilt, views=views, step=step)
+    ref = bundle[len(bundle) // 2]
+    n = (0.0, 0.0, -1.0)
+    dlo, dhi = oracle.bounding_distances(6.0, 16.0, n, ref.intrinsics)
+    planes = oracle.plane_distances(ref.intrinsics, ref.pose, bundle[0].intrinsics, bundle[0].pose,
+                                    dlo, dhi, n, 100000)
+    return bundle, PlaneStack(planes, n)
+
+
+@pytest.mark.parametrize("cost", COSTS)
+def test_sweep_cost_volume_bitexact(b200, oracle, rng, cost):
+    bundle, stack = _level_inputs(oracle)
+    ref = bundle[2]
+    h, w = ref.image.shape
+    lo = np.full((h, w), 6.0, np.float32)
+    hi = np.full((h, w), 16.0, np.float32)
+    # ragged ranges around a random prior, some pixels empty
+    mid = rng.uniform(6, 16, (h, w)).astype(np.float32)
+    rad = rng.uniform(0.2, 2.0, (h, w)).astype(np.float32)
+    sel = rng.random((h, w)) < 0.7
+    lo[sel] = np.maximum(6.0, mid - rad)[sel]
+    hi[sel] = np.minimum(16.0, mid + rad)[sel]
+    lo[rng.random((h, w)) < 0.05] = 20.0  # empty intervals
+    spec = {"census5": (CostKind.CensusHamming, 5, 5), "census97": (CostKind.CensusHamming, 9, 7),
+            "ncc5": (CostKind.NccTruncated, 5, 5), "ncc9": (CostKind.NccTruncated, 9, 9)}[cost]
+    cf = CostFunctionSpec(*spec)
+    a = b200.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    b = oracle.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    assert a.per_side == b.per_side
+    assert_same(a.first, b.first, "first")
+    assert_same(a.count, b.count, "count")
+    assert_same(a.offset, b.offset, "offset")
+    assert_same(a.costs, b.costs, "costs")
+    assert len(a.costs) > 1000
+
+
+def test_sweep_three_views_rotated(b200, oracle, rng):
+    """Non-lateral geometry: rotated matching views, non-fronto sweep normal."""
+    bundle, _, _ = render(oracle, "slanted", 72, 54, tilt=35.0, views=3, step=0.8)
+    from scenes import rotation
+    bundle[0].pose.rotation = rotation(rng, 0.03)
+    bundle[2].pose.rotation = rotation(rng, 0.03)
+    n = np.array([0.0, -0.3, -1.0])
+    n /= np.linalg.norm(n)
+    ref = bundle[1]
+    dlo, dhi = oracle.bounding_distances(5.0, 15.0, n, ref.intrinsics)
+    planes = oracle.plane_distances(ref.intrinsics, ref.pose, bundle[0].intrinsics, bundle[0].pose,
+                                    dlo, dhi, n, 100000)
+    stack = PlaneStack(planes, tuple(n))
+    h, w = ref.image.shape
+    lo = np.full((h, w), 5.0, np.float32)
+    hi = np.full((h, w), 15.0, np.float32)
+    for cf in (CostFunctionSpec(CostKind.CensusHamming, 5, 5), CostFunctionSpec(CostKind.NccTruncated, 5, 5)):
+        a = b200.sweep_cost_volume(bundle, 1, stack, lo, hi, cf)
+        b = oracle.sweep_cost_volume(bundle, 1, stack, lo, hi, cf)
+        assert_same(a.count, b.count, "count")
+        assert_same(a.costs, b.costs, "costs")
+
+
+def test_sweep_errors_match(b200, oracle):
+    bundle, stack = _level_inputs(oracle, w=32, h=24)
+    h, w = bundle[2].image.shape
+    lo = np.full((h, w), 6.0, np.float32)
+    hi = np.full((h, w), 16.0, np.float32)
+    for be in (b200, oracle):
+        with pytest.raises(ConfigError):
+            be.sweep_cost_volume(bundle, 2, stack, lo, hi, CostFunctionSpec(CostKind.CensusHamming, 7, 7))
+        with pytest.raises(InvalidInputError):
+            be.sweep_cost_volume(bundle, 0, stack, lo, hi, CostFunctionSpec())
+        with pytest.raises(InvalidInputError):
+            be.sweep_cost_volume(bundle, 2, PlaneStack(stack.distances[::-1].copy()), lo, hi,
+                                 CostFunctionSpec())
+
+
+def _volume(planes, w, h, rng, ragged=True, max_cost=300):
+    first, count, offset, costs = random_volume(rng, w, h, planes, ragged, max_cost)
+    return CostVolume(w, h, PlaneStack(harmonic_stack(planes)), 2, first, count, offset, costs)
+
+
+DIRS = [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1), (1, -1), (-1, 1)]
+
+
+@pytest.mark.parametrize("adaptive", [False, True])
+def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive):
+    img = rng.integers(0, 256, (9, 13)).astype(np.uint8)
+    intr = Intrinsics(100.0, 100.0, 6.0, 4.0, 13, 9)
+    cfg = SgmConfig(SgmVariant.Plane, 8, 7.0, adaptive, 40.0, 8.0, 10.0, 2)
+    for _ in range(4):
+        vol = _volume(11, 13, 9, rng)
+        for dx, dy in DIRS:
+            a = b200.aggregate_single_path(vol, img, cfg, intr, dx, dy)
+            b = oracle.aggregate_single_path(vol, img, cfg, intr, dx, dy)
+            assert_same(a.values, b.values, f"path {dx},{dy}")
+
+
+@pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.SurfaceNormal, SgmVariant.PathGradient])
+@pytest.mark.parametrize("paths", [8, 4])
+def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths):
+    w, h, planes = 37, 29, 48
+    img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    intr = Intrinsics(40.0, 40.0, 18.0, 14.0, w, h)
+    vol = _volume(planes, w, h, rng, ragged=True, max_cost=510)
+    pn = pd = None
+    if variant == SgmVariant.SurfaceNormal:
+        nrm = rng.normal(size=(h, w, 3))
+        nrm[..., 2] = -np.abs(nrm[..., 2]) - 1.0
+        nrm /= np.linalg.norm(nrm, axis=-1, keepdims=True)
+        pn = nrm.astype(np.float32)
+        pd = rng.uniform(10, 14, (h, w)).astype(np.float32)
+        pd[rng.random((h, w)) < 0.1] = 0
+    cfg = SgmConfig(variant, paths, 100.0, True, 0.0, 8.0, 10.0, 2)
+    a = b200.aggregate(vol, img, cfg, intr, pn, pd)
+    b = oracle.aggregate(vol, img, cfg, intr, pn, pd)
+    assert_same(a.values, b.values, "aggregate")
+    assert_same(b200.wta(a), oracle.wta(b), "wta")
+
+
+def test_aggregate_dense_wide(b200, oracle, rng):
+    """Dense coarsest-level shape: >32 hypotheses per pixel (multi-chunk lanes)."""
+    w, h, planes = 40, 24, 130
+    img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    intr = Intrinsics(40.0, 40.0, 19.5, 11.5, w, h)
+    vol = _volume(planes, w, h, rng, ragged=False, max_cost=510)
+    cfg = SgmConfig(SgmVariant.PathGradient, 8, 100.0, True, 0.0, 8.0, 10.0, 2)
+    a = b200.aggregate(vol, img, cfg, intr)
+    b = oracle.aggregate(vol, img, cfg, intr)
+    assert_same(a.values, b.values, "aggregate")
+
+
+def test_aggregate_errors(b200, oracle, rng):
+    vol = _volume(5, 6, 4, rng)
+    img = np.zeros((4, 6), np.uint8)
+    intr = Intrinsics(10.0, 10.0, 2.5, 1.5, 6, 4)
+    for be in (b200, oracle):
+        with pytest.raises(ConfigError):
+            be.aggregate(vol, img, SgmConfig(SgmVariant.SurfaceNormal), intr)
+        with pytest.raises(ConfigError):
+            be.aggregate(vol, img, SgmConfig(paths=6), intr)
+        with pytest.raises(ConfigError):
+            be.aggregate(vol, img, SgmConfig(phi2_adaptive=False, phi2_fixed=1.0), intr)
+
+
+def test_normal_offsets_bitexact(b200, oracle, rng):
+    w, h = 45, 33
+    stack = PlaneStack(harmonic_stack(90, fb=400.0, disp0=20.0))
+    intr = Intrinsics(50.0, 52.0, 22.0, 16.5, w, h)
+    nrm = rng.normal(size=(h, w, 3))
+    nrm[..., 2] = -np.abs(nrm[..., 2]) - 0.5
+    nrm /= np.linalg.norm(nrm, axis=-1, keepdims=True)
+    nrm = nrm.astype(np.float32)
+    nrm[rng.random((h, w)) < 0.05] = 0
+    depth = rng.uniform(12, 19, (h, w)).astype(np.float32)
+    depth[rng.random((h, w)) < 0.05] = 0
+    assert_same(b200.compute_normal_offsets(nrm, depth, stack, intr),
+                oracle.compute_normal_offsets(nrm, depth, stack, intr), "offsets")
+
+
+def test_tail_maps_bitexact(b200, oracle, rng):
+    w, h = 61, 47
+    intr = Intrinsics(70.0, 71.0, 30.5, 23.0, w, h)
+    yy, xx = np.mgrid[0:h, 0:w]
+    depth = (8.0 + 0.03 * xx + 0.05 * yy + rng.normal(0, 0.02, (h, w))).astype(np.float32)
+    depth[rng.random((h, w)) < 0.08] = 0.0
+    assert_same(b200.median_filter_5x5(depth), oracle.median_filter_5x5(depth), "median")
+    raw_a = b200.normals_from_depth(depth, intr)
+    raw_b = oracle.normals_from_depth(depth, intr)
+    assert_same(raw_a, raw_b, "raw normals")
+    img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    for r in (1, 2, 3):
+        sa = b200.smooth_normals(raw_b, img, r)
+        sb = oracle.smooth_normals(raw_b, img, r)
+        assert_same(sa, sb, f"smooth r={r}")
+    sn = (0.0, -0.2, -np.sqrt(1 - 0.04))
+    for rho in (60.0, 45.0):
+        assert_same(b200.confidence_map(sb, sn, rho), oracle.confidence_map(sb, sn, rho), "confidence")
+    for ow, oh in ((w * 2, h * 2), (w * 2 - 1, h * 2 - 1)):
+        assert_same(b200.upscale_nearest(depth, ow, oh), oracle.upscale_nearest(depth, ow, oh), "up d")
+        assert_same(b200.upscale_nearest(sb, ow, oh), oracle.upscale_nearest(sb, ow, oh), "up n")
+
+
+# ---------------------------------------------------------- end to end ----
+E2E = [
+    # (name, scene kwargs, config kwargs)
+    ("c4_fronto_ncc_pi", dict(kind="fronto", w=160, h=120, focal=160.0, depth=10.0, step=0.5, texture=0.35),
+     dict(d_min=8.0, d_max=14.0, levels=1, cost="ncc5")),
+    ("census_sn_3lvl", dict(kind="slanted", w=192, h=108, focal=192.0, depth=10.0, tilt=30.0, step=0.59,
+                            texture=0.2), dict(d_min=4.0, d_max=40.0, levels=3, cost="census5",
+                                               variant=SgmVariant.SurfaceNormal, max_planes=128)),
+    ("c5_slanted_pg", dict(kind="slanted", w=160, h=60, focal=80.0, depth=5.0, tilt=45.0, step=1.75,
+                           texture=0.35), dict(d_min=3.2, d_max=9.0, levels=2, cost="ncc5",
+                                               variant=SgmVariant.PathGradient)),
+    ("census97_4paths", dict(kind="fronto", w=96, h=80, focal=96.0, depth=10.0, step=0.6, views=3),
+     dict(d_min=8.0, d_max=13.0, levels=2, cost="census97", paths=4)),
+    ("ncc9_sn_7views", dict(kind="slanted", w=120, h=90, focal=120.0, depth=10.0, tilt=20.0, step=0.4,
+                            views=7), dict(d_min=6.0, d_max=20.0, levels=2, cost="ncc9",
+                                           variant=SgmVariant.SurfaceNormal)),
+]
+
+
+@pytest.mark.parametrize("name,scene,cfg", E2E, ids=[e[0] for e in E2E])
+def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg):
+    scene = dict(scene)
+    kind = scene.pop("kind")
+    bundle, _, _ = render(oracle, kind, **scene)
+    c = config(**cfg)
+    a = b200.estimate_bundle(bundle, c)
+    b = oracle.estimate_bundle(bundle, c)
+    assert_same(a.depth, b.depth, "depth")
+    assert_same(a.normals, b.normals, "normals")
+    assert_same(a.confidence, b.confidence, "confidence")
+    assert (b.depth > 0).mean() > 0.5
+
+
+def test_estimate_bundle_deterministic(b200, oracle):
+    bundle, _, _ = render(oracle, "slanted", 128, 96, tilt=30.0)
+    c = config(4.0, 40.0, levels=3, cost="census5", variant=SgmVariant.SurfaceNormal)
+    a = b200.estimate_bundle(bundle, c)
+    b = b200.estimate_bundle(bundle, c)
+    assert_same(a.depth, b.depth, "depth")
+    assert_same(a.normals, b.normals, "normals")
+
+
+def test_estimate_bundle_errors_match(b200, oracle):
+    bundle, _, _ = render(oracle, "fronto", 48, 32)
+    cases = [
+        (bundle[:4], config(8.0, 14.0), InvalidInputError),               # even bundle
+        (bundle, config(8.0, 14.0, variant=SgmVariant.SurfaceNormal), ConfigError),  # SN needs 2 levels
+        (bundle, config(8.0, 14.0, bundle_size=4), ConfigError),
+        (bundle, config(8.0, 14.0, max_planes=1), ConfigError),
+        (bundle, config(8.0, 14.0, normal_smoothing_radius=0), ConfigError),
+    ]
+    for bnd, c, exc in cases:
+        for be in (b200, oracle):
+            with pytest.raises(exc):
+                be.estimate_bundle(bnd, c)
+    # zero baseline -> GeometryError (test_pipeline.cpp:198-205)
+    flat = [type(v)(v.image, v.intrinsics, type(v.pose)(v.pose.rotation, np.zeros(3))) for v in bundle]
+    for be in (b200, oracle):
+        with pytest.raises(GeometryError):
+            be.estimate_bundle(flat, config(8.0, 14.0))
