@@ -77,6 +77,7 @@ SIGNATURES = {
     "ctx_stage_name": (C.c_char_p, [P, I32]),
     "ctx_stage_time": (C.c_int, [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "ctx_stage_reset": (None, [P]),
+    "ctx_sweep_stats": (C.c_int, [P, C.POINTER(C.c_uint64)]),
     "host_alloc": (P, [U64]),
     "host_free": (None, [P]),
     "estimate_bundle": (C.c_int, [P, C.POINTER(View_c), I32, C.POINTER(Config_c), P, P, P]),

@@ -12,6 +12,7 @@
 // same kernels on host-provided inputs for stage-wise parity tests.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -224,6 +225,8 @@ struct fmvs_ctx {
     int64_t launches = 0;
     // optional per-stage CUDA-event timing (bench.py roofline numbers)
     bool timing = false;
+    int sweep_exact = 0;  // FMVS_SWEEP_EXACT=1: force the exact per-hypothesis sweep
+    int sweep_stats = 0;  // FMVS_SWEEP_STATS=1: count certified-census fallbacks
     struct Span {
         int stage;
         cudaEvent_t a, b;
@@ -502,6 +505,9 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         sa.ww = cfg.cost.window_w;
         sa.wh = cfg.cost.window_h;
         sa.census_lut = d_clut;
+        sa.disable_tiled = ctx->sweep_exact;
+        if (ctx->sweep_stats)
+            sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(4);
         ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { k::sweep(sa, s); });
         ++launches;
 
@@ -679,10 +685,16 @@ int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
             fmvs::fail_input("ctx: null output");
         auto ctx = std::make_unique<fmvs_ctx>();
         ctx->device = device;
+        if (const char* e = std::getenv("FMVS_SWEEP_EXACT"))
+            ctx->sweep_exact = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FMVS_SWEEP_STATS"))
+            ctx->sweep_stats = std::atoi(e) != 0;
         ctx->use();
         FMVS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         FMVS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->staged, cudaEventDisableTiming));
         FMVS_CUDA_CHECK(cudaEventRecord(ctx->staged, ctx->stream));
+        if (ctx->sweep_stats)
+            FMVS_CUDA_CHECK(cudaMemset(ctx->buf("sweep_stats").as<unsigned long long>(4), 0, 32));
         *out = ctx.release();
     });
 }
@@ -714,6 +726,23 @@ int fmvs_ctx_synchronize(fmvs_ctx* ctx) {
 }
 
 void fmvs_ctx_set_timing(fmvs_ctx* ctx, int32_t enable) { ctx->timing = enable != 0; }
+
+// Diagnostics of the certified census sweep (FMVS_SWEEP_STATS=1): counts of
+// (hypothesis, view) evaluations, evaluations with >= 1 undecided bit, undecided
+// bits, exact-path views. Reads and clears the counters.
+int fmvs_ctx_sweep_stats(fmvs_ctx* ctx, uint64_t out[4]) {
+    return guarded([&] {
+        ctx->use();
+        for (int i = 0; i < 4; ++i)
+            out[i] = 0;
+        if (!ctx->sweep_stats)
+            return;
+        auto* d = ctx->buf("sweep_stats").as<unsigned long long>(4);
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        FMVS_CUDA_CHECK(cudaMemcpy(out, d, 32, cudaMemcpyDeviceToHost));
+        FMVS_CUDA_CHECK(cudaMemset(d, 0, 32));
+    });
+}
 
 int32_t fmvs_ctx_stage_count(fmvs_ctx* ctx) { return static_cast<int32_t>(ctx->stage_names.size()); }
 

@@ -15,6 +15,10 @@
 // first (same sequential walk) so the window need not be stored.
 // Roofline: FP64-issue-bound (~50 DP ops per bilinear sample); HBM traffic is
 // 2 B per hypothesis written plus the (L2-resident) images.
+#include <type_traits>
+
+#include <cub/block/block_scan.cuh>
+
 #include "host.hpp"
 #include "kernels.hpp"
 
@@ -158,6 +162,7 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
     constexpr int NSP = KIND == FMVS_COST_NCC ? NS : 1;
     __shared__ int s_prefix[kSeg + 1];
     __shared__ int s_first[kSeg];
+    __shared__ uint32_t s_rel[kSeg];
     __shared__ uint64_t s_bits[kSeg];
     __shared__ double s_mean[kSeg], s_var[kSeg];
     __shared__ float s_patch[kSeg][NSP];
@@ -174,9 +179,12 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
         if (t < npx) {
             const VolMeta m = a.meta[static_cast<size_t>(y) * a.w + x0 + t];
             cnt = meta_count(m.fc);
+            if (cnt <= a.exact_above)
+                cnt = 0;  // narrow pixel: handled by the tiled certified kernel
             s_first[t] = meta_first(m.fc);
+            s_rel[t] = m.rel;
             if (t == 0)
-                s_base = a.row_base[y] + m.rel;
+                s_base = a.row_base[y];
         }
         int incl = cnt;
 #pragma unroll
@@ -256,15 +264,437 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
             else
                 sum_r += c;
         }
-        a.costs[base + e] = static_cast<uint16_t>(min(sum_l, sum_r));
+        const uint64_t o = base + s_rel[j] + (e - s_prefix[j]);
+        a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
         if (a.agg_zero)
-            a.agg_zero[base + e] = 0u;
+            a.agg_zero[o] = 0u;
+    }
+}
+
+// ===================================================================
+// Tiled certified census sweep (narrow pixels, count <= kNarrowMax).
+//
+// For a fixed (plane, view) the warped sample belonging to reference pixel
+// (u, v) is the same bilinear lookup for every one of the WW*WH windows that
+// contain (u, v); the reference recomputes it per window through its FP64
+// walk. Here each CTA owns a 32x8 pixel tile, and for every plane of the
+// union of its pixels' ranges it warps the (tile + halo) once per view in
+// FP32 into shared memory, together with a rigorous bound E on
+// |f32 - v64| valid for EVERY window's FP64 walk value (coordinate error from
+// an anchored residual form of the homography, times the cell's bilinear
+// Lipschitz constant, plus arithmetic slack). A census bit is taken from the
+// FP32 values when |f_n - f_c| > E_n + E_c, which proves the FP64 comparison
+// of the reference has the same outcome; otherwise that one bit is recomputed
+// with the reference's exact FP64 walk. Costs are therefore bit-identical.
+// ===================================================================
+
+constexpr int kTW = 32, kTH = 8, kTiledThreads = kTW * kTH;
+constexpr int kNarrowMax = 192;
+constexpr int kMaxMatch = 8;
+
+struct TileParams {
+    float ax, bx, cx;  // r_x(du, dv) = q.x - xa * q.z
+    float ay, by, cy;  // r_y(du, dv) = q.y - ya * q.z
+    float az, bz, cz;  // q.z(du, dv)
+    float dx, dy;      // certified coordinate error bounds (pixels)
+    int xa, ya;        // integer anchors
+    int exact;         // certification impossible: exact FP64 for this view
+};
+
+// FP64 sample of window position (i, j) of pixel (x, y), exactly as the
+// reference computes it (matching.cpp:222-248).
+__device__ __noinline__ double exact_window_sample(const double* __restrict__ hp,
+                                                   const uint32_t* __restrict__ quad, int vw,
+                                                   int vh, double xd, double yd, int rx, int ry,
+                                                   int i, int j) {
+    using namespace dev;
+    double H[9];
+    for (int k = 0; k < 9; ++k)
+        H[k] = __ldg(hp + k);
+    const double cx = add(add(mul(H[0], xd), mul(H[1], yd)), H[2]);
+    const double cy = add(add(mul(H[3], xd), mul(H[4], yd)), H[5]);
+    const double cz = add(add(mul(H[6], xd), mul(H[7], yd)), H[8]);
+    double qx = sub(sub(cx, mul(double(rx), H[0])), mul(double(ry), H[1]));
+    double qy = sub(sub(cy, mul(double(rx), H[3])), mul(double(ry), H[4]));
+    double qz = sub(sub(cz, mul(double(rx), H[6])), mul(double(ry), H[7]));
+    for (int r = 0; r < i; ++r) {
+        qx = add(qx, H[1]);
+        qy = add(qy, H[4]);
+        qz = add(qz, H[7]);
+    }
+    for (int c = 0; c < j; ++c) {
+        qx = add(qx, H[0]);
+        qy = add(qy, H[3]);
+        qz = add(qz, H[6]);
+    }
+    return warp_sample(quad, vw, vh, qx, qy, qz);
+}
+
+// The reference's inside test of the warped window centre (matching.cpp:224-231).
+__device__ __noinline__ bool exact_inside(const double* __restrict__ hp, int vw, int vh, double xd,
+                                          double yd) {
+    using namespace dev;
+    const double cx = add(add(mul(__ldg(hp + 0), xd), mul(__ldg(hp + 1), yd)), __ldg(hp + 2));
+    const double cy = add(add(mul(__ldg(hp + 3), xd), mul(__ldg(hp + 4), yd)), __ldg(hp + 5));
+    const double cz = add(add(mul(__ldg(hp + 6), xd), mul(__ldg(hp + 7), yd)), __ldg(hp + 8));
+    if (!(cz > 0.0))
+        return false;
+    const double cxw = div(cx, cz), cyw = div(cy, cz);
+    return cxw >= 0.0 && cyw >= 0.0 && cxw <= double(vw) - 1.0 && cyw <= double(vh) - 1.0;
+}
+
+// Per-(tile, plane, view) residual coefficients and error bounds (FP64).
+__device__ TileParams make_tile_params(const double* __restrict__ hp, int u0, int v0, int du_max,
+                                       int dv_max) {
+    TileParams tp{};
+    double H[9];
+    for (int k = 0; k < 9; ++k)
+        H[k] = __ldg(hp + k);
+    const double U = u0, V = v0, DU = du_max, DV = dv_max;
+    const double q0x = H[0] * U + H[1] * V + H[2];
+    const double q0y = H[3] * U + H[4] * V + H[5];
+    const double q0z = H[6] * U + H[7] * V + H[8];
+    const double z10 = q0z + H[6] * DU, z01 = q0z + H[7] * DV, z11 = z10 + H[7] * DV;
+    const double zmin = fmin(fmin(q0z, z10), fmin(z01, z11));
+    const double two24 = 5.9604644775390625e-08;  // 2^-24
+    const double two45 = 2.842170943040401e-14;   // 2^-45
+    const double Mz = fabs(H[6]) * (fabs(U) + DU) + fabs(H[7]) * (fabs(V) + DV) + fabs(H[8]);
+    const double Mx = fabs(H[0]) * (fabs(U) + DU) + fabs(H[1]) * (fabs(V) + DV) + fabs(H[2]);
+    const double My = fabs(H[3]) * (fabs(U) + DU) + fabs(H[4]) * (fabs(V) + DV) + fabs(H[5]);
+    if (!(zmin > 64.0 * two45 * Mz) || !(q0z > 0.0)) {
+        tp.exact = 1;
+        return tp;
+    }
+    double xa = floor(q0x / q0z), ya = floor(q0y / q0z);
+    if (!(fabs(xa) < 4.0e6) || !(fabs(ya) < 4.0e6)) {
+        tp.exact = 1;
+        return tp;
+    }
+    const double axd = H[0] - xa * H[6], bxd = H[1] - xa * H[7], cxd = q0x - xa * q0z;
+    const double ayd = H[3] - ya * H[6], byd = H[4] - ya * H[7], cyd = q0y - ya * q0z;
+    const double Rx = fabs(axd) * DU + fabs(bxd) * DV + fabs(cxd);
+    const double Ry = fabs(ayd) * DU + fabs(byd) * DV + fabs(cyd);
+    const double Rz = fabs(H[6]) * DU + fabs(H[7]) * DV + fabs(q0z);
+    // FP32 evaluation (coefficient rounding + two FMA roundings) and FP64
+    // rounding of the coefficients / of the reference's own walk.
+    const double ez = 4.0 * two24 * Rz + two45 * Mz;
+    const double ex = 4.0 * two24 * Rx + two45 * (Mx + fabs(xa) * Mz);
+    const double ey = 4.0 * two24 * Ry + two45 * (My + fabs(ya) * Mz);
+    const double rzmin = zmin - ez;
+    if (!(rzmin > 0.0)) {
+        tp.exact = 1;
+        return tp;
+    }
+    const double Tx = (Rx + ex) / rzmin, Ty = (Ry + ey) / rzmin;
+    // division by rcp.approx (<= 2 ulp) + multiply (0.5 ulp): budget 8 ulp.
+    double dx = (ex + Tx * ez) / rzmin + 8.0 * two24 * Tx +
+                two45 * (Mx + (fabs(xa) + Tx) * Mz) / rzmin;
+    double dy = (ey + Ty * ez) / rzmin + 8.0 * two24 * Ty +
+                two45 * (My + (fabs(ya) + Ty) * Mz) / rzmin;
+    dx = dx * 1.01 + 1e-9;
+    dy = dy * 1.01 + 1e-9;
+    if (!(dx < 0.05) || !(dy < 0.05)) {
+        tp.exact = 1;
+        return tp;
+    }
+    tp.ax = __double2float_rn(axd);
+    tp.bx = __double2float_rn(bxd);
+    tp.cx = __double2float_rn(cxd);
+    tp.ay = __double2float_rn(ayd);
+    tp.by = __double2float_rn(byd);
+    tp.cy = __double2float_rn(cyd);
+    tp.az = __double2float_rn(H[6]);
+    tp.bz = __double2float_rn(H[7]);
+    tp.cz = __double2float_rn(q0z);
+    tp.dx = __double2float_ru(dx);
+    tp.dy = __double2float_ru(dy);
+    tp.xa = static_cast<int>(xa);
+    tp.ya = static_cast<int>(ya);
+    tp.exact = 0;
+    return tp;
+}
+
+// FP32 warp of tile sample (du, dv): cell-relative residual coordinates.
+__device__ __forceinline__ void tile_coords(const TileParams& tp, float du, float dv, float* tx,
+                                            float* ty) {
+    const float rz = fmaf(tp.az, du, fmaf(tp.bz, dv, tp.cz));
+    const float rx = fmaf(tp.ax, du, fmaf(tp.bx, dv, tp.cx));
+    const float ry = fmaf(tp.ay, du, fmaf(tp.by, dv, tp.cy));
+    const float r = __fdividef(1.0f, rz);
+    *tx = rx * r;
+    *ty = ry * r;
+}
+
+__device__ __forceinline__ int popcount_bits(uint32_t v) { return __popc(v); }
+__device__ __forceinline__ int popcount_bits(uint64_t v) { return __popcll(v); }
+__device__ __forceinline__ int lowest_bit(uint32_t v) { return __ffs(v) - 1; }
+__device__ __forceinline__ int lowest_bit(uint64_t v) { return __ffsll(static_cast<long long>(v)) - 1; }
+
+// Bit index of the census string (MSB = first window sample, centre skipped,
+// matching.cpp:251-258) -> row-major window position.
+template <int WW, int WH>
+__device__ __forceinline__ int bit_to_pos(int bi) {
+    constexpr int NB = WW * WH - 1, CENTER = (WW * WH) / 2;
+    const int o = NB - 1 - bi;
+    return o < CENTER ? o : o + 1;
+}
+
+constexpr int kItemCap = 1024;
+
+template <int WW, int WH>
+__global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a) {
+    using namespace dev;
+    using BitsT = typename std::conditional<(WW * WH - 1 > 32), uint64_t, uint32_t>::type;
+    using Scan = cub::BlockScan<int, kTiledThreads>;
+    constexpr int RX = WW / 2, RY = WH / 2;
+    constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
+    constexpr int CENTER = (WW * WH) / 2;
+    extern __shared__ float2 s_tile[];  // [nmatch][SH][SW] (value, bound)
+    __shared__ TileParams s_tp[kMaxMatch];
+    __shared__ int s_pmin, s_pmax;
+    __shared__ typename Scan::TempStorage s_scan;
+    __shared__ uint32_t s_items[kItemCap];  // (thread, view, window position)
+    __shared__ double s_vals[kItemCap];     // their exact FP64 samples
+
+    const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+    const int x = x0 + tx, y = y0 + ty;
+    const bool in_img = x < a.w && y < a.h;
+
+    int first = 0, count = 0;
+    uint64_t base = 0, ref_bits = 0;
+    if (in_img) {
+        const VolMeta m = a.meta[static_cast<size_t>(y) * a.w + x];
+        first = meta_first(m.fc);
+        count = meta_count(m.fc);
+        base = a.row_base[y] + m.rel;
+        if (count > kNarrowMax)
+            count = 0;  // wide pixel: the exact per-hypothesis kernel owns it
+        if (count > 0) {
+            const uint8_t* ref = a.ref_img;  // census_bits_at (matching.cpp:28-42)
+            const uint8_t c = ref[static_cast<size_t>(y) * a.w + x];
+            for (int dy = -RY; dy <= RY; ++dy)
+                for (int dx = -RX; dx <= RX; ++dx) {
+                    if (dx == 0 && dy == 0)
+                        continue;
+                    const int xx = min(max(x + dx, 0), a.w - 1);
+                    const int yy = min(max(y + dy, 0), a.h - 1);
+                    ref_bits = (ref_bits << 1) | (ref[static_cast<size_t>(yy) * a.w + xx] < c ? 1u : 0u);
+                }
+        }
+    }
+    if (threadIdx.x == 0) {
+        s_pmin = 0x7FFFFFFF;
+        s_pmax = -1;
+    }
+    __syncthreads();
+    if (count > 0) {
+        atomicMin(&s_pmin, first);
+        atomicMax(&s_pmax, first + count - 1);
+    }
+    __syncthreads();
+    const int pmin = s_pmin, pmax = s_pmax;
+    const int nm = a.nmatch;
+    const double xd = double(x), yd = double(y);
+
+    for (int p = pmin; p <= pmax; ++p) {
+        const bool need = count > 0 && p >= first && p < first + count;
+        if (!__syncthreads_or(need))
+            continue;
+        if (threadIdx.x < nm)
+            s_tp[threadIdx.x] = make_tile_params(
+                a.homs + (static_cast<size_t>(threadIdx.x) * a.nplanes + p) * 9, x0 - RX, y0 - RY,
+                SW - 1, SH - 1);
+        __syncthreads();
+        // ---- warp the tile + halo of every matching view into shared memory
+        for (int s = threadIdx.x; s < nm * SN; s += kTiledThreads) {
+            const int m = s / SN, r = s - m * SN;
+            const int dv = r / SW, du = r - dv * SW;
+            const TileParams tp = s_tp[m];
+            float2 out = make_float2(0.0f, 1e30f);
+            if (!tp.exact) {
+                float tcx, tcy;
+                tile_coords(tp, float(du), float(dv), &tcx, &tcy);
+                const int2 sz = a.sizes[m];
+                const float fx = floorf(tcx), fy = floorf(tcy);
+                int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
+                float ax = tcx - fx, ay = tcy - fy;
+                if (X0 < 0) { X0 = 0; ax = 0.0f; }
+                else if (X0 >= sz.x - 1) { X0 = sz.x - 1; ax = 0.0f; }
+                if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
+                else if (Y0 >= sz.y - 1) { Y0 = sz.y - 1; ay = 0.0f; }
+                const uint32_t q = __ldg(a.quads[m] + static_cast<size_t>(Y0) * sz.x + X0);
+                const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
+                const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
+                const float top = fmaf(ax, i10 - i00, i00);
+                const float bot = fmaf(ax, i11 - i01, i01);
+                const float f = fmaf(ay, bot - top, top);
+                const bool near_x = ax < tp.dx || ax > 1.0f - tp.dx;
+                const bool near_y = ay < tp.dy || ay > 1.0f - tp.dy;
+                const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
+                const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
+                out = make_float2(f, fmaf(gx, tp.dx, fmaf(gy, tp.dy, 2.0e-4f)));
+            }
+            s_tile[s] = out;
+        }
+        __syncthreads();
+        // ---- pass 1: FP32 census bits + undecided-bit masks per view
+        BitsT bits[kMaxMatch], uns[kMaxMatch];
+        uint32_t view_out = 0;    // bit m: window centre outside the view -> 255
+        uint32_t view_exact = 0;  // bit m: certification impossible -> exact path
+        int my_items = 0;
+#pragma unroll
+        for (int m = 0; m < kMaxMatch; ++m) {
+            bits[m] = 0;
+            uns[m] = 0;
+            if (!need || m >= nm)
+                continue;
+            const TileParams& tp = s_tp[m];
+            if (tp.exact) {
+                view_exact |= 1u << m;
+                continue;
+            }
+            const int2 sz = a.sizes[m];
+            // inside test of the window centre (matching.cpp:224-231), certified
+            float tcx, tcy;
+            tile_coords(tp, float(tx + RX), float(ty + RY), &tcx, &tcy);
+            const double X = double(tp.xa) + double(tcx), Y = double(tp.ya) + double(tcy);
+            const double ddx = tp.dx, ddy = tp.dy;
+            bool inside;
+            if (X - ddx >= 0.0 && Y - ddy >= 0.0 && X + ddx <= double(sz.x - 1) &&
+                Y + ddy <= double(sz.y - 1))
+                inside = true;
+            else if (X + ddx < 0.0 || Y + ddy < 0.0 || X - ddx > double(sz.x - 1) ||
+                     Y - ddy > double(sz.y - 1))
+                inside = false;
+            else
+                inside = exact_inside(a.homs + (static_cast<size_t>(m) * a.nplanes + p) * 9, sz.x,
+                                      sz.y, xd, yd);
+            if (!inside) {
+                view_out |= 1u << m;
+                continue;
+            }
+            const float2* t = s_tile + m * SN;
+            const float2 c = t[(ty + RY) * SW + tx + RX];
+            BitsT b = 0, u = 0;
+#pragma unroll
+            for (int i = 0; i < WH; ++i)
+#pragma unroll
+                for (int j = 0; j < WW; ++j) {
+                    if (i * WW + j == CENTER)
+                        continue;
+                    const float2 n = t[(ty + i) * SW + tx + j];
+                    const float d = n.x - c.x;
+                    b = (b << 1) | (d < 0.0f ? 1u : 0u);
+                    u = (u << 1) | (fabsf(d) > n.y + c.y ? 0u : 1u);
+                }
+            bits[m] = b;
+            uns[m] = u;
+            if (u)
+                my_items += 1 + popcount_bits(u);
+            if (a.stats) {
+                atomicAdd(a.stats + 0, 1ull);
+                if (u) {
+                    atomicAdd(a.stats + 1, 1ull);
+                    atomicAdd(a.stats + 2, static_cast<unsigned long long>(popcount_bits(u)));
+                }
+            }
+        }
+        // ---- pass 1b: CTA-wide list of the samples that need the exact walk
+        int off, total;
+        Scan(s_scan).ExclusiveSum(my_items, off, total);
+        if (my_items) {
+            int k = off;
+#pragma unroll
+            for (int m = 0; m < kMaxMatch; ++m) {
+                if (!uns[m])
+                    continue;
+                if (k < kItemCap)
+                    s_items[k] = threadIdx.x | (m << 8) | (CENTER << 12);
+                ++k;
+                BitsT u = uns[m];
+                while (u) {
+                    const int bi = lowest_bit(u);
+                    u &= u - 1;
+                    if (k < kItemCap)
+                        s_items[k] = threadIdx.x | (m << 8) | (bit_to_pos<WW, WH>(bi) << 12);
+                    ++k;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- pass 2: exact FP64 samples, one per thread (fully SIMT-parallel)
+        const int nitems = min(total, kItemCap);
+        for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
+            const uint32_t item = s_items[it];
+            const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = item >> 12;
+            const int2 sz = a.sizes[m];
+            s_vals[it] = exact_window_sample(a.homs + (static_cast<size_t>(m) * a.nplanes + p) * 9,
+                                             a.quads[m], sz.x, sz.y, double(x0 + t % kTW),
+                                             double(y0 + t / kTW), RX, RY, pos / WW, pos % WW);
+        }
+        __syncthreads();
+        // ---- pass 3: resolve undecided bits, per-side sums, min -> u16
+        if (need) {
+            int sum_l = 0, sum_r = 0, k = off;
+#pragma unroll
+            for (int m = 0; m < kMaxMatch; ++m) {
+                if (m >= nm)
+                    continue;
+                const int2 sz = a.sizes[m];
+                const double* hp = a.homs + (static_cast<size_t>(m) * a.nplanes + p) * 9;
+                int cost;
+                if ((view_exact >> m) & 1u) {
+                    if (a.stats)
+                        atomicAdd(a.stats + 3, 1ull);
+                    cost = view_cost<FMVS_COST_CENSUS, WW, WH>(a.quads[m], sz.x, sz.y, hp, xd, yd,
+                                                              ref_bits, nullptr, 0.0, 0.0,
+                                                              a.census_lut);
+                } else if ((view_out >> m) & 1u) {
+                    cost = 255;
+                } else {
+                    BitsT b = bits[m];
+                    if (uns[m]) {
+                        const double wc = k < kItemCap ? s_vals[k]
+                                                       : exact_window_sample(hp, a.quads[m], sz.x, sz.y,
+                                                                             xd, yd, RX, RY, RY, RX);
+                        ++k;
+                        BitsT u = uns[m];
+                        while (u) {
+                            const int bi = lowest_bit(u);
+                            u &= u - 1;
+                            const int pos = bit_to_pos<WW, WH>(bi);
+                            const double v = k < kItemCap
+                                                 ? s_vals[k]
+                                                 : exact_window_sample(hp, a.quads[m], sz.x, sz.y, xd,
+                                                                       yd, RX, RY, pos / WW, pos % WW);
+                            ++k;
+                            const BitsT one = 1;
+                            b = v < wc ? (b | (one << bi)) : (b & ~(one << bi));
+                        }
+                    }
+                    cost = a.census_lut[popcount_bits(b ^ static_cast<BitsT>(ref_bits))];
+                }
+                if (m < a.nleft)
+                    sum_l += cost;
+                else
+                    sum_r += cost;
+            }
+            const uint64_t o = base + static_cast<uint64_t>(p - first);
+            a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
+            if (a.agg_zero)
+                a.agg_zero[o] = 0u;
+        }
+        __syncthreads();
     }
 }
 
 }  // namespace
 
-void sweep(const SweepArgs& a, cudaStream_t s) {
+void sweep(const SweepArgs& a_in, cudaStream_t s) {
+    SweepArgs a = a_in;
+    const bool tiled = a.kind == FMVS_COST_CENSUS && !a.disable_tiled && a.nmatch <= kMaxMatch;
+    a.exact_above = tiled ? kNarrowMax : 0;
     const dim3 grid((a.w + kSeg - 1) / kSeg, a.h);
     if (a.kind == FMVS_COST_CENSUS && a.ww == 5)
         sweep_kernel<FMVS_COST_CENSUS, 5, 5><<<grid, kThreads, 0, s>>>(a);
@@ -274,6 +704,17 @@ void sweep(const SweepArgs& a, cudaStream_t s) {
         sweep_kernel<FMVS_COST_NCC, 5, 5><<<grid, kThreads, 0, s>>>(a);
     else
         sweep_kernel<FMVS_COST_NCC, 9, 9><<<grid, kThreads, 0, s>>>(a);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+    if (!tiled)
+        return;
+    const dim3 tgrid((a.w + kTW - 1) / kTW, (a.h + kTH - 1) / kTH);
+    if (a.ww == 5) {
+        const size_t smem = sizeof(float2) * a.nmatch * (kTW + 4) * (kTH + 4);
+        sweep_census_tiled<5, 5><<<tgrid, kTiledThreads, smem, s>>>(a);
+    } else {
+        const size_t smem = sizeof(float2) * a.nmatch * (kTW + 8) * (kTH + 6);
+        sweep_census_tiled<9, 7><<<tgrid, kTiledThreads, smem, s>>>(a);
+    }
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

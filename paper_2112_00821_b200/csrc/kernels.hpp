@@ -64,6 +64,11 @@ struct SweepArgs {
     uint32_t* agg_zero;              // optional: zeroed at the same entries
     int kind, ww, wh;
     const uint16_t* census_lut;      // [bits+1]
+    // set by the launcher: pixels with count <= exact_above go to the tiled
+    // certified census kernel, the rest to the exact per-hypothesis kernel
+    int exact_above;
+    int disable_tiled;               // force the exact per-hypothesis kernel
+    unsigned long long* stats;       // optional diagnostics: [view-evals, unsure evals, unsure bits, exact views]
 };
 void sweep(const SweepArgs& a, cudaStream_t s);
 

@@ -1,9 +1,10 @@
+# One GPU round trip: smoke, parity tests, a short bench (+ optional extra cmd)
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-nproc
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
 tail -30 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 5 --warmup 3 --cpu-baseline-steps 1 > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo bench rc=$?
-cat gpurun_out/bench1.json; tail -20 gpurun_out/bench1.err
-cat gpurun_out/smoke.log | tail -5
+timeout 600 python bench.py --steps ${STEPS:-10} --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+cat gpurun_out/bench.json; tail -20 gpurun_out/bench.err
+if [ -n "$EXTRA" ]; then bash -c "$EXTRA"; fi

@@ -100,6 +100,71 @@ def test_sweep_cost_volume_bitexact(b200, oracle, rng, cost):
     assert len(a.costs) > 1000
 
 
+@pytest.mark.parametrize("texture", ["quantized", "noise", "constant"])
+@pytest.mark.parametrize("cost", ["census5", "census97"])
+def test_sweep_certified_census_ties(b200, oracle, rng, texture, cost):
+    """Flat / quantised / noisy images stress the certified FP32 census path:
+    exact FP64 ties and near-ties must fall back to the reference walk."""
+    bundle, stack = _level_inputs(oracle, w=70, h=44)
+    for v in bundle:
+        if texture == "quantized":
+            v.image = ((v.image // 48) * 48).astype(np.uint8)
+        elif texture == "noise":
+            v.image = rng.integers(0, 256, v.image.shape).astype(np.uint8)
+        else:
+            v.image = np.full_like(v.image, 77)
+    h, w = bundle[2].image.shape
+    lo = np.full((h, w), 6.0, np.float32)
+    hi = np.full((h, w), 16.0, np.float32)
+    cf = CostFunctionSpec(CostKind.CensusHamming, *((5, 5) if cost == "census5" else (9, 7)))
+    a = b200.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    b = oracle.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    assert_same(a.costs, b.costs, "costs")
+
+
+def test_sweep_mixed_wide_and_narrow(b200, oracle, rng):
+    """Pixels with > 192 hypotheses (full-range, invalid prior) take the exact
+    per-hypothesis kernel, the rest the tiled certified kernel, in one call."""
+    bundle, _, _ = render(oracle, "slanted", 120, 40, focal=400.0, tilt=20.0, step=1.2)
+    ref = bundle[2]
+    n = (0.0, 0.0, -1.0)
+    dlo, dhi = oracle.bounding_distances(4.0, 40.0, n, ref.intrinsics)
+    planes = oracle.plane_distances(ref.intrinsics, ref.pose, bundle[0].intrinsics, bundle[0].pose,
+                                    dlo, dhi, n, 100000)
+    assert len(planes) > 192
+    stack = PlaneStack(planes, n)
+    h, w = ref.image.shape
+    lo = np.full((h, w), 4.0, np.float32)
+    hi = np.full((h, w), 40.0, np.float32)
+    narrow = rng.random((h, w)) < 0.7
+    mid = rng.uniform(8, 12, (h, w)).astype(np.float32)
+    lo[narrow] = (mid - 0.5)[narrow]
+    hi[narrow] = (mid + 0.5)[narrow]
+    cf = CostFunctionSpec(CostKind.CensusHamming, 5, 5)
+    a = b200.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    b = oracle.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    assert (b.count > 192).any() and (b.count[b.count > 0] <= 192).any()
+    assert_same(a.costs, b.costs, "costs")
+
+
+@pytest.mark.parametrize("views", [9, 11])
+def test_sweep_many_views(b200, oracle, views):
+    """9 views = the tiled kernel's maximum (8 matching), 11 = exact fallback path."""
+    bundle, _, _ = render(oracle, "slanted", 48, 36, tilt=20.0, views=views, step=0.3)
+    ref = bundle[views // 2]
+    n = (0.0, 0.0, -1.0)
+    dlo, dhi = oracle.bounding_distances(6.0, 16.0, n, ref.intrinsics)
+    planes = oracle.plane_distances(ref.intrinsics, ref.pose, bundle[0].intrinsics, bundle[0].pose,
+                                    dlo, dhi, n, 100000)
+    stack = PlaneStack(planes, n)
+    lo = np.full((36, 48), 6.0, np.float32)
+    hi = np.full((36, 48), 16.0, np.float32)
+    cf = CostFunctionSpec(CostKind.CensusHamming, 5, 5)
+    a = b200.sweep_cost_volume(bundle, views // 2, stack, lo, hi, cf)
+    b = oracle.sweep_cost_volume(bundle, views // 2, stack, lo, hi, cf)
+    assert_same(a.costs, b.costs, "costs")
+
+
 def test_sweep_three_views_rotated(b200, oracle, rng):
     """Non-lateral geometry: rotated matching views, non-fronto sweep normal."""
     bundle, _, _ = render(oracle, "slanted", 72, 54, tilt=35.0, views=3, step=0.8)
