@@ -544,6 +544,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         ga.variant = variant;
         ga.phi1 = std::llround(sc.phi1 * sc.penalty_scale);
         ga.phi2_lut = d_phi2;
+        ga.phi2_max = *std::max_element(phi2.begin(), phi2.end());
         ga.offsets = variant == FMVS_SGM_SURFACE_NORMAL ? offs : nullptr;
         ga.intr = intr;
         ga.nx = nx;
@@ -1162,6 +1163,7 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         ga.phi1 = std::llround(cfg->phi1 * cfg->penalty_scale);
         const std::vector<long long> lut = fmvs::phi2_table(*cfg);
         ga.phi2_lut = t.upload(lut.data(), lut.size(), s);
+        ga.phi2_max = *std::max_element(lut.begin(), lut.end());
         ga.intr = intr_of(*intr);
         ga.nx = planes->normal[0];
         ga.ny = planes->normal[1];

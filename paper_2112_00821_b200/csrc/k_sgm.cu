@@ -39,7 +39,9 @@ __device__ __forceinline__ bool scene_point(const dev::Intr& k, double nx, doubl
     return true;
 }
 
-template <int VARIANT>
+// V is the accumulator type of the recurrence: int64 like the reference, or
+// int32 when the host has proven every intermediate fits (sgm() below).
+template <int VARIANT, typename V>
 __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_lines) {
     using namespace dev;
     extern __shared__ uint32_t smem[];
@@ -51,8 +53,8 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
     int rem = gw;
     int d = 0;
     for (; d < a.ndirs; ++d) {
-        const int dx = a.dirs[d][0], dy = a.dirs[d][1];
-        const int n = (dx != 0 && dy != 0) ? a.h + a.w - 1 : (dy == 0 ? a.h : a.w);
+        const int ddx = a.dirs[d][0], ddy = a.dirs[d][1];
+        const int n = (ddx != 0 && ddy != 0) ? a.h + a.w - 1 : (ddy == 0 ? a.h : a.w);
         if (rem < n)
             break;
         rem -= n;
@@ -74,14 +76,9 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
         y = dy > 0 ? 0 : a.h - 1;
     }
 
-    uint32_t* buf_prev;
-    uint32_t* buf_cur;
-    if (a.scratch) {
-        buf_prev = a.scratch + static_cast<size_t>(gw) * 2 * a.pmax;
-    } else {
-        buf_prev = smem + static_cast<size_t>(warp) * 2 * a.pmax;
-    }
-    buf_cur = buf_prev + a.pmax;
+    uint32_t* buf_prev = (a.scratch ? a.scratch + static_cast<size_t>(gw) * 2 * a.pmax
+                                    : smem + static_cast<size_t>(warp) * 2 * a.pmax);
+    uint32_t* buf_cur = buf_prev + a.pmax;
 
     // SN: canonical slot and sign of (dx, dy) (sgm.cpp:72-80).
     int slot = 0, sign = 1;
@@ -97,98 +94,156 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
             }
         }
     }
+    const bool sn = VARIANT == FMVS_SGM_SURFACE_NORMAL && a.offsets != nullptr;
+    const int w = a.w, h = a.h;
+    const V phi1 = static_cast<V>(a.phi1);
+
+    // 2-deep software pipeline over the line: per-pixel operands of the
+    // current (0) and next (1) pixel are in registers; the first cost chunk
+    // of the next pixel and the operands of the one after are loaded while
+    // the current pixel's recurrence runs.
+    auto inside = [&](int xx, int yy) { return xx >= 0 && yy >= 0 && xx < w && yy < h; };
+    VolMeta m0{0u, 0u}, m1{0u, 0u};
+    uint64_t rb0 = 0, rb1 = 0;
+    int img0 = 0, img1 = 0, off0 = 0, off1 = 0;
+    bool v0 = inside(x, y), v1 = inside(x + dx, y + dy);
+    if (v0) {
+        const size_t p = static_cast<size_t>(y) * w + x;
+        m0 = a.meta[p];
+        rb0 = a.row_base[y];
+        img0 = a.image[p];
+        if (sn)
+            off0 = a.offsets[4 * p + slot];
+    }
+    if (v1) {
+        const size_t p = static_cast<size_t>(y + dy) * w + x + dx;
+        m1 = a.meta[p];
+        rb1 = a.row_base[y + dy];
+        img1 = a.image[p];
+        if (sn)
+            off1 = a.offsets[4 * p + slot];
+    }
+    uint32_t cost0 = 0;
+    if (v0 && lane < meta_count(m0.fc))
+        cost0 = a.costs[rb0 + m0.rel + lane];
 
     bool has_prev = false;
-    int prev_first = 0, prev_count = 0, px = 0, py = 0;
-    uint32_t prev_min = 0;
+    int prev_first = 0, prev_count = 0, img_prev = 0;
+    V prev_min = 0;
     // PG history (sgm.cpp:28-43)
     bool h1 = false, h2 = false;
     D3 p1{0, 0, 0}, p2{0, 0, 0};
     int h1_index = 0;
 
-    while (x >= 0 && y >= 0 && x < a.w && y < a.h) {
-        const size_t p = static_cast<size_t>(y) * a.w + x;
-        const VolMeta m = a.meta[p];
-        const int f = meta_first(m.fc);
-        const int c = meta_count(m.fc);
+    while (v0) {
+        // ---- prefetch: cost chunk 0 of pixel k+1, operands of pixel k+2
+        const int x2 = x + 2 * dx, y2 = y + 2 * dy;
+        const bool v2 = inside(x2, y2);
+        VolMeta m2{0u, 0u};
+        uint64_t rb2 = 0;
+        int img2 = 0, off2 = 0;
+        if (v2) {
+            const size_t p = static_cast<size_t>(y2) * w + x2;
+            m2 = a.meta[p];
+            rb2 = a.row_base[y2];
+            img2 = a.image[p];
+            if (sn)
+                off2 = a.offsets[4 * p + slot];
+        }
+        uint32_t cost1 = 0;
+        if (v1 && lane < meta_count(m1.fc))
+            cost1 = a.costs[rb1 + m1.rel + lane];
+
+        // ---- recurrence of pixel k (walk_line, sgm.cpp:97-195)
+        const int f = meta_first(m0.fc);
+        const int c = meta_count(m0.fc);
         if (c == 0) {
             has_prev = false;
             h1 = h2 = false;
-            x += dx;
-            y += dy;
-            continue;
-        }
-        const uint64_t base = a.row_base[y] + m.rel;
-        long long phi2 = 0;
-        int shift = 0;
-        if (has_prev) {
-            const int di = abs(int(a.image[p]) - int(a.image[static_cast<size_t>(py) * a.w + px]));
-            phi2 = a.phi2_lut[di];
-            if (VARIANT == FMVS_SGM_SURFACE_NORMAL && a.offsets) {
-                shift = sign * int(a.offsets[4 * p + slot]);
-            } else if (VARIANT == FMVS_SGM_PATH_GRADIENT && h1 && h2) {
-                const D3 pred = add3(p1, sub3(p1, p2));
-                const double delta_pred = -dot3(D3{a.nx, a.ny, a.nz}, pred);
-                if (delta_pred > 0.0) {
-                    const int pi = dev::nearest_index(a.planes, a.nplanes, delta_pred);
-                    shift = min(max(h1_index - pi, -3), 3);
+        } else {
+            const uint64_t base = rb0 + m0.rel;
+            V phi2 = 0;
+            int shift = 0;
+            if (has_prev) {
+                phi2 = static_cast<V>(a.phi2_lut[abs(img0 - img_prev)]);
+                if (sn) {
+                    shift = sign * off0;
+                } else if (VARIANT == FMVS_SGM_PATH_GRADIENT && h1 && h2) {
+                    const D3 pred = add3(p1, sub3(p1, p2));
+                    const double delta_pred = -dot3(D3{a.nx, a.ny, a.nz}, pred);
+                    if (delta_pred > 0.0) {
+                        const int pi = dev::nearest_index(a.planes, a.nplanes, delta_pred);
+                        shift = min(max(h1_index - pi, -3), 3);
+                    }
                 }
             }
-        }
-        uint32_t run_min = 0xFFFFFFFFu;
-        int run_arg = 0x7FFFFFFF;
-        const long long lo = prev_first, hi = prev_first + prev_count;
-        for (int i0 = 0; i0 < c; i0 += 32) {
-            const int i = i0 + lane;
-            if (i < c) {
-                const uint32_t s = a.costs[base + i];
-                uint32_t v;
-                if (!has_prev) {
-                    v = s;
+            const V base_best = prev_min + phi2;
+            const int toff = f + shift - prev_first;  // index of hypothesis 0 in prev
+            uint32_t run_min = 0xFFFFFFFFu;
+            int run_arg = 0x7FFFFFFF;
+            for (int i0 = 0; i0 < c; i0 += 32) {
+                const int i = i0 + lane;
+                if (i < c) {
+                    const uint32_t s = i0 == 0 ? cost0 : a.costs[base + i];
+                    uint32_t v;
+                    if (!has_prev) {
+                        v = s;
+                    } else {
+                        const int t = toff + i;
+                        V best = base_best;
+                        if (static_cast<unsigned>(t) < static_cast<unsigned>(prev_count))
+                            best = min(best, static_cast<V>(buf_prev[t]));
+                        if (static_cast<unsigned>(t - 1) < static_cast<unsigned>(prev_count))
+                            best = min(best, static_cast<V>(buf_prev[t - 1]) + phi1);
+                        if (static_cast<unsigned>(t + 1) < static_cast<unsigned>(prev_count))
+                            best = min(best, static_cast<V>(buf_prev[t + 1]) + phi1);
+                        v = static_cast<uint32_t>(static_cast<V>(s) + best - prev_min);
+                    }
+                    buf_cur[i] = v;
+                    atomicAdd(a.agg + base + i, v);
+                    if (v < run_min) {
+                        run_min = v;
+                        run_arg = i;
+                    }
+                }
+            }
+            const uint32_t nmin = __reduce_min_sync(0xFFFFFFFFu, run_min);
+            prev_min = static_cast<V>(nmin);
+            if (VARIANT == FMVS_SGM_PATH_GRADIENT) {
+                // lowest index attaining the minimum (sgm.cpp:166-174)
+                const int arg = __reduce_min_sync(0xFFFFFFFFu, run_min == nmin ? run_arg : 0x7FFFFFFF);
+                D3 pt;
+                if (scene_point(a.intr, a.nx, a.ny, a.nz, a.planes[f + arg], x, y, &pt)) {
+                    h2 = h1;
+                    p2 = p1;
+                    h1 = true;
+                    p1 = pt;
+                    h1_index = f + arg;
                 } else {
-                    const long long t = static_cast<long long>(f) + i + shift;
-                    long long best = static_cast<long long>(prev_min) + phi2;
-                    if (t >= lo && t < hi)
-                        best = min(best, static_cast<long long>(buf_prev[t - lo]));
-                    if (t - 1 >= lo && t - 1 < hi)
-                        best = min(best, static_cast<long long>(buf_prev[t - 1 - lo]) + a.phi1);
-                    if (t + 1 >= lo && t + 1 < hi)
-                        best = min(best, static_cast<long long>(buf_prev[t + 1 - lo]) + a.phi1);
-                    v = static_cast<uint32_t>(static_cast<long long>(s) + best -
-                                              static_cast<long long>(prev_min));
-                }
-                buf_cur[i] = v;
-                atomicAdd(a.agg + base + i, v);
-                if (v < run_min) {
-                    run_min = v;
-                    run_arg = i;
+                    h1 = h2 = false;
                 }
             }
+            __syncwarp();
+            uint32_t* tmp = buf_prev;
+            buf_prev = buf_cur;
+            buf_cur = tmp;
+            has_prev = true;
+            prev_first = f;
+            prev_count = c;
+            img_prev = img0;
         }
-        prev_min = __reduce_min_sync(0xFFFFFFFFu, run_min);
-        if (VARIANT == FMVS_SGM_PATH_GRADIENT) {
-            // lowest index attaining the minimum (sgm.cpp:166-174)
-            const int arg = __reduce_min_sync(0xFFFFFFFFu, run_min == prev_min ? run_arg : 0x7FFFFFFF);
-            D3 pt;
-            if (scene_point(a.intr, a.nx, a.ny, a.nz, a.planes[f + arg], x, y, &pt)) {
-                h2 = h1;
-                p2 = p1;
-                h1 = true;
-                p1 = pt;
-                h1_index = f + arg;
-            } else {
-                h1 = h2 = false;
-            }
-        }
-        __syncwarp();
-        uint32_t* tmp = buf_prev;
-        buf_prev = buf_cur;
-        buf_cur = tmp;
-        has_prev = true;
-        prev_first = f;
-        prev_count = c;
-        px = x;
-        py = y;
+        // ---- rotate the pipeline
+        m0 = m1;
+        rb0 = rb1;
+        img0 = img1;
+        off0 = off1;
+        cost0 = cost1;
+        v0 = v1;
+        m1 = m2;
+        rb1 = rb2;
+        img1 = img2;
+        off1 = off2;
+        v1 = v2;
         x += dx;
         y += dy;
     }
@@ -247,6 +302,21 @@ __global__ void normal_offsets_kernel(OffsetArgs a) {
 
 }  // namespace
 
+template <int VARIANT>
+void launch_sgm(const SgmArgs& a, int total, int blocks, size_t smem, bool fast32, cudaStream_t s) {
+    if (fast32) {
+        FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_kernel<VARIANT, int>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+        sgm_kernel<VARIANT, int><<<blocks, kWarps * 32, smem, s>>>(a, total);
+    } else {
+        FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_kernel<VARIANT, long long>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+        sgm_kernel<VARIANT, long long><<<blocks, kWarps * 32, smem, s>>>(a, total);
+    }
+}
+
 void sgm(const SgmArgs& a, cudaStream_t s) {
     int total = 0;
     for (int d = 0; d < a.ndirs; ++d) {
@@ -257,24 +327,19 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
         return;
     const int blocks = (total + kWarps - 1) / kWarps;
     const size_t smem = a.scratch ? 0 : static_cast<size_t>(kWarps) * 2 * a.pmax * sizeof(uint32_t);
+    // int32 recurrence is exact when every intermediate stays below 2^31:
+    // path values <= 65535 + phi2_max, candidates <= value + max(phi1, phi2).
+    const bool fast32 = a.phi1 >= 0 && a.phi2_max >= 0 && a.phi1 < (1ll << 28) &&
+                        a.phi2_max < (1ll << 28);
     switch (a.variant) {
         case FMVS_SGM_SURFACE_NORMAL:
-            FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_kernel<FMVS_SGM_SURFACE_NORMAL>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem)));
-            sgm_kernel<FMVS_SGM_SURFACE_NORMAL><<<blocks, kWarps * 32, smem, s>>>(a, total);
+            launch_sgm<FMVS_SGM_SURFACE_NORMAL>(a, total, blocks, smem, fast32, s);
             break;
         case FMVS_SGM_PATH_GRADIENT:
-            FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_kernel<FMVS_SGM_PATH_GRADIENT>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem)));
-            sgm_kernel<FMVS_SGM_PATH_GRADIENT><<<blocks, kWarps * 32, smem, s>>>(a, total);
+            launch_sgm<FMVS_SGM_PATH_GRADIENT>(a, total, blocks, smem, fast32, s);
             break;
         default:
-            FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_kernel<FMVS_SGM_PLANE>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem)));
-            sgm_kernel<FMVS_SGM_PLANE><<<blocks, kWarps * 32, smem, s>>>(a, total);
+            launch_sgm<FMVS_SGM_PLANE>(a, total, blocks, smem, fast32, s);
             break;
     }
     FMVS_CUDA_CHECK(cudaGetLastError());

@@ -440,17 +440,26 @@ __device__ __forceinline__ int bit_to_pos(int bi) {
 }
 
 constexpr int kItemCap = 1024;
+constexpr int kPlaneChunk = 16;  // tile parameters computed for this many planes at once
 
-template <int WW, int WH>
-__global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a) {
+struct ViewConst {
+    const uint32_t* quad;
+    const double* homs;  // homs of this view, plane 0
+    int w, h;
+    int left;            // 1 if the view lies left of the reference
+};
+
+template <int WW, int WH, int NM>
+__global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_census_tiled(SweepArgs a) {
     using namespace dev;
     using BitsT = typename std::conditional<(WW * WH - 1 > 32), uint64_t, uint32_t>::type;
     using Scan = cub::BlockScan<int, kTiledThreads>;
     constexpr int RX = WW / 2, RY = WH / 2;
     constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
     constexpr int CENTER = (WW * WH) / 2;
-    extern __shared__ float2 s_tile[];  // [nmatch][SH][SW] (value, bound)
-    __shared__ TileParams s_tp[kMaxMatch];
+    extern __shared__ float2 s_tile[];  // [NM][SH][SW] (value, bound) of the warped tile + halo
+    __shared__ TileParams s_tp[kPlaneChunk][NM];
+    __shared__ ViewConst s_vc[NM];
     __shared__ int s_pmin, s_pmax;
     __shared__ typename Scan::TempStorage s_scan;
     __shared__ uint32_t s_items[kItemCap];  // (thread, view, window position)
@@ -462,7 +471,8 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
     const bool in_img = x < a.w && y < a.h;
 
     int first = 0, count = 0;
-    uint64_t base = 0, ref_bits = 0;
+    uint64_t base = 0;
+    BitsT ref_bits = 0;
     if (in_img) {
         const VolMeta m = a.meta[static_cast<size_t>(y) * a.w + x];
         first = meta_first(m.fc);
@@ -487,6 +497,12 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
         s_pmin = 0x7FFFFFFF;
         s_pmax = -1;
     }
+    if (threadIdx.x < NM) {
+        const int m = threadIdx.x;
+        const int2 sz = a.sizes[m];
+        s_vc[m] = ViewConst{a.quads[m], a.homs + static_cast<size_t>(m) * a.nplanes * 9, sz.x, sz.y,
+                            m < a.nleft ? 1 : 0};
+    }
     __syncthreads();
     if (count > 0) {
         atomicMin(&s_pmin, first);
@@ -494,36 +510,42 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
     }
     __syncthreads();
     const int pmin = s_pmin, pmax = s_pmax;
-    const int nm = a.nmatch;
     const double xd = double(x), yd = double(y);
 
     for (int p = pmin; p <= pmax; ++p) {
         const bool need = count > 0 && p >= first && p < first + count;
+        const int slot = (p - pmin) % kPlaneChunk;
+        if (slot == 0) {
+            // tile parameters of the next kPlaneChunk planes x NM views, in parallel
+            __syncthreads();
+            for (int k = threadIdx.x; k < kPlaneChunk * NM; k += kTiledThreads) {
+                const int pp = p + k / NM, m = k % NM;
+                if (pp <= pmax)
+                    s_tp[k / NM][m] = make_tile_params(s_vc[m].homs + static_cast<size_t>(pp) * 9,
+                                                       x0 - RX, y0 - RY, SW - 1, SH - 1);
+            }
+        }
         if (!__syncthreads_or(need))
             continue;
-        if (threadIdx.x < nm)
-            s_tp[threadIdx.x] = make_tile_params(
-                a.homs + (static_cast<size_t>(threadIdx.x) * a.nplanes + p) * 9, x0 - RX, y0 - RY,
-                SW - 1, SH - 1);
-        __syncthreads();
         // ---- warp the tile + halo of every matching view into shared memory
-        for (int s = threadIdx.x; s < nm * SN; s += kTiledThreads) {
+#pragma unroll 2
+        for (int s = threadIdx.x; s < NM * SN; s += kTiledThreads) {
             const int m = s / SN, r = s - m * SN;
             const int dv = r / SW, du = r - dv * SW;
-            const TileParams tp = s_tp[m];
+            const TileParams& tp = s_tp[slot][m];
             float2 out = make_float2(0.0f, 1e30f);
             if (!tp.exact) {
                 float tcx, tcy;
                 tile_coords(tp, float(du), float(dv), &tcx, &tcy);
-                const int2 sz = a.sizes[m];
+                const ViewConst& vc = s_vc[m];
                 const float fx = floorf(tcx), fy = floorf(tcy);
                 int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
                 float ax = tcx - fx, ay = tcy - fy;
                 if (X0 < 0) { X0 = 0; ax = 0.0f; }
-                else if (X0 >= sz.x - 1) { X0 = sz.x - 1; ax = 0.0f; }
+                else if (X0 >= vc.w - 1) { X0 = vc.w - 1; ax = 0.0f; }
                 if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
-                else if (Y0 >= sz.y - 1) { Y0 = sz.y - 1; ay = 0.0f; }
-                const uint32_t q = __ldg(a.quads[m] + static_cast<size_t>(Y0) * sz.x + X0);
+                else if (Y0 >= vc.h - 1) { Y0 = vc.h - 1; ay = 0.0f; }
+                const uint32_t q = __ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0);
                 const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
                 const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
                 const float top = fmaf(ax, i10 - i00, i00);
@@ -538,45 +560,43 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
             s_tile[s] = out;
         }
         __syncthreads();
-        // ---- pass 1: FP32 census bits + undecided-bit masks per view
-        BitsT bits[kMaxMatch], uns[kMaxMatch];
+        // ---- pass 1: FP32 census bits; undecided-bit masks only where needed
+        BitsT bits[NM], uns[NM];
         uint32_t view_out = 0;    // bit m: window centre outside the view -> 255
         uint32_t view_exact = 0;  // bit m: certification impossible -> exact path
         int my_items = 0;
 #pragma unroll
-        for (int m = 0; m < kMaxMatch; ++m) {
+        for (int m = 0; m < NM; ++m) {
             bits[m] = 0;
             uns[m] = 0;
-            if (!need || m >= nm)
+            if (!need)
                 continue;
-            const TileParams& tp = s_tp[m];
+            const TileParams& tp = s_tp[slot][m];
             if (tp.exact) {
                 view_exact |= 1u << m;
                 continue;
             }
-            const int2 sz = a.sizes[m];
+            const ViewConst& vc = s_vc[m];
             // inside test of the window centre (matching.cpp:224-231), certified
             float tcx, tcy;
             tile_coords(tp, float(tx + RX), float(ty + RY), &tcx, &tcy);
-            const double X = double(tp.xa) + double(tcx), Y = double(tp.ya) + double(tcy);
-            const double ddx = tp.dx, ddy = tp.dy;
+            const float xlo = float(-tp.xa), xhi = float(vc.w - 1 - tp.xa);
+            const float ylo = float(-tp.ya), yhi = float(vc.h - 1 - tp.ya);
             bool inside;
-            if (X - ddx >= 0.0 && Y - ddy >= 0.0 && X + ddx <= double(sz.x - 1) &&
-                Y + ddy <= double(sz.y - 1))
-                inside = true;
-            else if (X + ddx < 0.0 || Y + ddy < 0.0 || X - ddx > double(sz.x - 1) ||
-                     Y - ddy > double(sz.y - 1))
+            if (tcx - tp.dx >= xlo && tcy - tp.dy >= ylo && tcx + tp.dx <= xhi && tcy + tp.dy <= yhi)
+                inside = true;  // (float ops above are exact or err toward ambiguity)
+            else if (tcx + tp.dx < xlo || tcy + tp.dy < ylo || tcx - tp.dx > xhi || tcy - tp.dy > yhi)
                 inside = false;
             else
-                inside = exact_inside(a.homs + (static_cast<size_t>(m) * a.nplanes + p) * 9, sz.x,
-                                      sz.y, xd, yd);
+                inside = exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd);
             if (!inside) {
                 view_out |= 1u << m;
                 continue;
             }
             const float2* t = s_tile + m * SN;
             const float2 c = t[(ty + RY) * SW + tx + RX];
-            BitsT b = 0, u = 0;
+            BitsT b = 0;
+            float margin = 3.0e38f;
 #pragma unroll
             for (int i = 0; i < WH; ++i)
 #pragma unroll
@@ -585,18 +605,30 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
                         continue;
                     const float2 n = t[(ty + i) * SW + tx + j];
                     const float d = n.x - c.x;
-                    b = (b << 1) | (d < 0.0f ? 1u : 0u);
-                    u = (u << 1) | (fabsf(d) > n.y + c.y ? 0u : 1u);
+                    b = (b << 1) | static_cast<BitsT>(__float_as_uint(d) >> 31);
+                    margin = fminf(margin, fabsf(d) - n.y);
                 }
             bits[m] = b;
-            uns[m] = u;
-            if (u)
-                my_items += 1 + popcount_bits(u);
+            if (margin <= c.y) {
+                BitsT u = 0;
+#pragma unroll
+                for (int i = 0; i < WH; ++i)
+#pragma unroll
+                    for (int j = 0; j < WW; ++j) {
+                        if (i * WW + j == CENTER)
+                            continue;
+                        const float2 n = t[(ty + i) * SW + tx + j];
+                        u = (u << 1) | (fabsf(n.x - c.x) > n.y + c.y ? 0u : 1u);
+                    }
+                uns[m] = u;
+                if (u)
+                    my_items += 1 + popcount_bits(u);
+            }
             if (a.stats) {
                 atomicAdd(a.stats + 0, 1ull);
-                if (u) {
+                if (uns[m]) {
                     atomicAdd(a.stats + 1, 1ull);
-                    atomicAdd(a.stats + 2, static_cast<unsigned long long>(popcount_bits(u)));
+                    atomicAdd(a.stats + 2, static_cast<unsigned long long>(popcount_bits(uns[m])));
                 }
             }
         }
@@ -606,7 +638,7 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
         if (my_items) {
             int k = off;
 #pragma unroll
-            for (int m = 0; m < kMaxMatch; ++m) {
+            for (int m = 0; m < NM; ++m) {
                 if (!uns[m])
                     continue;
                 if (k < kItemCap)
@@ -628,35 +660,34 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
         for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
             const uint32_t item = s_items[it];
             const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = item >> 12;
-            const int2 sz = a.sizes[m];
-            s_vals[it] = exact_window_sample(a.homs + (static_cast<size_t>(m) * a.nplanes + p) * 9,
-                                             a.quads[m], sz.x, sz.y, double(x0 + t % kTW),
-                                             double(y0 + t / kTW), RX, RY, pos / WW, pos % WW);
+            const ViewConst& vc = s_vc[m];
+            s_vals[it] = exact_window_sample(vc.homs + static_cast<size_t>(p) * 9, vc.quad, vc.w,
+                                             vc.h, double(x0 + t % kTW), double(y0 + t / kTW), RX,
+                                             RY, pos / WW, pos % WW);
         }
         __syncthreads();
         // ---- pass 3: resolve undecided bits, per-side sums, min -> u16
         if (need) {
             int sum_l = 0, sum_r = 0, k = off;
 #pragma unroll
-            for (int m = 0; m < kMaxMatch; ++m) {
-                if (m >= nm)
-                    continue;
-                const int2 sz = a.sizes[m];
-                const double* hp = a.homs + (static_cast<size_t>(m) * a.nplanes + p) * 9;
+            for (int m = 0; m < NM; ++m) {
+                const ViewConst& vc = s_vc[m];
                 int cost;
                 if ((view_exact >> m) & 1u) {
                     if (a.stats)
                         atomicAdd(a.stats + 3, 1ull);
-                    cost = view_cost<FMVS_COST_CENSUS, WW, WH>(a.quads[m], sz.x, sz.y, hp, xd, yd,
-                                                              ref_bits, nullptr, 0.0, 0.0,
+                    cost = view_cost<FMVS_COST_CENSUS, WW, WH>(vc.quad, vc.w, vc.h,
+                                                              vc.homs + static_cast<size_t>(p) * 9,
+                                                              xd, yd, ref_bits, nullptr, 0.0, 0.0,
                                                               a.census_lut);
                 } else if ((view_out >> m) & 1u) {
                     cost = 255;
                 } else {
                     BitsT b = bits[m];
                     if (uns[m]) {
+                        const double* hp = vc.homs + static_cast<size_t>(p) * 9;
                         const double wc = k < kItemCap ? s_vals[k]
-                                                       : exact_window_sample(hp, a.quads[m], sz.x, sz.y,
+                                                       : exact_window_sample(hp, vc.quad, vc.w, vc.h,
                                                                              xd, yd, RX, RY, RY, RX);
                         ++k;
                         BitsT u = uns[m];
@@ -666,16 +697,16 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
                             const int pos = bit_to_pos<WW, WH>(bi);
                             const double v = k < kItemCap
                                                  ? s_vals[k]
-                                                 : exact_window_sample(hp, a.quads[m], sz.x, sz.y, xd,
-                                                                       yd, RX, RY, pos / WW, pos % WW);
+                                                 : exact_window_sample(hp, vc.quad, vc.w, vc.h, xd, yd,
+                                                                       RX, RY, pos / WW, pos % WW);
                             ++k;
                             const BitsT one = 1;
                             b = v < wc ? (b | (one << bi)) : (b & ~(one << bi));
                         }
                     }
-                    cost = a.census_lut[popcount_bits(b ^ static_cast<BitsT>(ref_bits))];
+                    cost = a.census_lut[popcount_bits(b ^ ref_bits)];
                 }
-                if (m < a.nleft)
+                if (vc.left)
                     sum_l += cost;
                 else
                     sum_r += cost;
@@ -685,7 +716,26 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
             if (a.agg_zero)
                 a.agg_zero[o] = 0u;
         }
-        __syncthreads();
+    }
+}
+
+template <int WW, int WH, int NM>
+void launch_tiled_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
+    const size_t smem = sizeof(float2) * NM * (kTW + WW - 1) * (kTH + WH - 1);
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_census_tiled<WW, WH, NM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    sweep_census_tiled<WW, WH, NM><<<grid, kTiledThreads, smem, s>>>(a);
+}
+
+template <int WW, int WH>
+bool launch_tiled(const SweepArgs& a, dim3 grid, cudaStream_t s) {
+    switch (a.nmatch) {
+        case 2: launch_tiled_nm<WW, WH, 2>(a, grid, s); return true;
+        case 4: launch_tiled_nm<WW, WH, 4>(a, grid, s); return true;
+        case 6: launch_tiled_nm<WW, WH, 6>(a, grid, s); return true;
+        case 8: launch_tiled_nm<WW, WH, 8>(a, grid, s); return true;
+        default: return false;
     }
 }
 
@@ -693,7 +743,8 @@ __global__ void __launch_bounds__(kTiledThreads) sweep_census_tiled(SweepArgs a)
 
 void sweep(const SweepArgs& a_in, cudaStream_t s) {
     SweepArgs a = a_in;
-    const bool tiled = a.kind == FMVS_COST_CENSUS && !a.disable_tiled && a.nmatch <= kMaxMatch;
+    const bool tiled = a.kind == FMVS_COST_CENSUS && !a.disable_tiled &&
+                       (a.nmatch == 2 || a.nmatch == 4 || a.nmatch == 6 || a.nmatch == 8);
     a.exact_above = tiled ? kNarrowMax : 0;
     const dim3 grid((a.w + kSeg - 1) / kSeg, a.h);
     if (a.kind == FMVS_COST_CENSUS && a.ww == 5)
@@ -708,13 +759,10 @@ void sweep(const SweepArgs& a_in, cudaStream_t s) {
     if (!tiled)
         return;
     const dim3 tgrid((a.w + kTW - 1) / kTW, (a.h + kTH - 1) / kTH);
-    if (a.ww == 5) {
-        const size_t smem = sizeof(float2) * a.nmatch * (kTW + 4) * (kTH + 4);
-        sweep_census_tiled<5, 5><<<tgrid, kTiledThreads, smem, s>>>(a);
-    } else {
-        const size_t smem = sizeof(float2) * a.nmatch * (kTW + 8) * (kTH + 6);
-        sweep_census_tiled<9, 7><<<tgrid, kTiledThreads, smem, s>>>(a);
-    }
+    if (a.ww == 5)
+        launch_tiled<5, 5>(a, tgrid, s);
+    else
+        launch_tiled<9, 7>(a, tgrid, s);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -97,6 +97,7 @@ struct SgmArgs {
     int variant;
     long long phi1;
     const long long* phi2_lut;       // [256] device
+    long long phi2_max;              // max of the LUT (host), selects the int32 path
     const int16_t* offsets;          // SN shifts (4 per pixel) or null
     // PG (scene points)
     dev::Intr intr;
