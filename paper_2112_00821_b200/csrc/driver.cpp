@@ -122,6 +122,19 @@ struct Tmp {
 
 fmvs::V3 v3(const double* n) { return {n[0], n[1], n[2]}; }
 
+// Lanes per scanline of the grouped SGM kernel at the refined levels
+// (FMVS_SGM_G = 8 / 16 / 32; results are identical, only speed differs).
+int sgm_group() {
+    if (const char* e = std::getenv("FMVS_SGM_G")) {
+        const int g = std::atoi(e);
+        if (g == 8 || g == 16 || g == 32)
+            return g;
+        if (g == 0)
+            return 0;
+    }
+    return 8;
+}
+
 fmvs::dev::Intr intr_of(const fmvs_intrinsics& k) { return fmvs::dev::make_intr(k); }
 
 // Host plan of one level (everything data-independent).
@@ -439,10 +452,10 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
     }
     int pmax_smem_limit = (200 * 1024) / (4 * 2 * 4);
     uint32_t* sgm_scratch = nullptr;
-    if (max_p > pmax_smem_limit) {
+    {
         size_t lines = 0;
         for (auto& P : lv)
-            lines = std::max(lines, static_cast<size_t>(4 * (P.w + P.h) + 4 * (P.w + P.h - 1)));
+            lines = std::max(lines, static_cast<size_t>(k::sgm_total_lines(P.w, P.h, 8)));
         sgm_scratch = ctx->buf("sgm_scratch").as<uint32_t>(lines * 2 * max_p);
     }
 
@@ -560,7 +573,11 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
             ga.dirs[d][1] = kDirs[d][1];
         }
         ga.pmax = np;
-        ga.scratch = np > pmax_smem_limit ? sgm_scratch : nullptr;
+        // coarsest level: dense ranges, one line per warp-wide group; refined
+        // levels: ~12 hypotheses per pixel, 32/G lines per warp
+        ga.group = variant == FMVS_SGM_PATH_GRADIENT ? 0 : (l == L - 1 ? 32 : sgm_group());
+        ga.group_caps = l == L - 1 ? std::min(np, 1024) : 32;
+        ga.scratch = (ga.group > 0 || np > pmax_smem_limit) ? sgm_scratch : nullptr;
         ctx->timed(l == 0 ? "sgm_l0" : "sgm", [&] { k::sgm(ga, s); });
         ++launches;
 
@@ -1189,9 +1206,11 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
             ga.offsets = oa.out;
         }
         ga.pmax = pmax;
+        ga.group = cfg->variant == FMVS_SGM_PATH_GRADIENT ? 0 : sgm_group();
+        ga.group_caps = 32;
         const int limit = (200 * 1024) / (4 * 2 * 4);
-        if (pmax > limit) {
-            const size_t lines = 8 * static_cast<size_t>(w + h);
+        if (pmax > limit || ga.group > 0) {
+            const size_t lines = static_cast<size_t>(k::sgm_total_lines(w, h, 8));
             ga.scratch = t.alloc<uint32_t>(lines * 2 * pmax);
         }
         if (total > 0)

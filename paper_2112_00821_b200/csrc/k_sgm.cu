@@ -249,6 +249,188 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
     }
 }
 
+// Grouped variant (Plane / SurfaceNormal): 32/G scanlines per warp, G lanes
+// per line. At the refined levels a pixel has ~12 hypotheses, so packing
+// lines amortises the per-step bookkeeping (operand prefetch, REDUX, pipeline
+// rotation) over several lines. Each group keeps its path buffers in a small
+// shared-memory double buffer and spills pixels wider than `caps` hypotheses
+// to a per-line global buffer. The reduction is a group-masked REDUX.
+template <int VARIANT, typename V, int G>
+__global__ void __launch_bounds__(kWarps * 32) sgm_group_kernel(SgmArgs a, int total_lines,
+                                                                int caps) {
+    using namespace dev;
+    constexpr int LPW = 32 / G;
+    extern __shared__ uint32_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / G, gl = lane % G;
+    const unsigned gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (grp * G));
+    const int line = (blockIdx.x * kWarps + warp) * LPW + grp;
+    const int w = a.w, h = a.h;
+
+    int dx = 1, dy = 0, x = -1, y = -1;
+    if (line < total_lines) {
+        int rem = line, d = 0;
+        for (; d < a.ndirs; ++d) {
+            const int ddx = a.dirs[d][0], ddy = a.dirs[d][1];
+            const int n = (ddx != 0 && ddy != 0) ? h + w - 1 : (ddy == 0 ? h : w);
+            if (rem < n)
+                break;
+            rem -= n;
+        }
+        dx = a.dirs[d][0];
+        dy = a.dirs[d][1];
+        if (dy == 0) {
+            x = dx > 0 ? 0 : w - 1;
+            y = rem;
+        } else if (dx == 0) {
+            x = rem;
+            y = dy > 0 ? 0 : h - 1;
+        } else if (rem < h) {
+            x = dx > 0 ? 0 : w - 1;
+            y = rem;
+        } else {
+            const int k = rem - h;
+            x = dx > 0 ? k + 1 : k;
+            y = dy > 0 ? 0 : h - 1;
+        }
+    }
+    uint32_t* sA = smem + static_cast<size_t>(warp * LPW + grp) * 2 * caps;
+    uint32_t* sB = sA + caps;
+    uint32_t* gA = a.scratch ? a.scratch + static_cast<size_t>(line) * 2 * a.pmax : nullptr;
+    uint32_t* gB = gA ? gA + a.pmax : nullptr;
+
+    int slot = 0, sign = 1;
+    if (VARIANT == FMVS_SGM_SURFACE_NORMAL) {
+        const int cd[4][2] = {{1, 0}, {0, 1}, {1, 1}, {1, -1}};
+        for (int c = 0; c < 4; ++c) {
+            if (cd[c][0] == dx && cd[c][1] == dy) {
+                slot = c;
+                sign = 1;
+            } else if (cd[c][0] == -dx && cd[c][1] == -dy) {
+                slot = c;
+                sign = -1;
+            }
+        }
+    }
+    const bool sn = VARIANT == FMVS_SGM_SURFACE_NORMAL && a.offsets != nullptr;
+    const V phi1 = static_cast<V>(a.phi1);
+    auto inside = [&](int xx, int yy) { return xx >= 0 && yy >= 0 && xx < w && yy < h; };
+
+    VolMeta m0{0u, 0u}, m1{0u, 0u};
+    uint64_t rb0 = 0, rb1 = 0;
+    int img0 = 0, img1 = 0, off0 = 0, off1 = 0;
+    bool v0 = inside(x, y), v1 = v0 && inside(x + dx, y + dy);
+    if (v0) {
+        const size_t p = static_cast<size_t>(y) * w + x;
+        m0 = a.meta[p];
+        rb0 = a.row_base[y];
+        img0 = a.image[p];
+        if (sn)
+            off0 = a.offsets[4 * p + slot];
+    }
+    if (v1) {
+        const size_t p = static_cast<size_t>(y + dy) * w + x + dx;
+        m1 = a.meta[p];
+        rb1 = a.row_base[y + dy];
+        img1 = a.image[p];
+        if (sn)
+            off1 = a.offsets[4 * p + slot];
+    }
+    uint32_t cost0 = 0;
+    if (v0 && gl < meta_count(m0.fc))
+        cost0 = a.costs[rb0 + m0.rel + gl];
+
+    bool has_prev = false;
+    int prev_first = 0, prev_count = 0, img_prev = 0;
+    V prev_min = 0;
+    const uint32_t* prev = sA;
+
+    while (__any_sync(0xFFFFFFFFu, v0)) {
+        const int x2 = x + 2 * dx, y2 = y + 2 * dy;
+        const bool v2 = v1 && inside(x2, y2);
+        VolMeta m2{0u, 0u};
+        uint64_t rb2 = 0;
+        int img2 = 0, off2 = 0;
+        if (v2) {
+            const size_t p = static_cast<size_t>(y2) * w + x2;
+            m2 = a.meta[p];
+            rb2 = a.row_base[y2];
+            img2 = a.image[p];
+            if (sn)
+                off2 = a.offsets[4 * p + slot];
+        }
+        uint32_t cost1 = 0;
+        if (v1 && gl < meta_count(m1.fc))
+            cost1 = a.costs[rb1 + m1.rel + gl];
+
+        const int f = meta_first(m0.fc);
+        const int c = v0 ? meta_count(m0.fc) : 0;
+        uint32_t run_min = 0xFFFFFFFFu;
+        uint32_t* cur = nullptr;
+        if (c > 0) {
+            cur = c <= caps ? (prev == sA ? sB : sA) : (prev == gA ? gB : gA);
+            const uint64_t base = rb0 + m0.rel;
+            V phi2 = 0;
+            int shift = 0;
+            if (has_prev) {
+                phi2 = static_cast<V>(a.phi2_lut[abs(img0 - img_prev)]);
+                if (sn)
+                    shift = sign * off0;
+            }
+            const V base_best = prev_min + phi2;
+            const int toff = f + shift - prev_first;
+            for (int i0 = 0; i0 < c; i0 += G) {
+                const int i = i0 + gl;
+                if (i < c) {
+                    const uint32_t s = i0 == 0 ? cost0 : a.costs[base + i];
+                    uint32_t v;
+                    if (!has_prev) {
+                        v = s;
+                    } else {
+                        const int t = toff + i;
+                        V best = base_best;
+                        if (static_cast<unsigned>(t) < static_cast<unsigned>(prev_count))
+                            best = min(best, static_cast<V>(prev[t]));
+                        if (static_cast<unsigned>(t - 1) < static_cast<unsigned>(prev_count))
+                            best = min(best, static_cast<V>(prev[t - 1]) + phi1);
+                        if (static_cast<unsigned>(t + 1) < static_cast<unsigned>(prev_count))
+                            best = min(best, static_cast<V>(prev[t + 1]) + phi1);
+                        v = static_cast<uint32_t>(static_cast<V>(s) + best - prev_min);
+                    }
+                    cur[i] = v;
+                    atomicAdd(a.agg + base + i, v);
+                    run_min = min(run_min, v);
+                }
+            }
+        }
+        const uint32_t nmin = __reduce_min_sync(gmask, run_min);
+        __syncwarp();
+        if (c > 0) {
+            prev_min = static_cast<V>(nmin);
+            prev = cur;
+            has_prev = true;
+            prev_first = f;
+            prev_count = c;
+            img_prev = img0;
+        } else {
+            has_prev = false;
+        }
+        m0 = m1;
+        rb0 = rb1;
+        img0 = img1;
+        off0 = off1;
+        cost0 = cost1;
+        v0 = v1;
+        m1 = m2;
+        rb1 = rb2;
+        img1 = img2;
+        off1 = off2;
+        v1 = v2;
+        x += dx;
+        y += dy;
+    }
+}
+
 // compute_normal_offsets (sgm.cpp:252-299) on the upscaled prior maps.
 __global__ void normal_offsets_kernel(OffsetArgs a) {
     using namespace dev;
@@ -317,6 +499,28 @@ void launch_sgm(const SgmArgs& a, int total, int blocks, size_t smem, bool fast3
     }
 }
 
+template <int VARIANT, typename V, int G>
+void launch_group(const SgmArgs& a, int total, cudaStream_t s) {
+    constexpr int LPW = 32 / G;
+    const int caps = a.group_caps;
+    const int blocks = (total + kWarps * LPW - 1) / (kWarps * LPW);
+    const size_t smem = static_cast<size_t>(kWarps) * LPW * 2 * caps * sizeof(uint32_t);
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_group_kernel<VARIANT, V, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    sgm_group_kernel<VARIANT, V, G><<<blocks, kWarps * 32, smem, s>>>(a, total, caps);
+}
+
+template <int VARIANT, typename V>
+void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
+    if (a.group == 8)
+        launch_group<VARIANT, V, 8>(a, total, s);
+    else if (a.group == 16)
+        launch_group<VARIANT, V, 16>(a, total, s);
+    else
+        launch_group<VARIANT, V, 32>(a, total, s);
+}
+
 void sgm(const SgmArgs& a, cudaStream_t s) {
     int total = 0;
     for (int d = 0; d < a.ndirs; ++d) {
@@ -325,12 +529,28 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
     }
     if (total == 0)
         return;
-    const int blocks = (total + kWarps - 1) / kWarps;
-    const size_t smem = a.scratch ? 0 : static_cast<size_t>(kWarps) * 2 * a.pmax * sizeof(uint32_t);
     // int32 recurrence is exact when every intermediate stays below 2^31:
     // path values <= 65535 + phi2_max, candidates <= value + max(phi1, phi2).
     const bool fast32 = a.phi1 >= 0 && a.phi2_max >= 0 && a.phi1 < (1ll << 28) &&
                         a.phi2_max < (1ll << 28);
+    if (a.group > 0 && a.variant != FMVS_SGM_PATH_GRADIENT) {
+        // grouped kernel; scratch (global overflow buffers) is mandatory here
+        if (a.variant == FMVS_SGM_SURFACE_NORMAL) {
+            if (fast32)
+                launch_group_g<FMVS_SGM_SURFACE_NORMAL, int>(a, total, s);
+            else
+                launch_group_g<FMVS_SGM_SURFACE_NORMAL, long long>(a, total, s);
+        } else {
+            if (fast32)
+                launch_group_g<FMVS_SGM_PLANE, int>(a, total, s);
+            else
+                launch_group_g<FMVS_SGM_PLANE, long long>(a, total, s);
+        }
+        FMVS_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    const int blocks = (total + kWarps - 1) / kWarps;
+    const size_t smem = a.scratch ? 0 : static_cast<size_t>(kWarps) * 2 * a.pmax * sizeof(uint32_t);
     switch (a.variant) {
         case FMVS_SGM_SURFACE_NORMAL:
             launch_sgm<FMVS_SGM_SURFACE_NORMAL>(a, total, blocks, smem, fast32, s);
@@ -343,6 +563,10 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
             break;
     }
     FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+int sgm_total_lines(int w, int h, int ndirs) {
+    return ndirs == 8 ? 2 * h + 2 * w + 4 * (w + h - 1) : 2 * h + 2 * w;
 }
 
 // Largest per-warp path buffer that keeps kWarps warps in shared memory.

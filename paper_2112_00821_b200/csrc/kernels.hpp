@@ -107,9 +107,12 @@ struct SgmArgs {
     int ndirs;
     int dirs[8][2];
     int pmax;                        // per-warp path buffer length
-    uint32_t* scratch;               // global path buffers when pmax is too large for smem
+    uint32_t* scratch;               // global path buffers (2 x pmax per line)
+    int group;                       // lanes per line for Plane/SN (8, 16, 32); 0 = 1 line/warp kernel
+    int group_caps;                  // shared-memory path buffer length per line (grouped kernel)
 };
 void sgm(const SgmArgs& a, cudaStream_t s);
+int sgm_total_lines(int w, int h, int ndirs);
 
 // ---- K7: WTA + depth + parabola (sgm.cpp:333-363, pipeline.cpp:263-288) ---
 struct WtaArgs {

@@ -211,8 +211,10 @@ def _volume(planes, w, h, rng, ragged=True, max_cost=300):
 DIRS = [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1), (1, -1), (-1, 1)]
 
 
+@pytest.mark.parametrize("group", ["0", "8", "16", "32"])
 @pytest.mark.parametrize("adaptive", [False, True])
-def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive):
+def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive, group, monkeypatch):
+    monkeypatch.setenv("FMVS_SGM_G", group)
     img = rng.integers(0, 256, (9, 13)).astype(np.uint8)
     intr = Intrinsics(100.0, 100.0, 6.0, 4.0, 13, 9)
     cfg = SgmConfig(SgmVariant.Plane, 8, 7.0, adaptive, 40.0, 8.0, 10.0, 2)
@@ -224,9 +226,11 @@ def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive):
             assert_same(a.values, b.values, f"path {dx},{dy}")
 
 
+@pytest.mark.parametrize("group", ["0", "8", "32"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.SurfaceNormal, SgmVariant.PathGradient])
 @pytest.mark.parametrize("paths", [8, 4])
-def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths):
+def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths, group, monkeypatch):
+    monkeypatch.setenv("FMVS_SGM_G", group)
     w, h, planes = 37, 29, 48
     img = rng.integers(0, 256, (h, w)).astype(np.uint8)
     intr = Intrinsics(40.0, 40.0, 18.0, 14.0, w, h)
@@ -246,13 +250,17 @@ def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths):
     assert_same(b200.wta(a), oracle.wta(b), "wta")
 
 
-def test_aggregate_dense_wide(b200, oracle, rng):
-    """Dense coarsest-level shape: >32 hypotheses per pixel (multi-chunk lanes)."""
+@pytest.mark.parametrize("group", ["8", "16", "32"])
+@pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.PathGradient])
+def test_aggregate_dense_wide(b200, oracle, rng, group, variant, monkeypatch):
+    """Dense coarsest-level shape: >32 hypotheses per pixel (multi-chunk lanes,
+    global overflow buffers of the grouped kernel)."""
+    monkeypatch.setenv("FMVS_SGM_G", group)
     w, h, planes = 40, 24, 130
     img = rng.integers(0, 256, (h, w)).astype(np.uint8)
     intr = Intrinsics(40.0, 40.0, 19.5, 11.5, w, h)
     vol = _volume(planes, w, h, rng, ragged=False, max_cost=510)
-    cfg = SgmConfig(SgmVariant.PathGradient, 8, 100.0, True, 0.0, 8.0, 10.0, 2)
+    cfg = SgmConfig(variant, 8, 100.0, True, 0.0, 8.0, 10.0, 2)
     a = b200.aggregate(vol, img, cfg, intr)
     b = oracle.aggregate(vol, img, cfg, intr)
     assert_same(a.values, b.values, "aggregate")
@@ -328,8 +336,10 @@ E2E = [
 ]
 
 
+@pytest.mark.parametrize("group", ["8", "16"])
 @pytest.mark.parametrize("name,scene,cfg", E2E, ids=[e[0] for e in E2E])
-def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg):
+def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg, group, monkeypatch):
+    monkeypatch.setenv("FMVS_SGM_G", group)
     scene = dict(scene)
     kind = scene.pop("kind")
     bundle, _, _ = render(oracle, kind, **scene)
