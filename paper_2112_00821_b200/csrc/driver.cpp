@@ -519,6 +519,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         sa.wh = cfg.cost.window_h;
         sa.census_lut = d_clut;
         sa.disable_tiled = ctx->sweep_exact;
+        sa.plane_slicing = l == L - 1;  // uniform ranges: every pixel sweeps the whole stack
         if (ctx->sweep_stats)
             sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(4);
         ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { k::sweep(sa, s); });
@@ -1081,6 +1082,7 @@ int fmvs_sweep_cost_volume(fmvs_ctx* ctx, const fmvs_view* views, int32_t n, int
         sa.wh = cost->window_h;
         const std::vector<uint16_t> clut = fmvs::census_cost_table(cost->window_w * cost->window_h - 1);
         sa.census_lut = t.upload(clut.data(), clut.size(), s);
+        sa.plane_slicing = 1;
         k::sweep(sa, s);
         std::vector<fmvs::dev::VolMeta> meta(px);
         FMVS_CUDA_CHECK(cudaMemcpyAsync(meta.data(), ra.meta, px * 8, cudaMemcpyDeviceToHost, s));

@@ -509,7 +509,10 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
         atomicMax(&s_pmax, first + count - 1);
     }
     __syncthreads();
-    const int pmin = s_pmin, pmax = s_pmax;
+    // plane slice of this CTA (gridDim.z > 1 splits dense levels across CTAs)
+    const int slice = (a.nplanes + gridDim.z - 1) / gridDim.z;
+    const int pmin = max(s_pmin, static_cast<int>(blockIdx.z) * slice);
+    const int pmax = min(s_pmax, static_cast<int>(blockIdx.z + 1) * slice - 1);
     const double xd = double(x), yd = double(y);
 
     for (int p = pmin; p <= pmax; ++p) {
@@ -595,8 +598,7 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
             }
             const float2* t = s_tile + m * SN;
             const float2 c = t[(ty + RY) * SW + tx + RX];
-            BitsT b = 0;
-            float margin = 3.0e38f;
+            BitsT b = 0, u = 0;
 #pragma unroll
             for (int i = 0; i < WH; ++i)
 #pragma unroll
@@ -605,25 +607,14 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
                         continue;
                     const float2 n = t[(ty + i) * SW + tx + j];
                     const float d = n.x - c.x;
+                    // sign bit of d = (warped < centre); values are >= +0 so d is never -0
                     b = (b << 1) | static_cast<BitsT>(__float_as_uint(d) >> 31);
-                    margin = fminf(margin, fabsf(d) - n.y);
+                    u = (u << 1) | static_cast<BitsT>(fabsf(d) <= n.y + c.y);
                 }
             bits[m] = b;
-            if (margin <= c.y) {
-                BitsT u = 0;
-#pragma unroll
-                for (int i = 0; i < WH; ++i)
-#pragma unroll
-                    for (int j = 0; j < WW; ++j) {
-                        if (i * WW + j == CENTER)
-                            continue;
-                        const float2 n = t[(ty + i) * SW + tx + j];
-                        u = (u << 1) | (fabsf(n.x - c.x) > n.y + c.y ? 0u : 1u);
-                    }
-                uns[m] = u;
-                if (u)
-                    my_items += 1 + popcount_bits(u);
-            }
+            uns[m] = u;
+            if (u)
+                my_items += 1 + popcount_bits(u);
             if (a.stats) {
                 atomicAdd(a.stats + 0, 1ull);
                 if (uns[m]) {
@@ -758,7 +749,14 @@ void sweep(const SweepArgs& a_in, cudaStream_t s) {
     FMVS_CUDA_CHECK(cudaGetLastError());
     if (!tiled)
         return;
-    const dim3 tgrid((a.w + kTW - 1) / kTW, (a.h + kTH - 1) / kTH);
+    // Dense levels with few tiles: split the plane range across gridDim.z so
+    // the launch covers >= ~4 waves of 148 SMs x 3 CTAs.
+    const int tiles = ((a.w + kTW - 1) / kTW) * ((a.h + kTH - 1) / kTH);
+    int slices = 1;
+    if (a.plane_slicing)
+        while (slices < 64 && tiles * slices < 4 * 148 * 3 && a.nplanes / (2 * slices) >= 8)
+            slices *= 2;
+    const dim3 tgrid((a.w + kTW - 1) / kTW, (a.h + kTH - 1) / kTH, slices);
     if (a.ww == 5)
         launch_tiled<5, 5>(a, tgrid, s);
     else

@@ -68,6 +68,7 @@ struct SweepArgs {
     // certified census kernel, the rest to the exact per-hypothesis kernel
     int exact_above;
     int disable_tiled;               // force the exact per-hypothesis kernel
+    int plane_slicing;               // dense ranges: split planes across CTAs (grid z)
     unsigned long long* stats;       // optional diagnostics: [view-evals, unsure evals, unsure bits, exact views]
 };
 void sweep(const SweepArgs& a, cudaStream_t s);
