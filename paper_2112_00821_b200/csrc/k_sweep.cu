@@ -531,7 +531,6 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
         if (!__syncthreads_or(need))
             continue;
         // ---- warp the tile + halo of every matching view into shared memory
-#pragma unroll 2
         for (int s = threadIdx.x; s < NM * SN; s += kTiledThreads) {
             const int m = s / SN, r = s - m * SN;
             const int dv = r / SW, du = r - dv * SW;
@@ -598,7 +597,7 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
             }
             const float2* t = s_tile + m * SN;
             const float2 c = t[(ty + RY) * SW + tx + RX];
-            BitsT b = 0, u = 0;
+            BitsT b = 0, sure = 0;
 #pragma unroll
             for (int i = 0; i < WH; ++i)
 #pragma unroll
@@ -607,10 +606,14 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
                         continue;
                     const float2 n = t[(ty + i) * SW + tx + j];
                     const float d = n.x - c.x;
-                    // sign bit of d = (warped < centre); values are >= +0 so d is never -0
+                    // sign bit of d = (warped < centre); values are >= +0 so d is never -0.
+                    // sign bit of (E_n + E_c) - |d| = the comparison is certified
+                    // (|d| > E_n + E_c, exact test on floats; +0 counts as undecided).
                     b = (b << 1) | static_cast<BitsT>(__float_as_uint(d) >> 31);
-                    u = (u << 1) | static_cast<BitsT>(fabsf(d) <= n.y + c.y);
+                    sure = (sure << 1) | static_cast<BitsT>(__float_as_uint((n.y + c.y) - fabsf(d)) >> 31);
                 }
+            constexpr BitsT kAll = static_cast<BitsT>(~BitsT(0)) >> (sizeof(BitsT) * 8 - (WW * WH - 1));
+            const BitsT u = ~sure & kAll;
             bits[m] = b;
             uns[m] = u;
             if (u)
