@@ -12,12 +12,15 @@ coarsest level, census 5x5, SGM Pi-sn over 8 paths, normals + confidence.
 A step = one estimate_bundle of one bundle. Each rank runs its own stream of
 bundles (independent bundles: weak scaling, no collective on the data path).
 
-value : maps/s of the whole job, inputs resident in HBM, device-timed per
-        step with CUDA events on the library's stream, L2 flushed (256 MiB
-        memset) before every timed step; max over ranks.
-e2e   : the same metric through the public C ABI (fmvs_estimate_bundle) with
-        pinned HOST buffers: 5 images H2D + depth/normals/confidence D2H
-        inside the timed region (wall clock around the blocking calls).
+value : maps/s of the whole job: K bundles with inputs resident in HBM,
+        `--inflight` contexts (one CUDA stream each) processing bundles round
+        robin, device-timed with CUDA events (fork/join on a master stream);
+        inputs larger than L2 (a ring of 16 distinct bundles); max over ranks.
+latency_ms : one bundle alone, L2 flushed (256 MiB memset) before each step.
+e2e   : the same metric through the public blocking C ABI
+        (fmvs_estimate_bundle) from `--inflight` host threads with pinned HOST
+        buffers: 5 images H2D + depth/normals/confidence D2H inside the timed
+        region (wall clock around the calls).
 """
 from __future__ import annotations
 
@@ -147,91 +150,122 @@ def alg_bytes(stage, stats, n_views, paths):
 
 
 def run_b200(args, rank, world, device):
+    import threading as th
     import torch
     import paper_2112_00821_b200 as pkg
-    from paper_2112_00821_b200 import Backend
+    from paper_2112_00821_b200 import Backend, _abi
 
     scene, cfgkw, desc = WORKLOADS[args.workload]
     views = scene.get("views", 5)
+    dev = f"cuda:{device}"
     torch.cuda.set_device(device)
-    b200 = Backend.b200(device)
+    libpath = os.path.join(ROOT, "paper_2112_00821_b200", "_lib", "libfmvs.so")
+    if not os.path.exists(libpath):
+        raise RuntimeError("libfmvs.so not built (run __graft_entry__.build())")
+    M = max(1, args.inflight)
+    ctxs = [Backend(libpath, "fmvs_", device) for _ in range(M)]
+    b200 = ctxs[0]
     cfg = make_config(pkg, **cfgkw)
+    ccfg = cfg.to_c()
     ring = args.ring
     frames = render_frames(b200, scene, ring + views - 1)
     h, w = frames[0].image.shape
     px = w * h
-    # device-resident frames + outputs
-    d_frames = torch.from_numpy(np.stack([f.image for f in frames])).to(f"cuda:{device}")
-    d_depth = torch.empty((h, w), dtype=torch.float32, device=f"cuda:{device}")
-    d_norm = torch.empty((h, w, 3), dtype=torch.float32, device=f"cuda:{device}")
-    d_conf = torch.empty((h, w), dtype=torch.float32, device=f"cuda:{device}")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
-    stream = torch.cuda.ExternalStream(b200.fn["ctx_stream"](b200.ctx), device=f"cuda:{device}")
+    d_frames = torch.from_numpy(np.stack([f.image for f in frames])).to(dev)
+    outs = [(torch.empty((h, w), dtype=torch.float32, device=dev),
+             torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+             torch.empty((h, w), dtype=torch.float32, device=dev)) for _ in range(M)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    streams = [torch.cuda.ExternalStream(c.fn["ctx_stream"](c.ctx), device=dev) for c in ctxs]
 
-    from paper_2112_00821_b200 import _abi
-    from paper_2112_00821_b200.fassmvs import _views_c
-
-    def views_for(i, dev=True):
-        s = i % ring
+    def dev_views(i):
+        s0 = i % ring
         arr = (_abi.View_c * views)()
         for k in range(views):
-            f = frames[s + k]
-            arr[k].image = d_frames[s + k].data_ptr() if dev else f.image.ctypes.data
+            f = frames[s0 + k]
+            arr[k].image = d_frames[s0 + k].data_ptr()
             arr[k].intrinsics = f.intrinsics.to_c()
             arr[k].pose = f.pose.to_c()
         return arr
 
-    ccfg = cfg.to_c()
-    vlist = [views_for(i) for i in range(ring)]
+    vlist = [dev_views(i) for i in range(ring)]
 
-    def step(i):
-        rc = b200.fn["estimate_bundle_device"](b200.ctx, vlist[i % ring], views, C.byref(ccfg),
-                                               d_depth.data_ptr(), d_norm.data_ptr(), d_conf.data_ptr())
+    def step(ci, i):
+        c = ctxs[ci]
+        o = outs[ci]
+        rc = c.fn["estimate_bundle_device"](c.ctx, vlist[i % ring], views, C.byref(ccfg),
+                                            o[0].data_ptr(), o[1].data_ptr(), o[2].data_ptr())
         if rc != 0:
-            b200._check(rc)
+            c._check(rc)
 
-    # warmup
-    for i in range(args.warmup):
-        step(i)
-    b200._check(b200.fn["ctx_synchronize"](b200.ctx))
+    def sync_all():
+        for c in ctxs:
+            c._check(c.fn["ctx_synchronize"](c.ctx))
+
+    # warmup (every context, every ring slot touched once)
+    for i in range(max(args.warmup, 1) * M):
+        step(i % M, i)
+    sync_all()
     stats = b200.level_stats()
     launches_per_step = b200.last_launch_count()
-
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    torch.cuda.synchronize(device)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    with ClockSampler(device) as clocks:
-        for i in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.zero_()               # L2 flush, outside the timed events
-                evs[i][0].record(stream)
-            step(args.warmup + i)
-            with torch.cuda.stream(stream):
-                evs[i][1].record(stream)
-        b200._check(b200.fn["ctx_synchronize"](b200.ctx))
-        torch.cuda.synchronize(device)
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = sum(step_ms)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        dist.barrier()
-    maps_per_s = world * args.steps * 1000.0 / total_ms
     entries = sum(lv["entries"] for lv in stats)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: K bundles, M contexts in flight (round robin), device-timed
+    master = torch.cuda.Stream(device=dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ends = [torch.cuda.Event() for _ in range(M)]
+    barrier()
+    with ClockSampler(device) as clocks:
+        ev0.record(master)
+        for st in streams:
+            st.wait_event(ev0)
+        for i in range(args.steps):
+            step(i % M, args.warmup * M + i)
+        for e, st in zip(ends, streams):
+            e.record(st)
+            master.wait_event(e)
+        ev1.record(master)
+        ev1.synchronize()
+    total_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    maps_per_s = world * args.steps * 1000.0 / total_ms
+
+    # ---- latency: one bundle at a time, L2 flushed before every timed step
+    lat = []
+    s0 = streams[0]
+    for i in range(min(args.steps, 10)):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s0):
+            flush.zero_()
+            a_.record(s0)
+        step(0, i)
+        with torch.cuda.stream(s0):
+            b_.record(s0)
+        b_.synchronize()
+        lat.append(a_.elapsed_time(b_))
 
     # ---- per-stage CUDA-event timing pass (roofline of the dominant kernel)
     b200.fn["ctx_set_timing"](b200.ctx, 1)
     b200.fn["ctx_stage_reset"](b200.ctx)
-    nprof = max(3, min(args.steps, 8))
+    nprof = 5
     for i in range(nprof):
-        with torch.cuda.stream(stream):
+        with torch.cuda.stream(s0):
             flush.zero_()
-        step(i)
+        step(0, i)
         b200._check(b200.fn["ctx_synchronize"](b200.ctx))
     b200.fn["ctx_set_timing"](b200.ctx, 0)
     stages = {}
@@ -247,61 +281,71 @@ def run_b200(args, rank, world, device):
         st["gbs"] = b / (st["ms_per_step"] * 1e6) if b and st["ms_per_step"] > 0 else None
     dominant = max(stages, key=lambda n: stages[n]["ms_per_step"]) if stages else None
 
-    # ---- e2e through the public C ABI with pinned host buffers
-    hbuf_in = b200.fn["host_alloc"](px * views * ring)
-    hbuf_out = b200.fn["host_alloc"](px * 4 * 5)
-    hin = np.ctypeslib.as_array(C.cast(hbuf_in, C.POINTER(C.c_uint8)), shape=(ring, px * views))
-    frames_np = np.stack([f.image.reshape(-1) for f in frames])
+    # ---- e2e: the public blocking C ABI (fmvs_estimate_bundle) from M host
+    # threads, pinned HOST inputs/outputs, H2D + D2H inside the timed region
+    hin = b200.fn["host_alloc"](px * views * ring)
+    hout = [b200.fn["host_alloc"](px * 20) for _ in range(M)]
+    hin_np = np.ctypeslib.as_array(C.cast(hin, C.POINTER(C.c_uint8)), shape=(ring, px * views))
     host_views = []
-    for s in range(ring):
+    for s_ in range(ring):
         arr = (_abi.View_c * views)()
         for k in range(views):
-            f = frames[s + k]
-            hin[s, k * px:(k + 1) * px] = frames_np[s + k]
-            arr[k].image = hbuf_in + s * px * views + k * px
+            f = frames[s_ + k]
+            hin_np[s_, k * px:(k + 1) * px] = f.image.reshape(-1)
+            arr[k].image = hin + s_ * px * views + k * px
             arr[k].intrinsics = f.intrinsics.to_c()
             arr[k].pose = f.pose.to_c()
         host_views.append(arr)
-    o_depth, o_norm, o_conf = hbuf_out, hbuf_out + 4 * px, hbuf_out + 16 * px
 
-    def e2e_step(i):
-        rc = b200.fn["estimate_bundle"](b200.ctx, host_views[i % ring], views, C.byref(ccfg),
-                                        o_depth, o_norm, o_conf)
-        if rc != 0:
-            b200._check(rc)
+    def e2e_worker(ci, n, first_i, errs):
+        c = ctxs[ci]
+        o = hout[ci]
+        try:
+            for j in range(n):
+                rc = c.fn["estimate_bundle"](c.ctx, host_views[(first_i + j * M) % ring], views,
+                                             C.byref(ccfg), o, o + 4 * px, o + 16 * px)
+                if rc != 0:
+                    c._check(rc)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
 
-    for i in range(args.warmup):
-        e2e_step(i)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    torch.cuda.synchronize(device)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        e2e_step(i)
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    def run_e2e(nsteps):
+        errs = []
+        per = [nsteps // M + (1 if ci < nsteps % M else 0) for ci in range(M)]
+        ts = [th.Thread(target=e2e_worker, args=(ci, per[ci], ci, errs)) for ci in range(M)]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if errs:
+            raise errs[0]
+        return time.perf_counter() - t0
+
+    run_e2e(max(args.warmup, 1) * M)
+    barrier()
+    e2e_s = max_over_ranks(run_e2e(args.steps))
     e2e_maps = world * args.steps / e2e_s
-    b200.fn["host_free"](hbuf_in)
-    b200.fn["host_free"](hbuf_out)
+    b200.fn["host_free"](hin)
+    for o in hout:
+        b200.fn["host_free"](o)
 
     result = {
         "metric": METRIC, "value": round(maps_per_s, 3), "unit": "maps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u16",
         "data": "synthetic (device renderer of render.cpp value-noise plane, seed 1)",
-        "config": {"workload": desc, "bundles_in_ring": ring,
-                   "l2": "flushed before every timed step (256 MiB memset outside the events)",
-                   "parallelism": f"bundle-parallel x{world} (no collective)"},
+        "config": {"workload": desc, "bundles_in_flight": M, "bundles_in_ring": ring,
+                   "l2": (f"inputs larger than L2: ring of {ring} distinct bundles "
+                          f"({ring * views * px / 1e6:.0f} MB of frames), per-bundle working set "
+                          f"> L2; latency_ms is measured with a 256 MiB L2 flush before each step"),
+                   "parallelism": f"bundle-parallel x{world} GPUs x {M} streams (no collective)"},
         "mde_per_s": round(maps_per_s * entries / 1e6, 1),
         "entries_per_bundle": entries, "levels": stats,
+        "latency_ms": round(statistics.median(lat), 3),
         "gpu_launches": int(launches_per_step * args.steps),
         "e2e": {"value": round(e2e_maps, 3), "unit": "maps/s", "h2d_bytes_per_step": px * views,
-                "d2h_bytes_per_step": px * 20},
+                "d2h_bytes_per_step": px * 20, "host_threads": M},
         "clocks": clocks.summary(),
         "stages": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                    for k, v in stages.items()},
@@ -313,7 +357,9 @@ def run_b200(args, rank, world, device):
                               "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                               "traffic": None, "peak_source": peak_src,
                               "note": "achieved = algorithmic bytes / CUDA-event stage time; the "
-                                      "sweep is FP64-issue-bound, see DESIGN.md"}
+                                      "sweep is FP32/FP64-issue-bound, see DESIGN.md"}
+    for c in ctxs:
+        c.close()
     return result
 
 
@@ -346,7 +392,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--ring", type=int, default=8, help="distinct bundles cycled through")
+    ap.add_argument("--ring", type=int, default=16, help="distinct bundles cycled through")
+    ap.add_argument("--inflight", type=int, default=3, help="bundles in flight (contexts/streams)")
     ap.add_argument("--cpu-baseline-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
