@@ -520,6 +520,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         sa.census_lut = d_clut;
         sa.disable_tiled = ctx->sweep_exact;
         sa.plane_slicing = l == L - 1;  // uniform ranges: every pixel sweeps the whole stack
+        sa.narrow_max = l == L - 1 ? 65535 : 0;
         if (ctx->sweep_stats)
             sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(4);
         ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { k::sweep(sa, s); });
@@ -1083,6 +1084,8 @@ int fmvs_sweep_cost_volume(fmvs_ctx* ctx, const fmvs_view* views, int32_t n, int
         const std::vector<uint16_t> clut = fmvs::census_cost_table(cost->window_w * cost->window_h - 1);
         sa.census_lut = t.upload(clut.data(), clut.size(), s);
         sa.plane_slicing = 1;
+        if (const char* e = std::getenv("FMVS_SWEEP_NARROW"))
+            sa.narrow_max = std::atoi(e);
         k::sweep(sa, s);
         std::vector<fmvs::dev::VolMeta> meta(px);
         FMVS_CUDA_CHECK(cudaMemcpyAsync(meta.data(), ra.meta, px * 8, cudaMemcpyDeviceToHost, s));

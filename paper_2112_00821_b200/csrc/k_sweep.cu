@@ -449,6 +449,122 @@ struct ViewConst {
     int left;            // 1 if the view lies left of the reference
 };
 
+// FP64-coordinate variant of the tile parameters: the residual form is
+// evaluated in FP64 (3 FMA + a correctly rounded reciprocal), so the certified
+// coordinate error is ~1e-10 px and a sample's value bound collapses to the
+// FP32 bilinear arithmetic (~4e-5). Used by the NCC kernel, whose cost is a
+// smooth function of all samples and needs tight per-sample bounds.
+struct TileParams64 {
+    double ax, bx, cx, ay, by, cy, az, bz, cz;
+    float dx, dy;
+    int xa, ya;
+    int exact;
+};
+
+__device__ TileParams64 make_tile_params64(const double* __restrict__ hp, int u0, int v0,
+                                           int du_max, int dv_max) {
+    TileParams64 tp{};
+    double H[9];
+    for (int k = 0; k < 9; ++k)
+        H[k] = __ldg(hp + k);
+    const double U = u0, V = v0, DU = du_max, DV = dv_max;
+    const double q0x = H[0] * U + H[1] * V + H[2];
+    const double q0y = H[3] * U + H[4] * V + H[5];
+    const double q0z = H[6] * U + H[7] * V + H[8];
+    const double z10 = q0z + H[6] * DU, z01 = q0z + H[7] * DV, z11 = z10 + H[7] * DV;
+    const double zmin = fmin(fmin(q0z, z10), fmin(z01, z11));
+    const double two45 = 2.842170943040401e-14;   // 2^-45
+    const double two49 = 1.7763568394002505e-15;  // 2^-49
+    const double Mz = fabs(H[6]) * (fabs(U) + DU) + fabs(H[7]) * (fabs(V) + DV) + fabs(H[8]);
+    const double Mx = fabs(H[0]) * (fabs(U) + DU) + fabs(H[1]) * (fabs(V) + DV) + fabs(H[2]);
+    const double My = fabs(H[3]) * (fabs(U) + DU) + fabs(H[4]) * (fabs(V) + DV) + fabs(H[5]);
+    if (!(zmin > 64.0 * two45 * Mz) || !(q0z > 0.0)) {
+        tp.exact = 1;
+        return tp;
+    }
+    const double xa = floor(q0x / q0z), ya = floor(q0y / q0z);
+    if (!(fabs(xa) < 4.0e6) || !(fabs(ya) < 4.0e6)) {
+        tp.exact = 1;
+        return tp;
+    }
+    tp.ax = H[0] - xa * H[6];
+    tp.bx = H[1] - xa * H[7];
+    tp.cx = q0x - xa * q0z;
+    tp.ay = H[3] - ya * H[6];
+    tp.by = H[4] - ya * H[7];
+    tp.cy = q0y - ya * q0z;
+    tp.az = H[6];
+    tp.bz = H[7];
+    tp.cz = q0z;
+    const double Rx = fabs(tp.ax) * DU + fabs(tp.bx) * DV + fabs(tp.cx);
+    const double Ry = fabs(tp.ay) * DU + fabs(tp.by) * DV + fabs(tp.cy);
+    const double Rz = fabs(H[6]) * DU + fabs(H[7]) * DV + fabs(q0z);
+    // FP64 coefficient construction + FMA evaluation (generous 16 ulp) and the
+    // reference's own FP64 walk rounding (2^-45 relative to the magnitudes)
+    const double ez = two49 * (Rz + Mz) + two45 * Mz;
+    const double ex = two49 * (Rx + Mx + fabs(xa) * Mz) + two45 * (Mx + fabs(xa) * Mz);
+    const double ey = two49 * (Ry + My + fabs(ya) * Mz) + two45 * (My + fabs(ya) * Mz);
+    const double rzmin = zmin - ez;
+    if (!(rzmin > 0.0)) {
+        tp.exact = 1;
+        return tp;
+    }
+    const double Tx = (Rx + ex) / rzmin, Ty = (Ry + ey) / rzmin;
+    double dx = (ex + Tx * ez) / rzmin + two49 * Tx + 1e-12;
+    double dy = (ey + Ty * ez) / rzmin + two49 * Ty + 1e-12;
+    dx *= 1.01;
+    dy *= 1.01;
+    if (!(dx < 1e-3) || !(dy < 1e-3)) {
+        tp.exact = 1;
+        return tp;
+    }
+    tp.dx = __double2float_ru(dx);
+    tp.dy = __double2float_ru(dy);
+    tp.xa = static_cast<int>(xa);
+    tp.ya = static_cast<int>(ya);
+    tp.exact = 0;
+    return tp;
+}
+
+__device__ __forceinline__ void tile_coords64(const TileParams64& tp, double du, double dv,
+                                              double* tx, double* ty) {
+    const double rz = fma(tp.az, du, fma(tp.bz, dv, tp.cz));
+    const double rx = fma(tp.ax, du, fma(tp.bx, dv, tp.cx));
+    const double ry = fma(tp.ay, du, fma(tp.by, dv, tp.cy));
+    const double r = __drcp_rn(rz);
+    *tx = rx * r;
+    *ty = ry * r;
+}
+
+// Sample of the tile at (du, dv): FP64 residual coordinates, FP32 bilinear;
+// returns (value, bound) like the FP32-coordinate path.
+__device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const ViewConst& vc,
+                                                double du, double dv) {
+    double tx, ty;
+    tile_coords64(tp, du, dv, &tx, &ty);
+    const double fx = floor(tx), fy = floor(ty);
+    int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
+    float ax = __double2float_rn(tx - fx), ay = __double2float_rn(ty - fy);
+    if (X0 < 0) { X0 = 0; ax = 0.0f; }
+    else if (X0 >= vc.w - 1) { X0 = vc.w - 1; ax = 0.0f; }
+    if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
+    else if (Y0 >= vc.h - 1) { Y0 = vc.h - 1; ay = 0.0f; }
+    const uint32_t q = __ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0);
+    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
+    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
+    const float top = fmaf(ax, i10 - i00, i00);
+    const float bot = fmaf(ax, i11 - i01, i01);
+    const float f = fmaf(ay, bot - top, top);
+    // the float cast of (t - floor t) adds 2^-24 to the coordinate error
+    const float ddx = tp.dx + 6.0e-8f, ddy = tp.dy + 6.0e-8f;
+    const bool near_x = ax < ddx || ax > 1.0f - ddx;
+    const bool near_y = ay < ddy || ay > 1.0f - ddy;
+    const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
+    const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
+    // FP32 bilinear: 3 FMA + 2 SUB roundings on values <= 255 (< 4e-5)
+    return make_float2(f, fmaf(gx, ddx, fmaf(gy, ddy, 4.0e-5f)));
+}
+
 template <int WW, int WH, int NM>
 __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_census_tiled(SweepArgs a) {
     using namespace dev;
@@ -478,7 +594,7 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
         first = meta_first(m.fc);
         count = meta_count(m.fc);
         base = a.row_base[y] + m.rel;
-        if (count > kNarrowMax)
+        if (count > a.exact_above)
             count = 0;  // wide pixel: the exact per-hypothesis kernel owns it
         if (count > 0) {
             const uint8_t* ref = a.ref_img;  // census_bits_at (matching.cpp:28-42)
@@ -713,6 +829,341 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
     }
 }
 
+// ===================================================================
+// Tiled certified NCC sweep. Same tile warp as the census kernel; per
+// (pixel, plane, view) the window sums are taken in FP32 on centred samples,
+// and the sample bounds E are propagated rigorously to an interval of the
+// reference's FP64 cov = sab - mean*sb and var_b = sbb - sb^2/n (including
+// its own FP64 rounding), hence to an interval of 255*min(1 - ncc, 1). When
+// both ends round to the same integer the cost is certified; otherwise the
+// whole window is recomputed with the reference's exact FP64 walk (NS work
+// items, one sample per thread) and the reference's exact sum order.
+// ===================================================================
+
+constexpr int kNccItemCap = 2048;
+
+// The tail of the reference's NCC cost from its FP64 window sums
+// (matching.cpp:271-279).
+template <int NS>
+__device__ __forceinline__ int ncc_tail(double sb, double sbb, double sab, double ref_mean,
+                                        double ref_var) {
+    using namespace dev;
+    const double var_b = sub(sbb, div(mul(sb, sb), double(NS)));
+    if (var_b <= 0.0)
+        return 255;
+    const double ncc = div(sub(sab, mul(ref_mean, sb)), sqrt_(mul(ref_var, var_b)));
+    const double t = sub(1.0, ncc);
+    double cc = mul(255.0, 1.0 < t ? 1.0 : t);
+    cc = cc < 0.0 ? 0.0 : (255.0 < cc ? 255.0 : cc);
+    return static_cast<int>(lround(cc));
+}
+
+template <int WW, int WH, int NM>
+__global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a) {
+    using namespace dev;
+    using Scan = cub::BlockScan<int, kTiledThreads>;
+    constexpr int RX = WW / 2, RY = WH / 2, NS = WW * WH;
+    constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
+    extern __shared__ float2 s_tile[];  // [NM][SH][SW] (value, bound)
+    __shared__ float s_ref[SN];         // edge-clamped reference tile + halo
+    __shared__ TileParams64 s_tp[kPlaneChunk][NM];
+    __shared__ ViewConst s_vc[NM];
+    __shared__ int s_pmin, s_pmax;
+    __shared__ typename Scan::TempStorage s_scan;
+    __shared__ uint32_t s_items[kNccItemCap];
+    __shared__ double s_vals[kNccItemCap];
+    __shared__ int s_vcost[kNccItemCap / NS + 1];          // pass 2b results
+    __shared__ double s_rmean[kTiledThreads], s_rvar[kTiledThreads];
+
+    const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+    const int x = x0 + tx, y = y0 + ty;
+    const bool in_img = x < a.w && y < a.h;
+
+    for (int r = threadIdx.x; r < SN; r += kTiledThreads) {
+        const int dv = r / SW, du = r - dv * SW;
+        const int xx = min(max(x0 - RX + du, 0), a.w - 1);
+        const int yy = min(max(y0 - RY + dv, 0), a.h - 1);
+        s_ref[r] = float(a.ref_img[static_cast<size_t>(yy) * a.w + xx]);
+    }
+    int first = 0, count = 0;
+    uint64_t base = 0;
+    if (in_img) {
+        const VolMeta m = a.meta[static_cast<size_t>(y) * a.w + x];
+        first = meta_first(m.fc);
+        count = meta_count(m.fc);
+        base = a.row_base[y] + m.rel;
+        if (count > a.exact_above)
+            count = 0;  // wide pixel: the exact per-hypothesis kernel owns it
+    }
+    if (threadIdx.x == 0) {
+        s_pmin = 0x7FFFFFFF;
+        s_pmax = -1;
+    }
+    if (threadIdx.x < NM) {
+        const int m = threadIdx.x;
+        const int2 sz = a.sizes[m];
+        s_vc[m] = ViewConst{a.quads[m], a.homs + static_cast<size_t>(m) * a.nplanes * 9, sz.x, sz.y,
+                            m < a.nleft ? 1 : 0};
+    }
+    __syncthreads();
+    // reference patch mean and two-pass variance, exactly as matching.cpp:199-210
+    double ref_mean = 0.0, ref_var = 0.0;
+    float mean_f = 0.0f, var_rf = 0.0f, sar = 0.0f;
+    if (count > 0) {
+#pragma unroll
+        for (int i = 0; i < WH; ++i)
+#pragma unroll
+            for (int j = 0; j < WW; ++j)
+                ref_mean = add(ref_mean, double(s_ref[(ty + i) * SW + tx + j]));
+        ref_mean = div(ref_mean, double(NS));
+        double sabs = 0.0;
+#pragma unroll
+        for (int i = 0; i < WH; ++i)
+#pragma unroll
+            for (int j = 0; j < WW; ++j) {
+                const double d = sub(double(s_ref[(ty + i) * SW + tx + j]), ref_mean);
+                ref_var = add(ref_var, mul(d, d));
+                sabs += fabs(d);
+            }
+        mean_f = __double2float_rn(ref_mean);
+        var_rf = __double2float_rn(ref_var);
+        sar = __double2float_ru(sabs * 1.0001);
+        s_rmean[threadIdx.x] = ref_mean;
+        s_rvar[threadIdx.x] = ref_var;
+        atomicMin(&s_pmin, first);
+        atomicMax(&s_pmax, first + count - 1);
+    }
+    __syncthreads();
+    const int slice = (a.nplanes + gridDim.z - 1) / gridDim.z;
+    const int pmin = max(s_pmin, static_cast<int>(blockIdx.z) * slice);
+    const int pmax = min(s_pmax, static_cast<int>(blockIdx.z + 1) * slice - 1);
+    const double xd = double(x), yd = double(y);
+
+    for (int p = pmin; p <= pmax; ++p) {
+        const bool need = count > 0 && p >= first && p < first + count;
+        const int slot = (p - pmin) % kPlaneChunk;
+        if (slot == 0) {
+            __syncthreads();
+            for (int k = threadIdx.x; k < kPlaneChunk * NM; k += kTiledThreads) {
+                const int pp = p + k / NM, m = k % NM;
+                if (pp <= pmax)
+                    s_tp[k / NM][m] = make_tile_params64(s_vc[m].homs + static_cast<size_t>(pp) * 9,
+                                                         x0 - RX, y0 - RY, SW - 1, SH - 1);
+            }
+        }
+        if (!__syncthreads_or(need))
+            continue;
+        for (int s = threadIdx.x; s < NM * SN; s += kTiledThreads) {
+            const int m = s / SN, r = s - m * SN;
+            const int dv = r / SW, du = r - dv * SW;
+            const TileParams64& tp = s_tp[slot][m];
+            s_tile[s] = tp.exact ? make_float2(0.0f, 1e30f)
+                                 : tile_sample64(tp, s_vc[m], double(du), double(dv));
+        }
+        __syncthreads();
+        // ---- pass 1: certified NCC cost per view, or NS exact work items
+        int cost[NM];
+        uint32_t view_unsure = 0, view_exact = 0;
+        int my_items = 0;
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+            cost[m] = 255;
+            if (!need)
+                continue;
+            const TileParams64& tp = s_tp[slot][m];
+            if (tp.exact) {
+                view_exact |= 1u << m;
+                continue;
+            }
+            const ViewConst& vc = s_vc[m];
+            double tcx, tcy;
+            tile_coords64(tp, double(tx + RX), double(ty + RY), &tcx, &tcy);
+            const double X = double(tp.xa) + tcx, Y = double(tp.ya) + tcy;
+            const double ddx = double(tp.dx) + 1e-9, ddy = double(tp.dy) + 1e-9;
+            bool inside;
+            if (X - ddx >= 0.0 && Y - ddy >= 0.0 && X + ddx <= double(vc.w - 1) &&
+                Y + ddy <= double(vc.h - 1))
+                inside = true;
+            else if (X + ddx < 0.0 || Y + ddy < 0.0 || X - ddx > double(vc.w - 1) ||
+                     Y - ddy > double(vc.h - 1))
+                inside = false;
+            else
+                inside = exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd);
+            if (!inside || ref_var <= 0.0)
+                continue;  // 255 (matching.cpp:224-232, 262-263)
+            const float2* t = s_tile + m * SN;
+            const float fc = t[(ty + RY) * SW + tx + RX].x;
+            float su = 0.0f, suu = 0.0f, sru = 0.0f, emax = 0.0f;
+#pragma unroll
+            for (int i = 0; i < WH; ++i)
+#pragma unroll
+                for (int j = 0; j < WW; ++j) {
+                    const float2 n = t[(ty + i) * SW + tx + j];
+                    const float u = n.x - fc;
+                    su += u;
+                    suu = fmaf(u, u, suu);
+                    sru = fmaf(s_ref[(ty + i) * SW + tx + j] - mean_f, u, sru);
+                    emax = fmaxf(emax, n.y);
+                }
+            // rigorous intervals of the reference's cov and var_b (see header)
+            const float nf = float(NS);
+            const float g = float(NS + 4) * 1.0e-7f;              // FP32 summation + u rounding
+            const float abs_u = sqrtf(nf * suu) * 1.001f + 1e-6f;  // >= sum |u_i|
+            const float e_su = g * abs_u;
+            const float e_suu = g * suu;
+            const float su2n = su * su / nf;
+            const float varf = suu - su2n;
+            const float sru_abs = sqrtf(var_rf * suu) * 1.001f + 1e-6f;
+            const float e_sru = g * sru_abs + 3.2e-5f * abs_u;     // + centred-ref rounding
+            const float sqv = sqrtf(fmaxf(varf, 0.0f));
+            // var(w) - var(f) = 2 sum(f_i - fbar) e_i + sum (e_i - ebar)^2
+            const float dv_ = 1.01f * (2.0f * emax * sqrtf(nf) * sqv + nf * emax * emax + e_suu +
+                                       (2.0f * fabsf(su) * e_su + e_su * e_su) / nf +
+                                       3.0e-7f * (suu + su2n) + 1e-5f);
+            const float dc_ = 1.01f * (emax * sar + e_sru + 1e-5f);
+            const float v_lo = varf - dv_, v_hi = varf + dv_;
+            const float c_lo = sru - dc_, c_hi = sru + dc_;
+            bool certified = false;
+            if (v_lo > 0.0f) {
+                float n_hi = c_hi / sqrtf(var_rf * (c_hi >= 0.0f ? v_lo : v_hi));
+                float n_lo = c_lo / sqrtf(var_rf * (c_lo >= 0.0f ? v_hi : v_lo));
+                const float slack = 1e-5f * (fabsf(n_hi) + fabsf(n_lo)) + 1e-6f;
+                n_hi += slack;
+                n_lo -= slack;
+                float t_lo = 255.0f * fminf(1.0f - n_hi, 1.0f);
+                float t_hi = 255.0f * fminf(1.0f - n_lo, 1.0f);
+                t_lo = fminf(fmaxf(t_lo, 0.0f), 255.0f) - 1e-3f;
+                t_hi = fminf(fmaxf(t_hi, 0.0f), 255.0f) + 1e-3f;
+                const int k_lo = static_cast<int>(floorf(fmaxf(t_lo, 0.0f) + 0.5f));
+                const int k_hi = static_cast<int>(floorf(fminf(t_hi, 255.0f) + 0.5f));
+                if (k_lo == k_hi) {
+                    cost[m] = k_lo;
+                    certified = true;
+                }
+            }
+            if (!certified) {
+                view_unsure |= 1u << m;
+                my_items += NS;
+            }
+            if (a.stats) {
+                atomicAdd(a.stats + 0, 1ull);
+                if (!certified)
+                    atomicAdd(a.stats + 1, 1ull);
+            }
+        }
+        int off, total;
+        Scan(s_scan).ExclusiveSum(my_items, off, total);
+        if (my_items) {
+            int k = off;
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                if (!((view_unsure >> m) & 1u))
+                    continue;
+                for (int s = 0; s < NS; ++s, ++k)
+                    if (k < kNccItemCap)
+                        s_items[k] = threadIdx.x | (m << 8) | (s << 12);
+            }
+        }
+        __syncthreads();
+        const int nitems = min(total, kNccItemCap);
+        for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
+            const uint32_t item = s_items[it];
+            const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = item >> 12;
+            const ViewConst& vc = s_vc[m];
+            s_vals[it] = exact_window_sample(vc.homs + static_cast<size_t>(p) * 9, vc.quad, vc.w,
+                                             vc.h, double(x0 + t % kTW), double(y0 + t / kTW), RX,
+                                             RY, pos / WW, pos % WW);
+        }
+        __syncthreads();
+        // ---- pass 2b: the reference's sums and NCC of each undecided view
+        // (matching.cpp:265-279, same order), one thread per view
+        const int nviews_u = nitems / NS;
+        for (int v = threadIdx.x; v < nviews_u; v += kTiledThreads) {
+            const int k0 = v * NS;
+            const int t = s_items[k0] & 0xFF;
+            const int ttx = t % kTW, tty = t / kTW;
+            double sb = 0.0, sbb = 0.0, sab = 0.0;
+            for (int s = 0; s < NS; ++s) {
+                const int i = s / WW, j = s - (s / WW) * WW;
+                const double val = s_vals[k0 + s];
+                sb = add(sb, val);
+                sbb = add(sbb, mul(val, val));
+                sab = add(sab, mul(double(s_ref[(tty + i) * SW + ttx + j]), val));
+            }
+            s_vcost[v] = ncc_tail<NS>(sb, sbb, sab, s_rmean[t], s_rvar[t]);
+        }
+        __syncthreads();
+        // ---- pass 3: costs of undecided views from pass 2b, per-side sums
+        if (need) {
+            int sum_l = 0, sum_r = 0, k = off;
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                const ViewConst& vc = s_vc[m];
+                const double* hp = vc.homs + static_cast<size_t>(p) * 9;
+                int c = cost[m];
+                if ((view_exact >> m) & 1u) {
+                    const float* rp = nullptr;
+                    float patch[NS];
+#pragma unroll
+                    for (int i = 0; i < WH; ++i)
+#pragma unroll
+                        for (int j = 0; j < WW; ++j)
+                            patch[i * WW + j] = s_ref[(ty + i) * SW + tx + j];
+                    rp = patch;
+                    c = view_cost<FMVS_COST_NCC, WW, WH>(vc.quad, vc.w, vc.h, hp, xd, yd, 0ull, rp,
+                                                        ref_mean, ref_var, a.census_lut);
+                } else if ((view_unsure >> m) & 1u) {
+                    if (k + NS <= kNccItemCap) {
+                        c = s_vcost[k / NS];  // resolved by pass 2b
+                    } else {
+                        // list overflow (pathological inputs): the owner walks it
+                        double sb = 0.0, sbb = 0.0, sab = 0.0;
+                        for (int s = 0; s < NS; ++s) {
+                            const int i = s / WW, j = s - (s / WW) * WW;
+                            const double v = exact_window_sample(hp, vc.quad, vc.w, vc.h, xd, yd, RX,
+                                                                 RY, i, j);
+                            sb = add(sb, v);
+                            sbb = add(sbb, mul(v, v));
+                            sab = add(sab, mul(double(s_ref[(ty + i) * SW + tx + j]), v));
+                        }
+                        c = ncc_tail<NS>(sb, sbb, sab, ref_mean, ref_var);
+                    }
+                    k += NS;
+                }
+                if (vc.left)
+                    sum_l += c;
+                else
+                    sum_r += c;
+            }
+            const uint64_t o = base + static_cast<uint64_t>(p - first);
+            a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
+            if (a.agg_zero)
+                a.agg_zero[o] = 0u;
+        }
+    }
+}
+
+template <int WW, int WH, int NM>
+void launch_ncc_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
+    const size_t smem = sizeof(float2) * NM * (kTW + WW - 1) * (kTH + WH - 1);
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_ncc_tiled<WW, WH, NM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    sweep_ncc_tiled<WW, WH, NM><<<grid, kTiledThreads, smem, s>>>(a);
+}
+
+template <int WW, int WH>
+bool launch_ncc(const SweepArgs& a, dim3 grid, cudaStream_t s) {
+    switch (a.nmatch) {
+        case 2: launch_ncc_nm<WW, WH, 2>(a, grid, s); return true;
+        case 4: launch_ncc_nm<WW, WH, 4>(a, grid, s); return true;
+        case 6: launch_ncc_nm<WW, WH, 6>(a, grid, s); return true;
+        case 8: launch_ncc_nm<WW, WH, 8>(a, grid, s); return true;
+        default: return false;
+    }
+}
+
 template <int WW, int WH, int NM>
 void launch_tiled_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
     const size_t smem = sizeof(float2) * NM * (kTW + WW - 1) * (kTH + WH - 1);
@@ -737,9 +1188,13 @@ bool launch_tiled(const SweepArgs& a, dim3 grid, cudaStream_t s) {
 
 void sweep(const SweepArgs& a_in, cudaStream_t s) {
     SweepArgs a = a_in;
-    const bool tiled = a.kind == FMVS_COST_CENSUS && !a.disable_tiled &&
+    const bool tiled = !a.disable_tiled &&
                        (a.nmatch == 2 || a.nmatch == 4 || a.nmatch == 6 || a.nmatch == 8);
-    a.exact_above = tiled ? kNarrowMax : 0;
+    // Pixels wider than narrow_max (invalid-prior pixels sweeping the whole
+    // stack at refined levels) would inflate a tile's plane union: they take
+    // the exact per-hypothesis kernel. Uniform levels set narrow_max to the
+    // stack size (every pixel shares the range).
+    a.exact_above = tiled ? (a.narrow_max > 0 ? a.narrow_max : kNarrowMax) : 0;
     const dim3 grid((a.w + kSeg - 1) / kSeg, a.h);
     if (a.kind == FMVS_COST_CENSUS && a.ww == 5)
         sweep_kernel<FMVS_COST_CENSUS, 5, 5><<<grid, kThreads, 0, s>>>(a);
@@ -760,10 +1215,14 @@ void sweep(const SweepArgs& a_in, cudaStream_t s) {
         while (slices < 64 && tiles * slices < 4 * 148 * 3 && a.nplanes / (2 * slices) >= 8)
             slices *= 2;
     const dim3 tgrid((a.w + kTW - 1) / kTW, (a.h + kTH - 1) / kTH, slices);
-    if (a.ww == 5)
+    if (a.kind == FMVS_COST_CENSUS && a.ww == 5)
         launch_tiled<5, 5>(a, tgrid, s);
-    else
+    else if (a.kind == FMVS_COST_CENSUS)
         launch_tiled<9, 7>(a, tgrid, s);
+    else if (a.ww == 5)
+        launch_ncc<5, 5>(a, tgrid, s);
+    else
+        launch_ncc<9, 9>(a, tgrid, s);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -69,6 +69,7 @@ struct SweepArgs {
     int exact_above;
     int disable_tiled;               // force the exact per-hypothesis kernel
     int plane_slicing;               // dense ranges: split planes across CTAs (grid z)
+    int narrow_max;                  // pixels with more hypotheses take the exact kernel (0: default)
     unsigned long long* stats;       // optional diagnostics: [view-evals, unsure evals, unsure bits, exact views]
 };
 void sweep(const SweepArgs& a, cudaStream_t s);

@@ -10,8 +10,9 @@ from paper_2112_00821_b200 import Backend
 import bench
 
 b = Backend.b200()
-scene, cfgkw, _ = bench.WORKLOADS["c2"]
-frames = bench.render_frames(b, scene, 5)
+wl = sys.argv[1] if len(sys.argv) > 1 else "c2"
+scene, cfgkw, _ = bench.WORKLOADS[wl]
+frames = bench.render_frames(b, scene, scene.get("views", 5))
 cfg = bench.make_config(pkg, **cfgkw)
 b.estimate_bundle(frames, cfg)
 out = (C.c_uint64 * 4)()

@@ -100,23 +100,29 @@ def test_sweep_cost_volume_bitexact(b200, oracle, rng, cost):
     assert len(a.costs) > 1000
 
 
-@pytest.mark.parametrize("texture", ["quantized", "noise", "constant"])
-@pytest.mark.parametrize("cost", ["census5", "census97"])
+@pytest.mark.parametrize("texture", ["quantized", "noise", "constant", "ramp"])
+@pytest.mark.parametrize("cost", ["census5", "census97", "ncc5", "ncc9"])
 def test_sweep_certified_census_ties(b200, oracle, rng, texture, cost):
-    """Flat / quantised / noisy images stress the certified FP32 census path:
-    exact FP64 ties and near-ties must fall back to the reference walk."""
+    """Flat / quantised / noisy / ramp images stress the certified FP32 census
+    and NCC paths: exact FP64 ties, near-ties, flat windows (var_b <= 0) and
+    costs on rounding boundaries must fall back to the reference walk."""
     bundle, stack = _level_inputs(oracle, w=70, h=44)
     for v in bundle:
         if texture == "quantized":
             v.image = ((v.image // 48) * 48).astype(np.uint8)
         elif texture == "noise":
             v.image = rng.integers(0, 256, v.image.shape).astype(np.uint8)
+        elif texture == "ramp":
+            hh, ww = v.image.shape
+            v.image = ((np.arange(ww)[None, :] * 3 + np.arange(hh)[:, None]) % 256).astype(np.uint8)
         else:
             v.image = np.full_like(v.image, 77)
     h, w = bundle[2].image.shape
     lo = np.full((h, w), 6.0, np.float32)
     hi = np.full((h, w), 16.0, np.float32)
-    cf = CostFunctionSpec(CostKind.CensusHamming, *((5, 5) if cost == "census5" else (9, 7)))
+    spec = {"census5": (CostKind.CensusHamming, 5, 5), "census97": (CostKind.CensusHamming, 9, 7),
+            "ncc5": (CostKind.NccTruncated, 5, 5), "ncc9": (CostKind.NccTruncated, 9, 9)}[cost]
+    cf = CostFunctionSpec(*spec)
     a = b200.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
     b = oracle.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
     assert_same(a.costs, b.costs, "costs")
