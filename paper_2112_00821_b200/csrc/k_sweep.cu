@@ -539,9 +539,22 @@ __device__ __forceinline__ void tile_coords64(const TileParams64& tp, double du,
 // Sample of the tile at (du, dv): FP64 residual coordinates, FP32 bilinear;
 // returns (value, bound) like the FP32-coordinate path.
 __device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const ViewConst& vc,
-                                                double du, double dv) {
+                                                double du, double dv, uint8_t* in_flag) {
     double tx, ty;
     tile_coords64(tp, du, dv, &tx, &ty);
+    {
+        // certified inside test of this sample as a window centre
+        // (matching.cpp:224-231): 1 inside, 0 outside, 2 undecided
+        const double X = double(tp.xa) + tx, Y = double(tp.ya) + ty;
+        const double ddx = double(tp.dx) + 1e-9, ddy = double(tp.dy) + 1e-9;
+        const double wm = double(vc.w - 1), hm = double(vc.h - 1);
+        uint8_t fl = 2;
+        if (X - ddx >= 0.0 && Y - ddy >= 0.0 && X + ddx <= wm && Y + ddy <= hm)
+            fl = 1;
+        else if (X + ddx < 0.0 || Y + ddy < 0.0 || X - ddx > wm || Y - ddy > hm)
+            fl = 0;
+        *in_flag = fl;
+    }
     const double fx = floor(tx), fy = floor(ty);
     int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
     float ax = __double2float_rn(tx - fx), ay = __double2float_rn(ty - fy);
@@ -842,6 +855,9 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
 
 constexpr int kNccItemCap = 2048;
 
+// sqrt(x) for bounds: MUFU rsqrt based (relative error < 1e-6), 0 for x <= 0.
+__device__ __forceinline__ float sqrt_up(float x) { return x > 0.0f ? x * rsqrtf(x) * 1.0001f : 0.0f; }
+
 // The tail of the reference's NCC cost from its FP64 window sums
 // (matching.cpp:271-279).
 template <int NS>
@@ -866,6 +882,9 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
     constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
     extern __shared__ float2 s_tile[];  // [NM][SH][SW] (value, bound)
     __shared__ float s_ref[SN];         // edge-clamped reference tile + halo
+    // certified inside flag of each tile sample as a window centre (dynamic,
+    // behind the tile)
+    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_tile + NM * SN);
     __shared__ TileParams64 s_tp[kPlaneChunk][NM];
     __shared__ ViewConst s_vc[NM];
     __shared__ int s_pmin, s_pmax;
@@ -958,8 +977,10 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
             const int m = s / SN, r = s - m * SN;
             const int dv = r / SW, du = r - dv * SW;
             const TileParams64& tp = s_tp[slot][m];
+            uint8_t fl = 2;
             s_tile[s] = tp.exact ? make_float2(0.0f, 1e30f)
-                                 : tile_sample64(tp, s_vc[m], double(du), double(dv));
+                                 : tile_sample64(tp, s_vc[m], double(du), double(dv), &fl);
+            s_in[s] = fl;
         }
         __syncthreads();
         // ---- pass 1: certified NCC cost per view, or NS exact work items
@@ -977,19 +998,10 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
                 continue;
             }
             const ViewConst& vc = s_vc[m];
-            double tcx, tcy;
-            tile_coords64(tp, double(tx + RX), double(ty + RY), &tcx, &tcy);
-            const double X = double(tp.xa) + tcx, Y = double(tp.ya) + tcy;
-            const double ddx = double(tp.dx) + 1e-9, ddy = double(tp.dy) + 1e-9;
-            bool inside;
-            if (X - ddx >= 0.0 && Y - ddy >= 0.0 && X + ddx <= double(vc.w - 1) &&
-                Y + ddy <= double(vc.h - 1))
-                inside = true;
-            else if (X + ddx < 0.0 || Y + ddy < 0.0 || X - ddx > double(vc.w - 1) ||
-                     Y - ddy > double(vc.h - 1))
-                inside = false;
-            else
-                inside = exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd);
+            const uint8_t fl = s_in[m * SN + (ty + RY) * SW + tx + RX];
+            const bool inside =
+                fl == 2 ? exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd)
+                        : fl == 1;
             if (!inside || ref_var <= 0.0)
                 continue;  // 255 (matching.cpp:224-232, 262-263)
             const float2* t = s_tile + m * SN;
@@ -1007,27 +1019,30 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
                     emax = fmaxf(emax, n.y);
                 }
             // rigorous intervals of the reference's cov and var_b (see header)
-            const float nf = float(NS);
-            const float g = float(NS + 4) * 1.0e-7f;              // FP32 summation + u rounding
-            const float abs_u = sqrtf(nf * suu) * 1.001f + 1e-6f;  // >= sum |u_i|
+            // (approximate MUFU sqrt/rsqrt, rel. error < 1e-6, absorbed by the
+            // 1.001 / 1.01 factors and the 1e-5 ncc slack below)
+            constexpr float nf = float(NS), invn = 1.0f / float(NS);
+            const float sqrt_n = sqrtf(nf);
+            const float g = float(NS + 4) * 1.0e-7f;                // FP32 summation + u rounding
+            const float abs_u = sqrt_up(nf * suu) * 1.001f + 1e-6f;  // >= sum |u_i|
             const float e_su = g * abs_u;
             const float e_suu = g * suu;
-            const float su2n = su * su / nf;
+            const float su2n = su * su * invn;
             const float varf = suu - su2n;
-            const float sru_abs = sqrtf(var_rf * suu) * 1.001f + 1e-6f;
-            const float e_sru = g * sru_abs + 3.2e-5f * abs_u;     // + centred-ref rounding
-            const float sqv = sqrtf(fmaxf(varf, 0.0f));
+            const float sru_abs = sqrt_up(var_rf * suu) * 1.001f + 1e-6f;
+            const float e_sru = g * sru_abs + 3.2e-5f * abs_u;       // + centred-ref rounding
+            const float sqv = sqrt_up(fmaxf(varf, 0.0f)) * 1.001f;
             // var(w) - var(f) = 2 sum(f_i - fbar) e_i + sum (e_i - ebar)^2
-            const float dv_ = 1.01f * (2.0f * emax * sqrtf(nf) * sqv + nf * emax * emax + e_suu +
-                                       (2.0f * fabsf(su) * e_su + e_su * e_su) / nf +
+            const float dv_ = 1.01f * (2.0f * emax * sqrt_n * sqv + nf * emax * emax + e_suu +
+                                       (2.0f * fabsf(su) * e_su + e_su * e_su) * invn +
                                        3.0e-7f * (suu + su2n) + 1e-5f);
             const float dc_ = 1.01f * (emax * sar + e_sru + 1e-5f);
             const float v_lo = varf - dv_, v_hi = varf + dv_;
             const float c_lo = sru - dc_, c_hi = sru + dc_;
             bool certified = false;
             if (v_lo > 0.0f) {
-                float n_hi = c_hi / sqrtf(var_rf * (c_hi >= 0.0f ? v_lo : v_hi));
-                float n_lo = c_lo / sqrtf(var_rf * (c_lo >= 0.0f ? v_hi : v_lo));
+                float n_hi = c_hi * rsqrtf(var_rf * (c_hi >= 0.0f ? v_lo : v_hi));
+                float n_lo = c_lo * rsqrtf(var_rf * (c_lo >= 0.0f ? v_hi : v_lo));
                 const float slack = 1e-5f * (fabsf(n_hi) + fabsf(n_lo)) + 1e-6f;
                 n_hi += slack;
                 n_lo -= slack;
@@ -1146,7 +1161,7 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
 
 template <int WW, int WH, int NM>
 void launch_ncc_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
-    const size_t smem = sizeof(float2) * NM * (kTW + WW - 1) * (kTH + WH - 1);
+    const size_t smem = (sizeof(float2) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1);
     FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_ncc_tiled<WW, WH, NM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
