@@ -122,17 +122,16 @@ struct Tmp {
 
 fmvs::V3 v3(const double* n) { return {n[0], n[1], n[2]}; }
 
-// Lanes per scanline of the grouped SGM kernel at the refined levels
-// (FMVS_SGM_G = 8 / 16 / 32; results are identical, only speed differs).
-int sgm_group() {
-    if (const char* e = std::getenv("FMVS_SGM_G")) {
-        const int g = std::atoi(e);
-        if (g == 8 || g == 16 || g == 32)
-            return g;
-        if (g == 0)
-            return 0;
-    }
-    return 8;
+// Lane blocking of the SGM kernel at the refined levels: G lanes per scanline,
+// K hypotheses per lane and pass (FMVS_SGM_G / FMVS_SGM_K; results are
+// identical, only speed differs). G = 0 selects the one-line-per-warp kernel.
+void sgm_blocking(int* g, int* k) {
+    *g = 4;
+    *k = 4;
+    if (const char* e = std::getenv("FMVS_SGM_G"))
+        *g = std::atoi(e);
+    if (const char* e = std::getenv("FMVS_SGM_K"))
+        *k = std::atoi(e);
 }
 
 fmvs::dev::Intr intr_of(const fmvs_intrinsics& k) { return fmvs::dev::make_intr(k); }
@@ -456,7 +455,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         size_t lines = 0;
         for (auto& P : lv)
             lines = std::max(lines, static_cast<size_t>(k::sgm_total_lines(P.w, P.h, 8)));
-        sgm_scratch = ctx->buf("sgm_scratch").as<uint32_t>(lines * 2 * max_p);
+        sgm_scratch = ctx->buf("sgm_scratch").as<uint32_t>(lines * 2 * (max_p + 8));
     }
 
     const double cos_rho = std::cos(60.0 * M_PI / 180.0);
@@ -577,7 +576,13 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         ga.pmax = np;
         // coarsest level: dense ranges, one line per warp-wide group; refined
         // levels: ~12 hypotheses per pixel, 32/G lines per warp
-        ga.group = variant == FMVS_SGM_PATH_GRADIENT ? 0 : (l == L - 1 ? 32 : sgm_group());
+        sgm_blocking(&ga.group, &ga.kper);
+        if (l == L - 1) {
+            ga.group = 32;
+            ga.kper = 4;
+        }
+        if (variant == FMVS_SGM_PATH_GRADIENT)
+            ga.group = 0;
         ga.group_caps = l == L - 1 ? std::min(np, 1024) : 32;
         ga.scratch = (ga.group > 0 || np > pmax_smem_limit) ? sgm_scratch : nullptr;
         ctx->timed(l == 0 ? "sgm_l0" : "sgm", [&] { k::sgm(ga, s); });
@@ -1211,12 +1216,14 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
             ga.offsets = oa.out;
         }
         ga.pmax = pmax;
-        ga.group = cfg->variant == FMVS_SGM_PATH_GRADIENT ? 0 : sgm_group();
+        sgm_blocking(&ga.group, &ga.kper);
+        if (cfg->variant == FMVS_SGM_PATH_GRADIENT)
+            ga.group = 0;
         ga.group_caps = 32;
         const int limit = (200 * 1024) / (4 * 2 * 4);
         if (pmax > limit || ga.group > 0) {
             const size_t lines = static_cast<size_t>(k::sgm_total_lines(w, h, 8));
-            ga.scratch = t.alloc<uint32_t>(lines * 2 * pmax);
+            ga.scratch = t.alloc<uint32_t>(lines * 2 * (pmax + 8));
         }
         if (total > 0)
             k::sgm(ga, s);

@@ -249,21 +249,73 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
     }
 }
 
-// Grouped variant (Plane / SurfaceNormal): 32/G scanlines per warp, G lanes
-// per line. At the refined levels a pixel has ~12 hypotheses, so packing
-// lines amortises the per-step bookkeeping (operand prefetch, REDUX, pipeline
-// rotation) over several lines. Each group keeps its path buffers in a small
-// shared-memory double buffer and spills pixels wider than `caps` hypotheses
-// to a per-line global buffer. The reduction is a group-masked REDUX.
-template <int VARIANT, typename V, int G>
-__global__ void __launch_bounds__(kWarps * 32) sgm_group_kernel(SgmArgs a, int total_lines,
-                                                                int caps) {
+// Minimum over the G-lane group of the calling lane (G a power of two): a
+// full-warp REDUX for G = 32, an xor butterfly otherwise (a group-masked
+// REDUX with per-group masks serialises into one pass per group).
+template <int G>
+__device__ __forceinline__ uint32_t group_min(uint32_t v) {
+    if (G == 32)
+        return __reduce_min_sync(0xFFFFFFFFu, v);
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1)
+        v = min(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    return v;
+}
+
+// Operands of one pixel of a scanline, staged in registers ahead of its step.
+template <int K, typename V>
+struct LinePx {
+    // stage 1: raw loads only (no arithmetic on a value in flight, which
+    // would wait for it)
+    uint64_t rb;     // row base of the pixel's row
+    dev::VolMeta m;  // {offset in row, first | count << 16}
+    int img;         // reference intensity
+    int off;         // SN shift of the canonical direction (unsigned-extended raw)
+    bool v;          // inside the image
+    // stage 2
+    uint64_t base;   // entry index of hypothesis 0
+    V phi2;          // phi2 of the transition from the previous pixel
+    uint32_t s[K];   // costs of the first pass
+};
+
+constexpr int kSgmSlots = 6;  // register pipeline depth (pixels in flight per line)
+constexpr int kSent = 3;      // sentinel slots on each side of a path buffer
+constexpr uint32_t kSentinel = 0x3FFFFFFFu;
+
+// Register-blocked variant (Plane / SurfaceNormal): G lanes per scanline and
+// 32/G scanlines per warp; lane gl owns the K hypotheses i = gl + G*k of a
+// pass of G*K (pixels wider than a pass loop over passes). At the refined
+// levels a pixel has ~12 hypotheses, so G=4, K=4 covers it in one pass with 8
+// scanlines per warp.
+//
+// The recurrence is sequential along a line, so the kernel is bound by the
+// latency of one step. The operands are therefore staged through a
+// kSgmSlots-deep register pipeline, unrolled so that no slot is ever copied (a
+// register copy would wait for its pending load): at the step of pixel k the
+// meta / image / SN shift of pixel k+5 are loaded, the first-pass costs of
+// pixel k+3 (whose meta arrived two steps ago) are loaded and its phi2 is
+// looked up, and pixel k is computed from operands requested 3-5 steps
+// earlier.
+//
+// Path buffers: a per-line shared-memory double buffer (line stride padded so
+// the 32/G lines of a warp start in distinct banks); pixels wider than `caps`
+// hypotheses spill to a per-line global buffer. In the int32 recurrence (SENT)
+// every buffer carries kSent sentinel slots on both sides, so the ragged
+// predecessor window prev[t-1..t+1] needs no bounds tests: t is clamped into
+// [-2, prev_count + 1] and out-of-range slots read kSentinel, which never
+// beats prev_min + phi2 (all path values stay below 2^30 when the host picks
+// the int32 path).
+template <int VARIANT, typename V, int G, int K>
+__global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int total_lines,
+                                                                int caps, int stride) {
     using namespace dev;
+    constexpr bool SENT = sizeof(V) == 4;
     constexpr int LPW = 32 / G;
+    constexpr int PASS = G * K;
+    constexpr int S = kSgmSlots;
     extern __shared__ uint32_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / G, gl = lane % G;
-    const unsigned gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << (grp * G));
     const int line = (blockIdx.x * kWarps + warp) * LPW + grp;
     const int w = a.w, h = a.h;
 
@@ -294,10 +346,21 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_group_kernel(SgmArgs a, int t
             y = dy > 0 ? 0 : h - 1;
         }
     }
-    uint32_t* sA = smem + static_cast<size_t>(warp * LPW + grp) * 2 * caps;
-    uint32_t* sB = sA + caps;
-    uint32_t* gA = a.scratch ? a.scratch + static_cast<size_t>(line) * 2 * a.pmax : nullptr;
-    uint32_t* gB = gA ? gA + a.pmax : nullptr;
+    // buffer layout (both smem and global): [kSent sentinels][caps or pmax][kSent]
+    uint32_t* sA = smem + static_cast<size_t>(warp * LPW + grp) * stride + kSent;
+    uint32_t* sB = sA + caps + 2 * kSent;
+    const size_t gstride = static_cast<size_t>(a.pmax) + 2 * kSent;
+    uint32_t* gA = (a.scratch && line < total_lines) ? a.scratch + static_cast<size_t>(line) * 2 * gstride + kSent
+                                                     : nullptr;
+    uint32_t* gB = gA ? gA + gstride : nullptr;
+    if (SENT && gl < kSent) {
+        sA[-kSent + gl] = kSentinel;
+        sB[-kSent + gl] = kSentinel;
+        if (gA) {
+            gA[-kSent + gl] = kSentinel;
+            gB[-kSent + gl] = kSentinel;
+        }
+    }
 
     int slot = 0, sign = 1;
     if (VARIANT == FMVS_SGM_SURFACE_NORMAL) {
@@ -316,119 +379,136 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_group_kernel(SgmArgs a, int t
     const V phi1 = static_cast<V>(a.phi1);
     auto inside = [&](int xx, int yy) { return xx >= 0 && yy >= 0 && xx < w && yy < h; };
 
-    VolMeta m0{0u, 0u}, m1{0u, 0u};
-    uint64_t rb0 = 0, rb1 = 0;
-    int img0 = 0, img1 = 0, off0 = 0, off1 = 0;
-    bool v0 = inside(x, y), v1 = v0 && inside(x + dx, y + dy);
-    if (v0) {
-        const size_t p = static_cast<size_t>(y) * w + x;
-        m0 = a.meta[p];
-        rb0 = a.row_base[y];
-        img0 = a.image[p];
-        if (sn)
-            off0 = a.offsets[4 * p + slot];
+    using Px = LinePx<K, V>;
+    Px P[S];
+    // stage 1: meta, row base, image, SN shift (raw)
+    auto load_meta = [&](Px& q, int xx, int yy, bool valid) {
+        q.v = valid;
+        q.m = dev::VolMeta{0u, 0u};
+        q.rb = 0;
+        q.img = 0;
+        q.off = 0;
+        if (valid) {
+            const size_t p = static_cast<size_t>(yy) * w + xx;
+            q.m = a.meta[p];
+            q.rb = a.row_base[yy];
+            q.img = a.image[p];
+            if (sn)
+                q.off = a.offsets[4 * p + slot];
+        }
+    };
+    // stage 2: entry base, first-pass costs, phi2 of the transition from the
+    // previous pixel
+    auto load_costs = [&](Px& q, const Px& qprev) {
+        const int c = meta_count(q.m.fc);
+        q.base = q.rb + q.m.rel;
+        const uint16_t* cp = a.costs + q.base;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = gl + G * k;
+            q.s[k] = i < c ? cp[i] : 0u;
+        }
+        q.phi2 = (q.v && qprev.v) ? static_cast<V>(a.phi2_lut[abs(q.img - qprev.img)]) : V(0);
+    };
+
+    // prologue: pixels 0..S-2 through stage 1, pixels 0..S-4 through stage 2
+    {
+        bool valid = inside(x, y);
+#pragma unroll
+        for (int j = 0; j < S - 1; ++j) {
+            load_meta(P[j], x + j * dx, y + j * dy, valid);
+            valid = valid && inside(x + (j + 1) * dx, y + (j + 1) * dy);
+        }
+        P[S - 1].v = false;
+        P[S - 1].img = 0;
+#pragma unroll
+        for (int j = 0; j < S - 3; ++j)
+            load_costs(P[j], P[(j + S - 1) % S]);
     }
-    if (v1) {
-        const size_t p = static_cast<size_t>(y + dy) * w + x + dx;
-        m1 = a.meta[p];
-        rb1 = a.row_base[y + dy];
-        img1 = a.image[p];
-        if (sn)
-            off1 = a.offsets[4 * p + slot];
-    }
-    uint32_t cost0 = 0;
-    if (v0 && gl < meta_count(m0.fc))
-        cost0 = a.costs[rb0 + m0.rel + gl];
 
     bool has_prev = false;
-    int prev_first = 0, prev_count = 0, img_prev = 0;
+    int prev_first = 0, prev_count = 0;
     V prev_min = 0;
     const uint32_t* prev = sA;
 
-    while (__any_sync(0xFFFFFFFFu, v0)) {
-        const int x2 = x + 2 * dx, y2 = y + 2 * dy;
-        const bool v2 = v1 && inside(x2, y2);
-        VolMeta m2{0u, 0u};
-        uint64_t rb2 = 0;
-        int img2 = 0, off2 = 0;
-        if (v2) {
-            const size_t p = static_cast<size_t>(y2) * w + x2;
-            m2 = a.meta[p];
-            rb2 = a.row_base[y2];
-            img2 = a.image[p];
-            if (sn)
-                off2 = a.offsets[4 * p + slot];
-        }
-        uint32_t cost1 = 0;
-        if (v1 && gl < meta_count(m1.fc))
-            cost1 = a.costs[rb1 + m1.rel + gl];
-
-        const int f = meta_first(m0.fc);
-        const int c = v0 ? meta_count(m0.fc) : 0;
-        uint32_t run_min = 0xFFFFFFFFu;
-        uint32_t* cur = nullptr;
-        if (c > 0) {
-            cur = c <= caps ? (prev == sA ? sB : sA) : (prev == gA ? gB : gA);
-            const uint64_t base = rb0 + m0.rel;
-            V phi2 = 0;
-            int shift = 0;
-            if (has_prev) {
-                phi2 = static_cast<V>(a.phi2_lut[abs(img0 - img_prev)]);
-                if (sn)
-                    shift = sign * off0;
+    for (;;) {
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            Px& cur_px = P[u];
+            if (!__any_sync(0xFFFFFFFFu, cur_px.v))
+                goto done;
+            // stage 1 for pixel k+S-1, stage 2 for pixel k+S-3
+            {
+                Px& pn = P[(u + S - 1) % S];
+                const Px& pl = P[(u + S - 2) % S];
+                load_meta(pn, x + (S - 1) * dx, y + (S - 1) * dy,
+                          pl.v && inside(x + (S - 1) * dx, y + (S - 1) * dy));
+                load_costs(P[(u + S - 3) % S], P[(u + S - 4) % S]);
             }
-            const V base_best = prev_min + phi2;
-            const int toff = f + shift - prev_first;
-            for (int i0 = 0; i0 < c; i0 += G) {
-                const int i = i0 + gl;
-                if (i < c) {
-                    const uint32_t s = i0 == 0 ? cost0 : a.costs[base + i];
-                    uint32_t v;
-                    if (!has_prev) {
-                        v = s;
-                    } else {
-                        const int t = toff + i;
-                        V best = base_best;
-                        if (static_cast<unsigned>(t) < static_cast<unsigned>(prev_count))
-                            best = min(best, static_cast<V>(prev[t]));
-                        if (static_cast<unsigned>(t - 1) < static_cast<unsigned>(prev_count))
-                            best = min(best, static_cast<V>(prev[t - 1]) + phi1);
-                        if (static_cast<unsigned>(t + 1) < static_cast<unsigned>(prev_count))
-                            best = min(best, static_cast<V>(prev[t + 1]) + phi1);
-                        v = static_cast<uint32_t>(static_cast<V>(s) + best - prev_min);
+            // recurrence of pixel k (walk_line, sgm.cpp:97-195)
+            const int f = meta_first(cur_px.m.fc);
+            const int c = cur_px.v ? meta_count(cur_px.m.fc) : 0;
+            uint32_t run_min = 0xFFFFFFFFu;
+            uint32_t* cur = nullptr;
+            if (c > 0) {
+                cur = c <= caps ? (prev == sA ? sB : sA) : (prev == gA ? gB : gA);
+                const V phi2 = has_prev ? cur_px.phi2 : V(0);
+                const int shift = (has_prev && sn) ? sign * static_cast<int>(static_cast<int16_t>(cur_px.off)) : 0;
+                const V base_best = prev_min + phi2;
+                const int toff = f + shift - prev_first;
+                const uint16_t* cp = a.costs + cur_px.base;
+                uint32_t* ap = a.agg + cur_px.base;
+                for (int i0 = 0; i0 < c; i0 += PASS) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const int i = i0 + gl + G * k;
+                        if (i < c) {
+                            const uint32_t sc = i0 == 0 ? cur_px.s[k] : cp[i];
+                            uint32_t v;
+                            if (!has_prev) {
+                                v = sc;
+                            } else if (SENT) {
+                                const int t = min(max(toff + i, -2), prev_count + 1);
+                                const V b3 = min(static_cast<V>(prev[t - 1]), static_cast<V>(prev[t + 1])) + phi1;
+                                const V best = min(min(base_best, static_cast<V>(prev[t])), b3);
+                                v = static_cast<uint32_t>(static_cast<V>(sc) + best - prev_min);
+                            } else {
+                                const int t = toff + i;
+                                V best = base_best;
+                                if (static_cast<unsigned>(t) < static_cast<unsigned>(prev_count))
+                                    best = min(best, static_cast<V>(prev[t]));
+                                if (static_cast<unsigned>(t - 1) < static_cast<unsigned>(prev_count))
+                                    best = min(best, static_cast<V>(prev[t - 1]) + phi1);
+                                if (static_cast<unsigned>(t + 1) < static_cast<unsigned>(prev_count))
+                                    best = min(best, static_cast<V>(prev[t + 1]) + phi1);
+                                v = static_cast<uint32_t>(static_cast<V>(sc) + best - prev_min);
+                            }
+                            cur[i] = v;
+                            atomicAdd(ap + i, v);
+                            run_min = min(run_min, v);
+                        }
                     }
-                    cur[i] = v;
-                    atomicAdd(a.agg + base + i, v);
-                    run_min = min(run_min, v);
                 }
+                if (SENT && gl < kSent)
+                    cur[c + gl] = kSentinel;
             }
+            const uint32_t nmin = group_min<G>(run_min);
+            __syncwarp();
+            if (c > 0) {
+                prev_min = static_cast<V>(nmin);
+                prev = cur;
+                has_prev = true;
+                prev_first = f;
+                prev_count = c;
+            } else {
+                has_prev = false;
+            }
+            x += dx;
+            y += dy;
         }
-        const uint32_t nmin = __reduce_min_sync(gmask, run_min);
-        __syncwarp();
-        if (c > 0) {
-            prev_min = static_cast<V>(nmin);
-            prev = cur;
-            has_prev = true;
-            prev_first = f;
-            prev_count = c;
-            img_prev = img0;
-        } else {
-            has_prev = false;
-        }
-        m0 = m1;
-        rb0 = rb1;
-        img0 = img1;
-        off0 = off1;
-        cost0 = cost1;
-        v0 = v1;
-        m1 = m2;
-        rb1 = rb2;
-        img1 = img2;
-        off1 = off2;
-        v1 = v2;
-        x += dx;
-        y += dy;
     }
+done:
+    return;
 }
 
 // compute_normal_offsets (sgm.cpp:252-299) on the upscaled prior maps.
@@ -499,26 +579,37 @@ void launch_sgm(const SgmArgs& a, int total, int blocks, size_t smem, bool fast3
     }
 }
 
-template <int VARIANT, typename V, int G>
-void launch_group(const SgmArgs& a, int total, cudaStream_t s) {
+template <int VARIANT, typename V, int G, int K>
+void launch_lanes(const SgmArgs& a, int total, cudaStream_t s) {
     constexpr int LPW = 32 / G;
     const int caps = a.group_caps;
+    // line stride = 2 * caps padded so stride % 32 == G % 32: the LPW lines of
+    // a warp start in distinct banks
+    int stride = 2 * (caps + 2 * kSent);
+    stride += ((G % 32) - stride % 32 + 32) % 32;
     const int blocks = (total + kWarps * LPW - 1) / (kWarps * LPW);
-    const size_t smem = static_cast<size_t>(kWarps) * LPW * 2 * caps * sizeof(uint32_t);
-    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_group_kernel<VARIANT, V, G>,
+    const size_t smem = static_cast<size_t>(kWarps) * LPW * stride * sizeof(uint32_t);
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_lanes_kernel<VARIANT, V, G, K>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
-    sgm_group_kernel<VARIANT, V, G><<<blocks, kWarps * 32, smem, s>>>(a, total, caps);
+    sgm_lanes_kernel<VARIANT, V, G, K><<<blocks, kWarps * 32, smem, s>>>(a, total, caps, stride);
 }
 
 template <int VARIANT, typename V>
 void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
-    if (a.group == 8)
-        launch_group<VARIANT, V, 8>(a, total, s);
-    else if (a.group == 16)
-        launch_group<VARIANT, V, 16>(a, total, s);
+    const int g = a.group, k = a.kper;
+    if (g == 4 && k == 4)
+        launch_lanes<VARIANT, V, 4, 4>(a, total, s);
+    else if (g == 8 && k == 2)
+        launch_lanes<VARIANT, V, 8, 2>(a, total, s);
+    else if (g == 8 && k == 4)
+        launch_lanes<VARIANT, V, 8, 4>(a, total, s);
+    else if (g == 32 && k == 1)
+        launch_lanes<VARIANT, V, 32, 1>(a, total, s);
+    else if (g == 32 && k == 4)
+        launch_lanes<VARIANT, V, 32, 4>(a, total, s);
     else
-        launch_group<VARIANT, V, 32>(a, total, s);
+        throw Error(FMVS_ERR_CONFIG, "sgm: unsupported lane blocking");
 }
 
 void sgm(const SgmArgs& a, cudaStream_t s) {

@@ -110,7 +110,8 @@ struct SgmArgs {
     int dirs[8][2];
     int pmax;                        // per-warp path buffer length
     uint32_t* scratch;               // global path buffers (2 x pmax per line)
-    int group;                       // lanes per line for Plane/SN (8, 16, 32); 0 = 1 line/warp kernel
+    int group;                       // lanes per line for Plane/SN (4, 8, 32); 0 = 1 line/warp kernel
+    int kper;                        // hypotheses per lane and pass (register blocking)
     int group_caps;                  // shared-memory path buffer length per line (grouped kernel)
 };
 void sgm(const SgmArgs& a, cudaStream_t s);

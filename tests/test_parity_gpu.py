@@ -217,10 +217,18 @@ def _volume(planes, w, h, rng, ragged=True, max_cost=300):
 DIRS = [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1), (1, -1), (-1, 1)]
 
 
-@pytest.mark.parametrize("group", ["0", "8", "16", "32"])
+def _blocking(monkeypatch, gk):
+    """Lane blocking of the SGM kernel: 'GxK' (G lanes per line, K hypotheses
+    per lane and pass) or '0' (one line per warp)."""
+    g, _, k = gk.partition("x")
+    monkeypatch.setenv("FMVS_SGM_G", g)
+    monkeypatch.setenv("FMVS_SGM_K", k or "1")
+
+
+@pytest.mark.parametrize("group", ["0", "4x4", "8x2", "8x4", "32x1", "32x4"])
 @pytest.mark.parametrize("adaptive", [False, True])
 def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive, group, monkeypatch):
-    monkeypatch.setenv("FMVS_SGM_G", group)
+    _blocking(monkeypatch, group)
     img = rng.integers(0, 256, (9, 13)).astype(np.uint8)
     intr = Intrinsics(100.0, 100.0, 6.0, 4.0, 13, 9)
     cfg = SgmConfig(SgmVariant.Plane, 8, 7.0, adaptive, 40.0, 8.0, 10.0, 2)
@@ -232,11 +240,11 @@ def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive, group, mon
             assert_same(a.values, b.values, f"path {dx},{dy}")
 
 
-@pytest.mark.parametrize("group", ["0", "8", "32"])
+@pytest.mark.parametrize("group", ["0", "4x4", "8x2", "32x4"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.SurfaceNormal, SgmVariant.PathGradient])
 @pytest.mark.parametrize("paths", [8, 4])
 def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths, group, monkeypatch):
-    monkeypatch.setenv("FMVS_SGM_G", group)
+    _blocking(monkeypatch, group)
     w, h, planes = 37, 29, 48
     img = rng.integers(0, 256, (h, w)).astype(np.uint8)
     intr = Intrinsics(40.0, 40.0, 18.0, 14.0, w, h)
@@ -256,12 +264,12 @@ def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths, group, m
     assert_same(b200.wta(a), oracle.wta(b), "wta")
 
 
-@pytest.mark.parametrize("group", ["8", "16", "32"])
+@pytest.mark.parametrize("group", ["4x4", "8x4", "32x1", "32x4"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.PathGradient])
 def test_aggregate_dense_wide(b200, oracle, rng, group, variant, monkeypatch):
-    """Dense coarsest-level shape: >32 hypotheses per pixel (multi-chunk lanes,
-    global overflow buffers of the grouped kernel)."""
-    monkeypatch.setenv("FMVS_SGM_G", group)
+    """Dense coarsest-level shape: >32 hypotheses per pixel (multi-pass lanes,
+    global overflow buffers of the lane-blocked kernel)."""
+    _blocking(monkeypatch, group)
     w, h, planes = 40, 24, 130
     img = rng.integers(0, 256, (h, w)).astype(np.uint8)
     intr = Intrinsics(40.0, 40.0, 19.5, 11.5, w, h)
@@ -342,10 +350,10 @@ E2E = [
 ]
 
 
-@pytest.mark.parametrize("group", ["8", "16"])
+@pytest.mark.parametrize("group", ["4x4", "8x2"])
 @pytest.mark.parametrize("name,scene,cfg", E2E, ids=[e[0] for e in E2E])
 def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg, group, monkeypatch):
-    monkeypatch.setenv("FMVS_SGM_G", group)
+    _blocking(monkeypatch, group)
     scene = dict(scene)
     kind = scene.pop("kind")
     bundle, _, _ = render(oracle, kind, **scene)
