@@ -233,7 +233,7 @@ def run_b200(args, rank, world, device):
     views = scene.get("views", 5)
     dev = f"cuda:{device}"
     torch.cuda.set_device(device)
-    libpath = os.path.join(ROOT, "paper_2112_00821_b200", "_lib", "libfmvs.so")
+    libpath = os.environ.get("FMVS_LIB") or os.path.join(ROOT, "paper_2112_00821_b200", "_lib", "libfmvs.so")
     if not os.path.exists(libpath):
         raise RuntimeError("libfmvs.so not built (run __graft_entry__.build())")
     M = max(1, args.inflight)

@@ -146,8 +146,9 @@ int fmvs_ctx_stage_time(fmvs_ctx* ctx, int32_t index, double* ms, int64_t* calls
 void fmvs_ctx_stage_reset(fmvs_ctx* ctx);
 /* Diagnostics of the certified census sweep (enabled by FMVS_SWEEP_STATS=1 at
  * context creation): {hypothesis-view evaluations, evaluations with an
- * undecided bit, undecided bits, exact-path views}; read-and-clear. */
-int fmvs_ctx_sweep_stats(fmvs_ctx* ctx, uint64_t out[4]);
+ * undecided bit, undecided bits, exact-path views, tile-plane iterations run,
+ * tile-plane iterations skipped, exact samples taken, 0}; read-and-clear. */
+int fmvs_ctx_sweep_stats(fmvs_ctx* ctx, uint64_t out[8]);
 /* Pinned host memory for zero-staging H2D/D2H of bundles and maps. */
 void* fmvs_host_alloc(uint64_t bytes);
 void fmvs_host_free(void* ptr);

@@ -521,9 +521,8 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         sa.plane_slicing = l == L - 1;  // uniform ranges: every pixel sweeps the whole stack
         sa.narrow_max = l == L - 1 ? 65535 : 0;
         if (ctx->sweep_stats)
-            sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(4);
-        ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { k::sweep(sa, s); });
-        ++launches;
+            sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(8);
+        ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { launches += k::sweep(sa, s); });
 
         int variant = cfg.sgm.variant;
         if (variant == FMVS_SGM_SURFACE_NORMAL && !have_prior)
@@ -719,7 +718,7 @@ int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
         FMVS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->staged, cudaEventDisableTiming));
         FMVS_CUDA_CHECK(cudaEventRecord(ctx->staged, ctx->stream));
         if (ctx->sweep_stats)
-            FMVS_CUDA_CHECK(cudaMemset(ctx->buf("sweep_stats").as<unsigned long long>(4), 0, 32));
+            FMVS_CUDA_CHECK(cudaMemset(ctx->buf("sweep_stats").as<unsigned long long>(8), 0, 64));
         *out = ctx.release();
     });
 }
@@ -754,18 +753,19 @@ void fmvs_ctx_set_timing(fmvs_ctx* ctx, int32_t enable) { ctx->timing = enable !
 
 // Diagnostics of the certified census sweep (FMVS_SWEEP_STATS=1): counts of
 // (hypothesis, view) evaluations, evaluations with >= 1 undecided bit, undecided
-// bits, exact-path views. Reads and clears the counters.
-int fmvs_ctx_sweep_stats(fmvs_ctx* ctx, uint64_t out[4]) {
+// bits, exact-path views, tile-plane iterations run, tile-plane iterations
+// skipped, exact samples taken, 0. Reads and clears the counters.
+int fmvs_ctx_sweep_stats(fmvs_ctx* ctx, uint64_t out[8]) {
     return guarded([&] {
         ctx->use();
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 8; ++i)
             out[i] = 0;
         if (!ctx->sweep_stats)
             return;
-        auto* d = ctx->buf("sweep_stats").as<unsigned long long>(4);
+        auto* d = ctx->buf("sweep_stats").as<unsigned long long>(8);
         FMVS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        FMVS_CUDA_CHECK(cudaMemcpy(out, d, 32, cudaMemcpyDeviceToHost));
-        FMVS_CUDA_CHECK(cudaMemset(d, 0, 32));
+        FMVS_CUDA_CHECK(cudaMemcpy(out, d, 64, cudaMemcpyDeviceToHost));
+        FMVS_CUDA_CHECK(cudaMemset(d, 0, 64));
     });
 }
 

@@ -289,6 +289,11 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
 // ===================================================================
 
 constexpr int kTW = 32, kTH = 8, kTiledThreads = kTW * kTH;
+// resident CTAs per SM the census kernel is compiled for (register budget)
+#ifndef FMVS_CENSUS_MINB5
+#define FMVS_CENSUS_MINB5 3
+#endif
+#define FMVS_CENSUS_MINB(n) ((n) > 25 ? 2 : FMVS_CENSUS_MINB5)
 constexpr int kNarrowMax = 192;
 constexpr int kMaxMatch = 8;
 
@@ -421,6 +426,20 @@ __device__ __forceinline__ void tile_coords(const TileParams& tp, float du, floa
     const float rx = fmaf(tp.ax, du, fmaf(tp.bx, dv, tp.cx));
     const float ry = fmaf(tp.ay, du, fmaf(tp.by, dv, tp.cy));
     const float r = __fdividef(1.0f, rz);
+    *tx = rx * r;
+    *ty = ry * r;
+}
+
+// Same as tile_coords with the reciprocal as one MUFU.RCP (rcp.approx.ftz:
+// <= 1 ulp, inside the 8-ulp division budget of make_tile_params; rz is a
+// normal positive float whenever the parameters are certified).
+__device__ __forceinline__ void tile_coords_fast(const TileParams& tp, float du, float dv, float* tx,
+                                                 float* ty) {
+    const float rz = fmaf(tp.az, du, fmaf(tp.bz, dv, tp.cz));
+    const float rx = fmaf(tp.ax, du, fmaf(tp.bx, dv, tp.cx));
+    const float ry = fmaf(tp.ay, du, fmaf(tp.by, dv, tp.cy));
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(rz));
     *tx = rx * r;
     *ty = ry * r;
 }
@@ -579,18 +598,19 @@ __device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const Vi
 }
 
 template <int WW, int WH, int NM>
-__global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_census_tiled(SweepArgs a) {
+__global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) sweep_census_tiled(SweepArgs a) {
     using namespace dev;
     using BitsT = typename std::conditional<(WW * WH - 1 > 32), uint64_t, uint32_t>::type;
-    using Scan = cub::BlockScan<int, kTiledThreads>;
     constexpr int RX = WW / 2, RY = WH / 2;
     constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
     constexpr int CENTER = (WW * WH) / 2;
     extern __shared__ float2 s_tile[];  // [NM][SH][SW] (value, bound) of the warped tile + halo
     __shared__ TileParams s_tp[kPlaneChunk][NM];
     __shared__ ViewConst s_vc[NM];
+    __shared__ uint8_t s_inflag[NM * kTW * kTH];  // certified inside flag of each window centre
+    constexpr int kTPV = kTiledThreads / NM;      // tile-build threads per view
     __shared__ int s_pmin, s_pmax;
-    __shared__ typename Scan::TempStorage s_scan;
+    __shared__ int s_count;  // exact samples listed for the current plane
     __shared__ uint32_t s_items[kItemCap];  // (thread, view, window position)
     __shared__ double s_vals[kItemCap];     // their exact FP64 samples
 
@@ -625,6 +645,7 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
     if (threadIdx.x == 0) {
         s_pmin = 0x7FFFFFFF;
         s_pmax = -1;
+        s_count = 0;
     }
     if (threadIdx.x < NM) {
         const int m = threadIdx.x;
@@ -648,49 +669,84 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
         const bool need = count > 0 && p >= first && p < first + count;
         const int slot = (p - pmin) % kPlaneChunk;
         if (slot == 0) {
-            // tile parameters of the next kPlaneChunk planes x NM views, in parallel
-            __syncthreads();
+            // tile parameters of the next kPlaneChunk planes x NM views, in
+            // parallel (the previous chunk's were last read in pass 1 of the
+            // previous plane, before its barrier I)
             for (int k = threadIdx.x; k < kPlaneChunk * NM; k += kTiledThreads) {
                 const int pp = p + k / NM, m = k % NM;
                 if (pp <= pmax)
                     s_tp[k / NM][m] = make_tile_params(s_vc[m].homs + static_cast<size_t>(pp) * 9,
                                                        x0 - RX, y0 - RY, SW - 1, SH - 1);
             }
+            __syncthreads();
         }
-        if (!__syncthreads_or(need))
-            continue;
-        // ---- warp the tile + halo of every matching view into shared memory
-        for (int s = threadIdx.x; s < NM * SN; s += kTiledThreads) {
-            const int m = s / SN, r = s - m * SN;
-            const int dv = r / SW, du = r - dv * SW;
-            const TileParams& tp = s_tp[slot][m];
-            float2 out = make_float2(0.0f, 1e30f);
-            if (!tp.exact) {
-                float tcx, tcy;
-                tile_coords(tp, float(du), float(dv), &tcx, &tcy);
-                const ViewConst& vc = s_vc[m];
-                const float fx = floorf(tcx), fy = floorf(tcy);
-                int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
-                float ax = tcx - fx, ay = tcy - fy;
-                if (X0 < 0) { X0 = 0; ax = 0.0f; }
-                else if (X0 >= vc.w - 1) { X0 = vc.w - 1; ax = 0.0f; }
-                if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
-                else if (Y0 >= vc.h - 1) { Y0 = vc.h - 1; ay = 0.0f; }
-                const uint32_t q = __ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0);
-                const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
-                const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
-                const float top = fmaf(ax, i10 - i00, i00);
-                const float bot = fmaf(ax, i11 - i01, i01);
-                const float f = fmaf(ay, bot - top, top);
-                const bool near_x = ax < tp.dx || ax > 1.0f - tp.dx;
-                const bool near_y = ay < tp.dy || ay > 1.0f - tp.dy;
-                const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
-                const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
-                out = make_float2(f, fmaf(gx, tp.dx, fmaf(gy, tp.dy, 2.0e-4f)));
+        // Three barriers per plane: tile complete (T), exact-sample list
+        // complete (I), exact samples taken (P). The tile of plane p+1 may be
+        // built while slower warps finish pass 3 of plane p: pass 3 reads
+        // neither the tile nor the inside flags, and every warp finished
+        // reading them (pass 1) before barrier I of plane p.
+        if (a.stats && threadIdx.x == 0)
+            atomicAdd(a.stats + 4, 1ull);
+        // ---- warp the tile + halo of every matching view into shared memory.
+        // Each thread serves one view (its tile parameters stay in registers)
+        // and strides over that view's samples; interior samples also record
+        // the certified inside flag of the window centre (matching.cpp:224-231).
+        if (threadIdx.x < NM * kTPV) {
+            const int m = threadIdx.x / kTPV;
+            const TileParams tp = s_tp[slot][m];
+            float2* t = s_tile + m * SN;
+            uint8_t* fl = s_inflag + m * (kTW * kTH);
+            if (tp.exact) {
+                for (int r = threadIdx.x - m * kTPV; r < SN; r += kTPV)
+                    t[r] = make_float2(0.0f, 1e30f);
+            } else {
+                const uint32_t* quad = s_vc[m].quad;
+                const int vw = s_vc[m].w, vh = s_vc[m].h;
+                const float xlo = float(-tp.xa), xhi = float(vw - 1 - tp.xa);
+                const float ylo = float(-tp.ya), yhi = float(vh - 1 - tp.ya);
+                int r = threadIdx.x - m * kTPV;
+                int dv = r / SW, du = r - dv * SW;
+                for (; r < SN; r += kTPV) {
+                    float tcx, tcy;
+                    tile_coords_fast(tp, float(du), float(dv), &tcx, &tcy);
+                    if (du >= RX && du < RX + kTW && dv >= RY && dv < RY + kTH) {
+                        uint8_t f = 2;  // undecided -> exact test in pass 1
+                        if (tcx - tp.dx >= xlo && tcy - tp.dy >= ylo && tcx + tp.dx <= xhi &&
+                            tcy + tp.dy <= yhi)
+                            f = 1;  // (float ops above are exact or err toward ambiguity)
+                        else if (tcx + tp.dx < xlo || tcy + tp.dy < ylo || tcx - tp.dx > xhi ||
+                                 tcy - tp.dy > yhi)
+                            f = 0;
+                        fl[(dv - RY) * kTW + du - RX] = f;
+                    }
+                    const float fx = floorf(tcx), fy = floorf(tcy);
+                    int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
+                    float ax = tcx - fx, ay = tcy - fy;
+                    if (X0 < 0) { X0 = 0; ax = 0.0f; }
+                    else if (X0 >= vw - 1) { X0 = vw - 1; ax = 0.0f; }
+                    if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
+                    else if (Y0 >= vh - 1) { Y0 = vh - 1; ay = 0.0f; }
+                    const uint32_t q = __ldg(quad + (Y0 * vw + X0));
+                    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
+                    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
+                    const float top = fmaf(ax, i10 - i00, i00);
+                    const float bot = fmaf(ax, i11 - i01, i01);
+                    const float f = fmaf(ay, bot - top, top);
+                    const bool near_x = ax < tp.dx || ax > 1.0f - tp.dx;
+                    const bool near_y = ay < tp.dy || ay > 1.0f - tp.dy;
+                    const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
+                    const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
+                    t[r] = make_float2(f, fmaf(gx, tp.dx, fmaf(gy, tp.dy, 2.0e-4f)));
+                    du += kTPV % SW;
+                    dv += kTPV / SW;
+                    if (du >= SW) {
+                        du -= SW;
+                        ++dv;
+                    }
+                }
             }
-            s_tile[s] = out;
         }
-        __syncthreads();
+        __syncthreads();  // T
         // ---- pass 1: FP32 census bits; undecided-bit masks only where needed
         BitsT bits[NM], uns[NM];
         uint32_t view_out = 0;    // bit m: window centre outside the view -> 255
@@ -709,17 +765,10 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
             }
             const ViewConst& vc = s_vc[m];
             // inside test of the window centre (matching.cpp:224-231), certified
-            float tcx, tcy;
-            tile_coords(tp, float(tx + RX), float(ty + RY), &tcx, &tcy);
-            const float xlo = float(-tp.xa), xhi = float(vc.w - 1 - tp.xa);
-            const float ylo = float(-tp.ya), yhi = float(vc.h - 1 - tp.ya);
-            bool inside;
-            if (tcx - tp.dx >= xlo && tcy - tp.dy >= ylo && tcx + tp.dx <= xhi && tcy + tp.dy <= yhi)
-                inside = true;  // (float ops above are exact or err toward ambiguity)
-            else if (tcx + tp.dx < xlo || tcy + tp.dy < ylo || tcx - tp.dx > xhi || tcy - tp.dy > yhi)
-                inside = false;
-            else
-                inside = exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd);
+            // in the tile build; undecided -> the reference's exact FP64 test
+            const uint8_t fl = s_inflag[m * (kTW * kTH) + threadIdx.x];
+            const bool inside = fl == 2 ? exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd)
+                                        : fl == 1;
             if (!inside) {
                 view_out |= 1u << m;
                 continue;
@@ -756,8 +805,11 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
             }
         }
         // ---- pass 1b: CTA-wide list of the samples that need the exact walk
-        int off, total;
-        Scan(s_scan).ExclusiveSum(my_items, off, total);
+        // (slots allocated with a shared-memory atomic: the list order varies,
+        // each thread reads back exactly its own slots)
+        int off = 0;
+        if (my_items)
+            off = atomicAdd(&s_count, my_items);
         if (my_items) {
             int k = off;
 #pragma unroll
@@ -777,9 +829,12 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
                 }
             }
         }
-        __syncthreads();
+        __syncthreads();  // I
         // ---- pass 2: exact FP64 samples, one per thread (fully SIMT-parallel)
+        const int total = s_count;
         const int nitems = min(total, kItemCap);
+        if (a.stats && threadIdx.x == 0)
+            atomicAdd(a.stats + 6, static_cast<unsigned long long>(total));
         for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
             const uint32_t item = s_items[it];
             const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = item >> 12;
@@ -788,7 +843,9 @@ __global__ void __launch_bounds__(kTiledThreads, (WW * WH > 25 ? 2 : 3)) sweep_c
                                              vc.h, double(x0 + t % kTW), double(y0 + t / kTW), RX,
                                              RY, pos / WW, pos % WW);
         }
-        __syncthreads();
+        __syncthreads();  // P
+        if (threadIdx.x == 0)
+            s_count = 0;  // next plane allocates after its barrier T
         // ---- pass 3: resolve undecided bits, per-side sums, min -> u16
         if (need) {
             int sum_l = 0, sum_r = 0, k = off;
@@ -1201,7 +1258,7 @@ bool launch_tiled(const SweepArgs& a, dim3 grid, cudaStream_t s) {
 
 }  // namespace
 
-void sweep(const SweepArgs& a_in, cudaStream_t s) {
+int sweep(const SweepArgs& a_in, cudaStream_t s) {
     SweepArgs a = a_in;
     const bool tiled = !a.disable_tiled &&
                        (a.nmatch == 2 || a.nmatch == 4 || a.nmatch == 6 || a.nmatch == 8);
@@ -1221,7 +1278,7 @@ void sweep(const SweepArgs& a_in, cudaStream_t s) {
         sweep_kernel<FMVS_COST_NCC, 9, 9><<<grid, kThreads, 0, s>>>(a);
     FMVS_CUDA_CHECK(cudaGetLastError());
     if (!tiled)
-        return;
+        return 1;
     // Dense levels with few tiles: split the plane range across gridDim.z so
     // the launch covers >= ~4 waves of 148 SMs x 3 CTAs.
     const int tiles = ((a.w + kTW - 1) / kTW) * ((a.h + kTH - 1) / kTH);
@@ -1239,6 +1296,7 @@ void sweep(const SweepArgs& a_in, cudaStream_t s) {
     else
         launch_ncc<9, 9>(a, tgrid, s);
     FMVS_CUDA_CHECK(cudaGetLastError());
+    return 2;  // exact (wide pixels) + tiled
 }
 
 }  // namespace k

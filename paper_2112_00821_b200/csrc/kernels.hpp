@@ -70,9 +70,11 @@ struct SweepArgs {
     int disable_tiled;               // force the exact per-hypothesis kernel
     int plane_slicing;               // dense ranges: split planes across CTAs (grid z)
     int narrow_max;                  // pixels with more hypotheses take the exact kernel (0: default)
-    unsigned long long* stats;       // optional diagnostics: [view-evals, unsure evals, unsure bits, exact views]
+    unsigned long long* stats;       // optional diagnostics (fmvs_ctx_sweep_stats)
 };
-void sweep(const SweepArgs& a, cudaStream_t s);
+// returns the number of kernels launched
+int sweep(const SweepArgs& a, cudaStream_t s);
+
 
 // ---- K5: surface-normal SGM shifts (sgm.cpp:252-299) ---------------------
 struct OffsetArgs {

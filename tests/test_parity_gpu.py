@@ -105,7 +105,9 @@ def test_sweep_cost_volume_bitexact(b200, oracle, rng, cost):
 def test_sweep_certified_census_ties(b200, oracle, rng, texture, cost):
     """Flat / quantised / noisy / ramp images stress the certified FP32 census
     and NCC paths: exact FP64 ties, near-ties, flat windows (var_b <= 0) and
-    costs on rounding boundaries must fall back to the reference walk."""
+    costs on rounding boundaries must fall back to the reference walk. The
+    constant image leaves every census bit undecided, overflowing the per-warp
+    exact-sample list (lanes then walk serially)."""
     bundle, stack = _level_inputs(oracle, w=70, h=44)
     for v in bundle:
         if texture == "quantized":
