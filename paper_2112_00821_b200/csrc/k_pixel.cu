@@ -92,7 +92,16 @@ __global__ void wta_depth_kernel(WtaArgs a) {
 }
 
 // median_filter_5x5 (pipeline.cpp:175-198): element valid/2 of the sorted
-// valid window, by exact rank selection (no sort).
+// valid window. The 25 samples sit in registers (invalid / outside -> +inf,
+// which sorts behind every valid depth), a fully unrolled Batcher odd-even
+// merge network over 32 slots sorts them, and element valid/2 is picked by a
+// static select chain: no local memory, no data-dependent indexing. Sorting
+// only permutes values, so the result is exactly the reference's element.
+// Batcher odd-even merge sorting network over 32 slots (generated).
+constexpr int kMedianComparators = 191;
+__device__ constexpr int8_t kMedianA[kMedianComparators] = {0,2,4,6,8,10,12,14,16,18,20,22,24,26,28,30,0,1,4,5,8,9,12,13,16,17,20,21,24,25,28,29,1,5,9,13,17,21,25,29,0,1,2,3,8,9,10,11,16,17,18,19,24,25,26,27,2,3,10,11,18,19,26,27,1,3,5,9,11,13,17,19,21,25,27,29,0,1,2,3,4,5,6,7,16,17,18,19,20,21,22,23,4,5,6,7,20,21,22,23,2,3,6,7,10,11,18,19,22,23,26,27,1,3,5,7,9,11,13,17,19,21,23,25,27,29,0,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15,8,9,10,11,12,13,14,15,4,5,6,7,12,13,14,15,20,21,22,23,2,3,6,7,10,11,14,15,18,19,22,23,26,27,1,3,5,7,9,11,13,15,17,19,21,23,25,27,29};
+__device__ constexpr int8_t kMedianB[kMedianComparators] = {1,3,5,7,9,11,13,15,17,19,21,23,25,27,29,31,2,3,6,7,10,11,14,15,18,19,22,23,26,27,30,31,2,6,10,14,18,22,26,30,4,5,6,7,12,13,14,15,20,21,22,23,28,29,30,31,4,5,12,13,20,21,28,29,2,4,6,10,12,14,18,20,22,26,28,30,8,9,10,11,12,13,14,15,24,25,26,27,28,29,30,31,8,9,10,11,24,25,26,27,4,5,8,9,12,13,20,21,24,25,28,29,2,4,6,8,10,12,14,18,20,22,24,26,28,30,16,17,18,19,20,21,22,23,24,25,26,27,28,29,30,31,16,17,18,19,20,21,22,23,8,9,10,11,16,17,18,19,24,25,26,27,4,5,8,9,12,13,16,17,20,21,24,25,28,29,2,4,6,8,10,12,14,16,18,20,22,24,26,28,30};
+
 __global__ void median5_kernel(const float* __restrict__ in, int w, int h,
                                float* __restrict__ out) {
     using namespace dev;
@@ -100,34 +109,42 @@ __global__ void median5_kernel(const float* __restrict__ in, int w, int h,
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= w || y >= h)
         return;
-    float win[25];
+    constexpr int N = 32;
+    float v[N];
     int in_image = 0, valid = 0;
 #pragma unroll
     for (int dy = -2; dy <= 2; ++dy)
 #pragma unroll
         for (int dx = -2; dx <= 2; ++dx) {
             const int xx = x + dx, yy = y + dy;
-            if (xx < 0 || yy < 0 || xx >= w || yy >= h)
-                continue;
-            ++in_image;
-            const float d = __ldg(in + static_cast<size_t>(yy) * w + xx);
-            if (depth_ok(d))
-                win[valid++] = d;
+            const int i = (dy + 2) * 5 + dx + 2;
+            float d = INFINITY;
+            if (xx >= 0 && yy >= 0 && xx < w && yy < h) {
+                ++in_image;
+                d = __ldg(in + static_cast<size_t>(yy) * w + xx);
+                if (depth_ok(d))
+                    ++valid;
+                else
+                    d = INFINITY;
+            }
+            v[i] = d;
         }
+#pragma unroll
+    for (int i = 25; i < N; ++i)
+        v[i] = INFINITY;
+#pragma unroll
+    for (int c = 0; c < kMedianComparators; ++c) {
+        const float lo = fminf(v[kMedianA[c]], v[kMedianB[c]]);
+        const float hi = fmaxf(v[kMedianA[c]], v[kMedianB[c]]);
+        v[kMedianA[c]] = lo;
+        v[kMedianB[c]] = hi;
+    }
     float res = 0.0f;
     if (!(2 * valid < in_image)) {
         const int k = valid / 2;
-        for (int i = 0; i < valid; ++i) {
-            int less = 0, leq = 0;
-            for (int j = 0; j < valid; ++j) {
-                less += win[j] < win[i];
-                leq += win[j] <= win[i];
-            }
-            if (less <= k && k < leq) {
-                res = win[i];
-                break;
-            }
-        }
+#pragma unroll
+        for (int i = 0; i < 25; ++i)
+            res = k == i ? v[i] : res;
     }
     out[static_cast<size_t>(y) * w + x] = res;
 }
