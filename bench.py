@@ -176,7 +176,7 @@ def alg_bytes(stage, stats, n_views, paths):
 # scripts/ncu_summary.py), per stage: DRAM bytes of one launch and SM
 # throughput. Read from the committed summary; never measured under ncu here.
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "r1", "ncu_c2_full.json")
-NCU_KEYS = {"sweep_l0": "full_sweep_census_tiled", "sgm_l0": "full_sgm_group_kernel"}
+NCU_KEYS = {"sweep_l0": "full_sweep_census_tiled", "sgm_l0": "full_sgm_lanes_kernel"}
 
 
 def roofline_entry(stage, st, peak, peak_src):
