@@ -272,6 +272,57 @@ int fmvs_render_plane_scene(fmvs_ctx* ctx, int32_t kind, int32_t width, int32_t 
                             uint8_t* images, float* gt_depth, float* gt_normals_xyz,
                             fmvs_intrinsics* intr, fmvs_pose* poses);
 
+/* ------------------------------------------ post-filters -- */
+/* dog_mask (postfilter.hpp:13-18, postfilter.cpp:67-79): out = width*height
+ * bytes, 1 = textured (keep). */
+int fmvs_dog_mask(fmvs_ctx* ctx, const uint8_t* image, int32_t width, int32_t height,
+                  uint8_t* out);
+/* apply_mask (postfilter.hpp:20-22, postfilter.cpp:81-93), in place on host
+ * maps of width*height pixels (normals interleaved xyz). */
+int fmvs_apply_mask(fmvs_ctx* ctx, float* depth, float* normals_xyz, float* confidence,
+                    int32_t width, int32_t height, const uint8_t* mask);
+/* ConsistencyView (postfilter.hpp:24-28): depth map (width*height floats) with
+ * its camera. */
+typedef struct fmvs_consistency_view {
+    const float* depth;
+    int32_t width, height;
+    fmvs_intrinsics intrinsics;
+    fmvs_pose pose;
+} fmvs_consistency_view;
+enum { FMVS_LOOKUP_NEAREST = 0, FMVS_LOOKUP_BILINEAR = 1 };   /* DepthLookup, postfilter.hpp:30 */
+/* GeomFilterConfig (postfilter.hpp:32-36). */
+typedef struct fmvs_geom_filter_config {
+    double eta_r;   /* reprojection threshold, pixels (10) */
+    int32_t eta_h;  /* required consistent neighbour views (3) */
+    int32_t lookup; /* FMVS_LOOKUP_* (nearest) */
+} fmvs_geom_filter_config;
+void fmvs_geom_filter_config_default(fmvs_geom_filter_config* cfg);
+/* geometric_consistency_mask (postfilter.hpp:44-45, postfilter.cpp:95-160):
+ * keep = width*height bytes of window[ref_index]; 1 = keep. */
+int fmvs_geometric_consistency_mask(fmvs_ctx* ctx, const fmvs_consistency_view* window,
+                                    int32_t n_views, int32_t ref_index,
+                                    const fmvs_geom_filter_config* cfg, uint8_t* keep);
+
+/* -------------------------------------- sequence driver -- */
+enum { FMVS_FILTER_NONE = 0, FMVS_FILTER_DOG = 1, FMVS_FILTER_GEOM = 2, FMVS_FILTER_BOTH = 3 };
+/* The `fassmvs estimate` loop over a frame sequence (tools/fassmvs.cpp:
+ * 92-176) without the file I/O: bundles of cfg->bundle_size consecutive
+ * frames centred on ref = half, half + stride, ... while ref + half <
+ * n_frames, each estimated on the device; then (filter) the DoG texture mask
+ * of each result's reference frame, and the geometric consistency mask of each
+ * result against a window of min(5, m) neighbouring results (all masks
+ * computed before any is applied, :163-176). Frames are host images; results
+ * are written result-major: depth[r*W*H], normals_xyz[r*3*W*H],
+ * confidence[r*W*H] (all frames must share one size), ref_frames[r] = the
+ * reference frame index. *n_results is always set; FMVS_ERR_CAPACITY if it
+ * exceeds capacity. Errors follow the CLI: ConfigError for an invalid bundle
+ * size, stride or filter and for a geometric window smaller than eta_h + 1;
+ * InvalidInputError for a sequence shorter than one bundle. */
+int fmvs_estimate_sequence(fmvs_ctx* ctx, const fmvs_view* frames, int32_t n_frames,
+                           int32_t stride, const fmvs_config* cfg, int32_t filter,
+                           float* depth, float* normals_xyz, float* confidence,
+                           int32_t* ref_frames, int32_t capacity, int32_t* n_results);
+
 #ifdef __cplusplus
 }
 #endif

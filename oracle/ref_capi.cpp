@@ -5,7 +5,9 @@
 //
 // TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
 // CPU-baseline leg load this library. Nothing here is on the product path.
+#include <algorithm>
 #include <cstring>
+#include <stdexcept>
 #include <exception>
 #include <string>
 #include <vector>
@@ -468,12 +470,132 @@ int ref_render_plane_scene(void*, int32_t kind, int32_t w, int32_t h, double foc
     });
 }
 
-// DoG texture mask (postfilter.hpp:18-48), used by the accuracy criteria.
-int ref_dog_mask(const uint8_t* image, int32_t w, int32_t h, uint8_t* out) {
+// --- post-filters (postfilter.hpp) and the CLI estimate loop ------------
+
+
+// dog_mask (postfilter.hpp:18, postfilter.cpp:67-79).
+int ref_dog_mask(void*, const uint8_t* image, int32_t w, int32_t h, uint8_t* out) {
     return guard([&] {
         const TextureMask m = dog_mask(to_image(image, w, h));
         for (std::size_t p = 0; p < m.size(); ++p)
             out[p] = m.data()[p] ? 1 : 0;
+    });
+}
+
+// apply_mask (postfilter.hpp:21-22), in place.
+int ref_apply_mask(void*, float* depth, float* normals_xyz, float* confidence, int32_t w, int32_t h,
+                   const uint8_t* mask) {
+    return guard([&] {
+        DepthMap d = to_depth(depth, w, h);
+        NormalMap n = make_normal_map(w, h);
+        for (int i = 0; i < w * h; ++i)
+            n.data()[i] = Eigen::Vector3f(normals_xyz[3 * i], normals_xyz[3 * i + 1], normals_xyz[3 * i + 2]);
+        ConfidenceMap c = to_depth(confidence, w, h);
+        TextureMask m(w, h, 0);
+        std::memcpy(m.data(), mask, static_cast<std::size_t>(w) * h);
+        apply_mask(d, n, c, m);
+        std::memcpy(depth, d.data(), sizeof(float) * d.size());
+        write_normals(n, normals_xyz);
+        std::memcpy(confidence, c.data(), sizeof(float) * c.size());
+    });
+}
+
+void ref_geom_filter_config_default(fmvs_geom_filter_config* c) {
+    const GeomFilterConfig g;
+    c->eta_r = g.eta_r;
+    c->eta_h = g.eta_h;
+    c->lookup = g.lookup == DepthLookup::Bilinear ? FMVS_LOOKUP_BILINEAR : FMVS_LOOKUP_NEAREST;
+}
+
+// geometric_consistency_mask (postfilter.hpp:44-45, postfilter.cpp:95-160).
+int ref_geometric_consistency_mask(void*, const fmvs_consistency_view* window, int32_t n,
+                                   int32_t ref_index, const fmvs_geom_filter_config* cfg,
+                                   uint8_t* keep) {
+    return guard([&] {
+        std::vector<ConsistencyView> win(n);
+        for (int i = 0; i < n; ++i)
+            win[i] = {to_depth(window[i].depth, window[i].width, window[i].height),
+                      to_intr(window[i].intrinsics), to_pose(window[i].pose)};
+        GeomFilterConfig g;
+        if (cfg) {
+            g.eta_r = cfg->eta_r;
+            g.eta_h = cfg->eta_h;
+            g.lookup = cfg->lookup == FMVS_LOOKUP_BILINEAR ? DepthLookup::Bilinear : DepthLookup::Nearest;
+        }
+        const TextureMask m = geometric_consistency_mask(win, ref_index, g);
+        for (std::size_t p = 0; p < m.size(); ++p)
+            keep[p] = m.data()[p] ? 1 : 0;
+    });
+}
+
+// The `fassmvs estimate` loop (tools/fassmvs.cpp:92-176) restated with the
+// reference's own library calls, minus file I/O and the report: the oracle of
+// fmvs_estimate_sequence.
+int ref_estimate_sequence(void*, const fmvs_view* frames_c, int32_t n_frames, int32_t stride,
+                          const fmvs_config* cfg, int32_t filter, float* depth, float* normals_xyz,
+                          float* confidence, int32_t* ref_frames, int32_t capacity,
+                          int32_t* n_results) {
+    if (n_results)
+        *n_results = 0;
+    return guard([&] {
+        if (cfg->bundle_size < 3 || cfg->bundle_size % 2 == 0)
+            throw ConfigError("--bundle-size must be odd and at least 3");
+        if (stride < 1)
+            throw ConfigError("--stride must be at least 1");
+        if (filter < 0 || filter > 3)
+            throw ConfigError("--filter must be none, dog, geom or both");
+        const PipelineConfig config = to_config(*cfg);
+        config.validate();
+        std::vector<CalibratedView> frames = to_bundle(frames_c, n_frames);
+        for (auto& v : frames)
+            v.validate();
+        if (static_cast<int>(frames.size()) < config.bundle_size)
+            throw InvalidInputError("sequence shorter than one bundle");
+        const int half = config.bundle_size / 2;
+        struct FrameResult {
+            int frame;
+            BundleResult maps;
+        };
+        std::vector<FrameResult> results;
+        for (int ref = half; ref + half < static_cast<int>(frames.size()); ref += stride) {
+            std::vector<CalibratedView> bundle(frames.begin() + (ref - half),
+                                               frames.begin() + (ref + half + 1));
+            results.push_back({ref, estimate_bundle(bundle, config)});
+        }
+        const int m = static_cast<int>(results.size());
+        if (n_results)
+            *n_results = m;
+        if (m > capacity)
+            throw std::runtime_error("capacity");
+        if (filter == 1 || filter == 3)
+            for (auto& r : results) {
+                const TextureMask mask = dog_mask(frames[r.frame].image);
+                apply_mask(r.maps.depth, r.maps.normals, r.maps.confidence, mask);
+            }
+        if (filter == 2 || filter == 3) {
+            const int window_size = std::min(5, m);
+            std::vector<TextureMask> masks(m);
+            for (int i = 0; i < m; ++i) {
+                const int start = std::clamp(i - window_size / 2, 0, m - window_size);
+                std::vector<ConsistencyView> window;
+                for (int k = start; k < start + window_size; ++k)
+                    window.push_back({results[k].maps.depth, frames[results[k].frame].intrinsics,
+                                      frames[results[k].frame].pose});
+                masks[i] = geometric_consistency_mask(window, i - start);
+            }
+            for (int i = 0; i < m; ++i)
+                apply_mask(results[i].maps.depth, results[i].maps.normals, results[i].maps.confidence,
+                           masks[i]);
+        }
+        std::size_t px = 0;
+        for (int r = 0; r < m; ++r) {
+            const BundleResult& b = results[r].maps;
+            px = b.depth.size();
+            std::memcpy(depth + r * px, b.depth.data(), sizeof(float) * px);
+            write_normals(b.normals, normals_xyz + 3 * r * px);
+            std::memcpy(confidence + r * px, b.confidence.data(), sizeof(float) * px);
+            ref_frames[r] = results[r].frame;
+        }
     });
 }
 

@@ -7,14 +7,15 @@ Python binding of that ABI, mirroring the reference API names
 binding when the library is not built raises.
 """
 from .fassmvs import (  # noqa: F401
-    AggregatedVolume, Backend, BundleResult, CalibratedView, ConfigError, CostFunctionSpec,
-    CostKind, CostVolume, CudaError, GeometryError, Intrinsics, InvalidInputError,
-    PipelineConfig, PlaneStack, Pose, RangeKind, RangePolicy, SgmConfig, SgmVariant,
-    default_backend, estimate_bundle)
+    AggregatedVolume, Backend, BundleResult, CalibratedView, ConfigError, ConsistencyView,
+    CostFunctionSpec, CostKind, CostVolume, CudaError, DepthLookup, Filter, FrameResult,
+    GeomFilterConfig, GeometryError, Intrinsics, InvalidInputError, PipelineConfig, PlaneStack,
+    Pose, RangeKind, RangePolicy, SgmConfig, SgmVariant, default_backend, estimate_bundle)
 
 __all__ = [
     "AggregatedVolume", "Backend", "BundleResult", "CalibratedView", "ConfigError",
-    "CostFunctionSpec", "CostKind", "CostVolume", "CudaError", "GeometryError", "Intrinsics",
+    "ConsistencyView", "CostFunctionSpec", "CostKind", "CostVolume", "CudaError", "DepthLookup",
+    "Filter", "FrameResult", "GeomFilterConfig", "GeometryError", "Intrinsics",
     "InvalidInputError", "PipelineConfig", "PlaneStack", "Pose", "RangeKind", "RangePolicy",
     "SgmConfig", "SgmVariant", "default_backend", "estimate_bundle",
 ]

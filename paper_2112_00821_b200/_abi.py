@@ -50,6 +50,15 @@ class Config_c(C.Structure):
                 ("cost", CostSpec_c), ("normal_smoothing_radius", C.c_int32)]
 
 
+class ConsistencyView_c(C.Structure):
+    _fields_ = [("depth", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32),
+                ("intrinsics", Intrinsics_c), ("pose", Pose_c)]
+
+
+class GeomFilterConfig_c(C.Structure):
+    _fields_ = [("eta_r", C.c_double), ("eta_h", C.c_int32), ("lookup", C.c_int32)]
+
+
 class LevelStats_c(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("planes", C.c_int32),
                 ("entries", C.c_uint64)]
@@ -108,13 +117,19 @@ SIGNATURES = {
     "upscale_nearest": (C.c_int, [P, P, I32, I32, I32, I32, I32, P]),
     "render_plane_scene": (C.c_int, [P, I32, I32, I32, D, D, D, I32, D, U64, D, P, P, P,
                                      C.POINTER(Intrinsics_c), C.POINTER(Pose_c)]),
+    "dog_mask": (C.c_int, [P, P, I32, I32, P]),
+    "apply_mask": (C.c_int, [P, P, P, P, I32, I32, P]),
+    "geom_filter_config_default": (None, [C.POINTER(GeomFilterConfig_c)]),
+    "geometric_consistency_mask": (C.c_int, [P, C.POINTER(ConsistencyView_c), I32, I32,
+                                             C.POINTER(GeomFilterConfig_c), P]),
+    "estimate_sequence": (C.c_int, [P, C.POINTER(View_c), I32, I32, C.POINTER(Config_c), I32, P, P,
+                                    P, P, I32, C.POINTER(I32)]),
 }
 
 # Entry points only the oracle library has.
 ORACLE_EXTRAS = {
     "worker_count": (C.c_int, []),
     "gaussian_blur": (C.c_int, [P, I32, I32, I32, D, P]),
-    "dog_mask": (C.c_int, [P, I32, I32, P]),
 }
 
 

@@ -1427,3 +1427,229 @@ int fmvs_render_plane_scene(fmvs_ctx* ctx, int32_t kind, int32_t w, int32_t h, d
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ post-filters (§8f) --
+namespace {
+
+// DoG texture mask of a device image (postfilter.cpp:67-79) into d_mask.
+void dog_mask_device(fmvs_ctx* ctx, const uint8_t* d_img, int w, int h, uint8_t* d_mask) {
+    cudaStream_t s = ctx->stream;
+    const size_t px = static_cast<size_t>(w) * h;
+    const std::vector<double> kw = fmvs::blur_kernel(3, 1.4);
+    k::BlurKernel bk{};
+    bk.radius = 3;
+    for (size_t i = 0; i < kw.size(); ++i)
+        bk.w[i] = kw[i];
+    float* tmp = ctx->buf("dog_tmp").as<float>(px);
+    int* labels = ctx->buf("dog_labels").as<int>(px);
+    int* sizes = ctx->buf("dog_sizes").as<int>(px);
+    uint8_t* act = ctx->buf("dog_act").as<uint8_t>(px);
+    k::gaussian_blur_dog(d_img, w, h, bk, tmp, act, s);
+    k::remove_speckles(act, w, h, 1, 7, labels, sizes, s);
+    k::dilate3(act, w, h, d_mask, s);
+    k::remove_speckles(d_mask, w, h, 0, 21, labels, sizes, s);
+}
+
+void check_geom_window(int n, int ref_index, const fmvs_geom_filter_config& c) {
+    if (c.eta_h < 1 || n < c.eta_h + 1)  // postfilter.cpp:97-100
+        fmvs::fail_config("geometric filter: window smaller than eta_h + 1 views");
+    if (ref_index < 0 || ref_index >= n)
+        fmvs::fail_input("geometric filter: reference index out of range");
+}
+
+k::GeomView geom_view(const float* d_depth, int w, int h, const fmvs_intrinsics& k0,
+                      const fmvs_pose& pose) {
+    k::GeomView g{};
+    g.depth = d_depth;
+    g.w = w;
+    g.h = h;
+    g.k = intr_of(k0);
+    for (int i = 0; i < 9; ++i)
+        g.R[i] = pose.rotation[i];
+    for (int i = 0; i < 3; ++i)
+        g.C[i] = pose.center[i];
+    return g;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmvs_dog_mask(fmvs_ctx* ctx, const uint8_t* image, int32_t w, int32_t h, uint8_t* out) {
+    return guarded([&] {
+        ctx->use();
+        if (w <= 0 || h <= 0)
+            return;
+        const size_t px = static_cast<size_t>(w) * h;
+        Tmp t;
+        const uint8_t* d_img = t.upload(image, px, ctx->stream);
+        uint8_t* d_mask = t.alloc<uint8_t>(px);
+        dog_mask_device(ctx, d_img, w, h, d_mask);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out, d_mask, px, cudaMemcpyDeviceToHost, ctx->stream));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int fmvs_apply_mask(fmvs_ctx* ctx, float* depth, float* normals_xyz, float* confidence, int32_t w,
+                    int32_t h, const uint8_t* mask) {
+    return guarded([&] {
+        ctx->use();
+        const size_t px = static_cast<size_t>(std::max(w, 0)) * std::max(h, 0);
+        if (!px)
+            return;
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        float* d = t.upload(depth, px, s);
+        float* n = t.upload(normals_xyz, 3 * px, s);
+        float* c = t.upload(confidence, px, s);
+        const uint8_t* m = t.upload(mask, px, s);
+        k::apply_mask(d, n, c, m, static_cast<int>(px), s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(depth, d, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(normals_xyz, n, 3 * px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(confidence, c, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+void fmvs_geom_filter_config_default(fmvs_geom_filter_config* c) {
+    c->eta_r = 10.0;  // postfilter.hpp:32-36
+    c->eta_h = 3;
+    c->lookup = FMVS_LOOKUP_NEAREST;
+}
+
+int fmvs_geometric_consistency_mask(fmvs_ctx* ctx, const fmvs_consistency_view* window, int32_t n,
+                                    int32_t ref_index, const fmvs_geom_filter_config* cfg,
+                                    uint8_t* keep) {
+    return guarded([&] {
+        ctx->use();
+        fmvs_geom_filter_config c;
+        fmvs_geom_filter_config_default(&c);
+        if (cfg)
+            c = *cfg;
+        check_geom_window(n, ref_index, c);
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        std::vector<k::GeomView> gv(n);
+        for (int i = 0; i < n; ++i) {
+            const size_t px = static_cast<size_t>(window[i].width) * window[i].height;
+            gv[i] = geom_view(t.upload(window[i].depth, px, s), window[i].width, window[i].height,
+                              window[i].intrinsics, window[i].pose);
+        }
+        const int w = window[ref_index].width, h = window[ref_index].height;
+        const size_t px = static_cast<size_t>(std::max(w, 0)) * std::max(h, 0);
+        if (!px)
+            return;
+        k::GeomArgs ga{};
+        ga.views = t.upload(gv.data(), gv.size(), s);
+        ga.n = n;
+        ga.ref = ref_index;
+        ga.eta_r = c.eta_r;
+        ga.eta_h = c.eta_h;
+        ga.bilinear = c.lookup == FMVS_LOOKUP_BILINEAR;
+        ga.keep = t.alloc<uint8_t>(px);
+        k::geometric_mask(ga, w, h, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(keep, ga.keep, px, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_estimate_sequence(fmvs_ctx* ctx, const fmvs_view* frames, int32_t n_frames, int32_t stride,
+                           const fmvs_config* cfg, int32_t filter, float* depth, float* normals_xyz,
+                           float* confidence, int32_t* ref_frames, int32_t capacity,
+                           int32_t* n_results) {
+    if (n_results)
+        *n_results = 0;
+    return guarded([&] {
+        ctx->use();
+        if (!cfg)
+            fmvs::fail_config("estimate: null config");
+        // tools/fassmvs.cpp:93-119 (CLI checks, then PipelineConfig::validate)
+        if (cfg->bundle_size < 3 || cfg->bundle_size % 2 == 0)
+            fmvs::fail_config("--bundle-size must be odd and at least 3");
+        if (stride < 1)
+            fmvs::fail_config("--stride must be at least 1");
+        if (filter < FMVS_FILTER_NONE || filter > FMVS_FILTER_BOTH)
+            fmvs::fail_config("--filter must be none, dog, geom or both");
+        fmvs::validate_config(*cfg);
+        for (int i = 0; i < n_frames; ++i)  // :121-133
+            fmvs::validate_view(frames[i]);
+        if (n_frames < cfg->bundle_size)  // :134-135
+            fmvs::fail_input("sequence shorter than one bundle");
+        const int half = cfg->bundle_size / 2;
+        std::vector<int> refs;  // :145-149
+        for (int r = half; r + half < n_frames; r += stride)
+            refs.push_back(r);
+        const int m = static_cast<int>(refs.size());
+        if (n_results)
+            *n_results = m;
+        if (m > capacity)
+            throw fmvs::Error(FMVS_ERR_CAPACITY, "estimate_sequence: result capacity too small");
+        const int w = frames[0].intrinsics.width, h = frames[0].intrinsics.height;
+        for (int i = 0; i < n_frames; ++i)
+            if (frames[i].intrinsics.width != w || frames[i].intrinsics.height != h)
+                fmvs::fail_input("estimate_sequence: frames must share one size");
+        const size_t px = static_cast<size_t>(w) * h;
+        cudaStream_t s = ctx->stream;
+        // frames resident on the device once; bundles reference them in place
+        uint8_t* d_frames = ctx->buf("seq_frames").as<uint8_t>(px * n_frames);
+        for (int i = 0; i < n_frames; ++i)
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(d_frames + i * px, frames[i].image, px, cudaMemcpyHostToDevice, s));
+        float* d_maps = ctx->buf("seq_maps").as<float>(5 * px * m);  // depth | normals | conf
+        float* d_depth = d_maps;
+        float* d_normals = d_maps + px * m;
+        float* d_conf = d_maps + 4 * px * m;
+        std::vector<const uint8_t*> d_images(cfg->bundle_size);
+        for (int r = 0; r < m; ++r) {
+            const int first = refs[r] - half;
+            for (int k2 = 0; k2 < cfg->bundle_size; ++k2)
+                d_images[k2] = d_frames + (first + k2) * px;
+            run_bundle(ctx, frames + first, cfg->bundle_size, *cfg, d_images.data(), d_depth + r * px,
+                       d_normals + 3 * r * px, d_conf + r * px);
+        }
+        uint8_t* d_mask = ctx->buf("seq_masks").as<uint8_t>(px * std::max(m, 1));
+        if (filter == FMVS_FILTER_DOG || filter == FMVS_FILTER_BOTH) {  // :151-158
+            for (int r = 0; r < m; ++r) {
+                dog_mask_device(ctx, d_frames + refs[r] * px, w, h, d_mask);
+                k::apply_mask(d_depth + r * px, d_normals + 3 * r * px, d_conf + r * px, d_mask,
+                              static_cast<int>(px), s);
+            }
+        }
+        if (filter == FMVS_FILTER_GEOM || filter == FMVS_FILTER_BOTH) {  // :159-176
+            fmvs_geom_filter_config gc;
+            fmvs_geom_filter_config_default(&gc);
+            const int ws = std::min(5, m);
+            check_geom_window(ws, 0, gc);
+            std::vector<k::GeomView> gv(m);
+            for (int r = 0; r < m; ++r)
+                gv[r] = geom_view(d_depth + r * px, w, h, frames[refs[r]].intrinsics, frames[refs[r]].pose);
+            k::GeomView* d_gv = ctx->buf("seq_geom_views").as<k::GeomView>(m);
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(d_gv, gv.data(), sizeof(k::GeomView) * m, cudaMemcpyHostToDevice, s));
+            // every mask from the unfiltered window before any is applied
+            for (int i = 0; i < m; ++i) {
+                const int start = std::clamp(i - ws / 2, 0, m - ws);
+                k::GeomArgs ga{};
+                ga.views = d_gv + start;
+                ga.n = ws;
+                ga.ref = i - start;
+                ga.eta_r = gc.eta_r;
+                ga.eta_h = gc.eta_h;
+                ga.bilinear = gc.lookup == FMVS_LOOKUP_BILINEAR;
+                ga.keep = d_mask + i * px;
+                k::geometric_mask(ga, w, h, s);
+            }
+            for (int i = 0; i < m; ++i)
+                k::apply_mask(d_depth + i * px, d_normals + 3 * i * px, d_conf + i * px, d_mask + i * px,
+                              static_cast<int>(px), s);
+        }
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(depth, d_depth, 4 * px * m, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(normals_xyz, d_normals, 12 * px * m, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(confidence, d_conf, 4 * px * m, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (int r = 0; r < m; ++r)
+            ref_frames[r] = refs[r];
+        finish_stats(ctx);
+        ctx->collect();
+    });
+}
+
+}  // extern "C"

@@ -352,6 +352,18 @@ std::vector<double> smoothing_table(int radius) {
     return t;
 }
 
+std::vector<double> blur_kernel(int radius, double sigma) {  // pipeline.cpp:33-40
+    std::vector<double> k(2 * radius + 1);
+    double sum = 0.0;
+    for (int i = -radius; i <= radius; ++i) {
+        k[i + radius] = std::exp(-0.5 * i * i / (sigma * sigma));
+        sum += k[i + radius];
+    }
+    for (auto& v : k)
+        v /= sum;
+    return k;
+}
+
 void blur3_kernel(double k[3]) {  // gaussian_blur(radius 1, sigma 1), pipeline.cpp:33-40
     const int radius = 1;
     const double sigma = 1.0;

@@ -128,6 +128,7 @@ double parabola_refine(double d_prev, double d_win, double d_next, double c_prev
 std::vector<long long> phi2_table(const fmvs_sgm_config& cfg);          // 256 entries
 std::vector<double> smoothing_table(int radius);                         // (2r^2+1) x 256
 void blur3_kernel(double k[3]);                                          // sigma 1, radius 1
+std::vector<double> blur_kernel(int radius, double sigma);               // pipeline.cpp:33-40
 std::vector<uint16_t> census_cost_table(int bits);                       // bits+1 entries
 
 }  // namespace fmvs

@@ -147,6 +147,40 @@ void confidence(const float* normals_xyz, int w, int h, double cos_rho, double p
 void upscale(const float* in, int iw, int ih, int ch, float* out, int ow, int oh,
              cudaStream_t s);
 
+// ---- post-filters (postfilter.cpp) -----------------------------------------
+// gaussian_blur weights (pipeline.cpp:33-40), host-computed, radius <= 7
+struct BlurKernel {
+    int radius;
+    double w[15];
+};
+// gaussian_blur(img) fused with the DoG activation |I - blur| > 0.5
+// (postfilter.cpp:68-74); tmp: w*h floats
+void gaussian_blur_dog(const uint8_t* img, int w, int h, const BlurKernel& k, float* tmp,
+                       uint8_t* mask, cudaStream_t s);
+// remove_speckles (postfilter.cpp:14-51): labels, sizes: w*h ints each
+void remove_speckles(uint8_t* mask, int w, int h, uint8_t value, int min_size, int* labels,
+                     int* sizes, cudaStream_t s);
+void dilate3(const uint8_t* in, int w, int h, uint8_t* out, cudaStream_t s);
+// apply_mask (postfilter.cpp:81-93) on device maps of n pixels
+void apply_mask(float* depth, float* normals_xyz, float* conf, const uint8_t* mask, int n,
+                cudaStream_t s);
+struct GeomView {                    // ConsistencyView (postfilter.hpp:24-28)
+    const float* depth;
+    int w, h;
+    dev::Intr k;
+    double R[9];
+    double C[3];
+};
+struct GeomArgs {
+    const GeomView* views;           // device array
+    int n, ref;
+    double eta_r;
+    int eta_h;
+    int bilinear;                    // DepthLookup::Bilinear
+    uint8_t* keep;
+};
+void geometric_mask(const GeomArgs& a, int w, int h, cudaStream_t s);
+
 // ---- synthetic input: render_scene for one textured plane ------------------
 struct RenderArgs {
     int w, h;

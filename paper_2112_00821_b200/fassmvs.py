@@ -234,6 +234,41 @@ class AggregatedVolume:  # sgm.hpp:39-49
     values: np.ndarray  # uint32 (total)
 
 
+class DepthLookup(enum.IntEnum):  # postfilter.hpp:30
+    Nearest = 0
+    Bilinear = 1
+
+
+@dataclass
+class GeomFilterConfig:  # postfilter.hpp:32-36
+    eta_r: float = 10.0
+    eta_h: int = 3
+    lookup: DepthLookup = DepthLookup.Nearest
+
+    def to_c(self) -> _abi.GeomFilterConfig_c:
+        return _abi.GeomFilterConfig_c(float(self.eta_r), int(self.eta_h), int(self.lookup))
+
+
+@dataclass
+class ConsistencyView:  # postfilter.hpp:24-28
+    depth: np.ndarray       # float32 (h, w)
+    intrinsics: "Intrinsics"
+    pose: "Pose"
+
+
+class Filter(enum.IntEnum):  # the CLI's --filter (tools/fassmvs.cpp:97-99)
+    none = 0
+    dog = 1
+    geom = 2
+    both = 3
+
+
+@dataclass
+class FrameResult:  # tools/fassmvs.cpp:140-143
+    frame: int
+    maps: BundleResult
+
+
 # ----------------------------------------------------------- helpers ------
 def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
@@ -544,6 +579,68 @@ class Backend:
         out = np.zeros((height, width) + (() if ch == 1 else (ch,)), np.float32)
         self._check(self.fn["upscale_nearest"](self.ctx, _ptr(a), iw, ih, ch, width, height, _ptr(out)))
         return out
+
+    # -------------------------------------------- post-filters (§8f)
+    def dog_mask(self, image: np.ndarray) -> np.ndarray:
+        """dog_mask (postfilter.hpp:18): uint8 (h, w), 1 = textured."""
+        img = np.ascontiguousarray(image, np.uint8)
+        h, w = img.shape
+        out = np.zeros((h, w), np.uint8)
+        self._check(self.fn["dog_mask"](self.ctx, _ptr(img), w, h, _ptr(out)))
+        return out
+
+    def apply_mask(self, depth: np.ndarray, normals: np.ndarray, confidence: np.ndarray,
+                   mask: np.ndarray) -> BundleResult:
+        """apply_mask (postfilter.hpp:21-22); returns the masked maps."""
+        d, n, c = _f32(depth).copy(), _f32(normals).copy(), _f32(confidence).copy()
+        m = np.ascontiguousarray(mask, np.uint8)
+        h, w = d.shape
+        if n.shape[:2] != (h, w) or c.shape != (h, w) or m.shape != (h, w):
+            raise InvalidInputError("apply mask: map sizes differ")
+        self._check(self.fn["apply_mask"](self.ctx, _ptr(d), _ptr(n), _ptr(c), w, h, _ptr(m)))
+        return BundleResult(d, n, c)
+
+    def geometric_consistency_mask(self, window: Sequence[ConsistencyView], ref_index: int,
+                                   config: GeomFilterConfig | None = None) -> np.ndarray:
+        """geometric_consistency_mask (postfilter.hpp:44-45): uint8 keep mask."""
+        cfg = (config or GeomFilterConfig()).to_c()
+        arr = (_abi.ConsistencyView_c * max(1, len(window)))()
+        keep = []
+        for i, v in enumerate(window):
+            d = _f32(v.depth)
+            keep.append(d)
+            arr[i].depth = _ptr(d)
+            arr[i].height, arr[i].width = d.shape
+            arr[i].intrinsics = v.intrinsics.to_c()
+            arr[i].pose = v.pose.to_c()
+        shape = window[ref_index].depth.shape if 0 <= ref_index < len(window) else (1, 1)
+        out = np.zeros(shape, np.uint8)
+        self._check(self.fn["geometric_consistency_mask"](self.ctx, arr, len(window), ref_index,
+                                                          C.byref(cfg), _ptr(out)))
+        del keep
+        return out
+
+    def estimate_sequence(self, frames: Sequence[CalibratedView], config: PipelineConfig,
+                          stride: int = 1, filter: Filter = Filter.none) -> list:
+        """The `fassmvs estimate` loop (tools/fassmvs.cpp:92-176) without file
+        I/O: list of FrameResult(frame, maps) for ref = half, half+stride, ..."""
+        views, keep = _views_c(frames)
+        cfg = config.to_c()
+        n = len(frames)
+        h, w = (frames[0].image.shape if n else (1, 1))
+        half = max(config.bundle_size, 1) // 2
+        cap = max(1, (n - 2 * half + max(stride, 1) - 1) // max(stride, 1)) if n else 1
+        depth = np.zeros((cap, h, w), np.float32)
+        normals = np.zeros((cap, h, w, 3), np.float32)
+        conf = np.zeros((cap, h, w), np.float32)
+        refs = np.zeros(cap, np.int32)
+        nres = C.c_int32(0)
+        self._check(self.fn["estimate_sequence"](self.ctx, views, n, stride, C.byref(cfg), int(filter),
+                                                 _ptr(depth), _ptr(normals), _ptr(conf), _ptr(refs),
+                                                 cap, C.byref(nres)))
+        del keep
+        return [FrameResult(int(refs[r]), BundleResult(depth[r], normals[r], conf[r]))
+                for r in range(nres.value)]
 
     # ------------------------------------------------- synthetic scenes
     def render_plane_scene(self, kind: str, width: int, height: int, focal: float, depth: float,
