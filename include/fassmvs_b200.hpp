@@ -25,6 +25,7 @@
 #include "fassmvs/errors.hpp"
 #include "fassmvs/matching.hpp"
 #include "fassmvs/pipeline.hpp"
+#include "fassmvs/postfilter.hpp"
 #include "fassmvs/sgm.hpp"
 #include "fmvs.h"
 
@@ -167,6 +168,34 @@ inline fassmvs::CostVolume sweep_cost_volume(const std::vector<fassmvs::Calibrat
     v.offset.assign(off.begin(), off.end());
     v.per_side = per_side;
     return v;
+}
+
+// fassmvs::dog_mask (postfilter.hpp:18) on the B200 library.
+inline fassmvs::TextureMask dog_mask(const fassmvs::ImageU8& image,
+                                     Context& ctx = Context::thread_default()) {
+    fassmvs::TextureMask m(image.width(), image.height(), 0);
+    check(fmvs_dog_mask(ctx.get(), image.data(), image.width(), image.height(), m.data()));
+    return m;
+}
+
+// fassmvs::geometric_consistency_mask (postfilter.hpp:44-45) on the B200 library.
+inline fassmvs::TextureMask geometric_consistency_mask(
+    const std::vector<fassmvs::ConsistencyView>& window, int ref_index,
+    const fassmvs::GeomFilterConfig& config = {}, Context& ctx = Context::thread_default()) {
+    std::vector<fmvs_consistency_view> w(window.size());
+    for (size_t k = 0; k < window.size(); ++k)
+        w[k] = fmvs_consistency_view{window[k].depth.data(), window[k].depth.width(),
+                                     window[k].depth.height(), to_c(window[k].intrinsics),
+                                     to_c(window[k].pose)};
+    const fmvs_geom_filter_config c{config.eta_r, config.eta_h,
+                                    config.lookup == fassmvs::DepthLookup::Bilinear ? FMVS_LOOKUP_BILINEAR
+                                                                                    : FMVS_LOOKUP_NEAREST};
+    const bool ok = ref_index >= 0 && ref_index < static_cast<int>(window.size());
+    fassmvs::TextureMask keep(ok ? window[ref_index].depth.width() : 0,
+                              ok ? window[ref_index].depth.height() : 0, 1);
+    check(fmvs_geometric_consistency_mask(ctx.get(), w.data(), static_cast<int32_t>(w.size()),
+                                          ref_index, &c, keep.data()));
+    return keep;
 }
 
 }  // namespace fassmvs_b200
