@@ -736,7 +736,10 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                     const bool near_y = ay < tp.dy || ay > 1.0f - tp.dy;
                     const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
                     const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
-                    t[r] = make_float2(f, fmaf(gx, tp.dx, fmaf(gy, tp.dy, 2.0e-4f)));
+                    // interval [lo, hi] of every FP64 walk value of this sample
+                    // (outward rounded)
+                    const float e = fmaf(gx, tp.dx, fmaf(gy, tp.dy, 2.0e-4f));
+                    t[r] = make_float2(__fsub_rd(f, e), __fadd_ru(f, e));
                     du += kTPV % SW;
                     dv += kTPV / SW;
                     if (du >= SW) {
@@ -774,8 +777,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                 continue;
             }
             const float2* t = s_tile + m * SN;
-            const float2 c = t[(ty + RY) * SW + tx + RX];
-            BitsT b = 0, sure = 0;
+            const float2 c = t[(ty + RY) * SW + tx + RX];  // (lo, hi) of the centre
+            BitsT lt = 0, nge = 0;
 #pragma unroll
             for (int i = 0; i < WH; ++i)
 #pragma unroll
@@ -783,16 +786,16 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                     if (i * WW + j == CENTER)
                         continue;
                     const float2 n = t[(ty + i) * SW + tx + j];
-                    const float d = n.x - c.x;
-                    // sign bit of d = (warped < centre); values are >= +0 so d is never -0.
-                    // sign bit of (E_n + E_c) - |d| = the comparison is certified
-                    // (|d| > E_n + E_c, exact test on floats; +0 counts as undecided).
-                    b = (b << 1) | static_cast<BitsT>(__float_as_uint(d) >> 31);
-                    sure = (sure << 1) | static_cast<BitsT>(__float_as_uint((n.y + c.y) - fabsf(d)) >> 31);
+                    // certified n < c  <=>  hi_n < lo_c  <=>  sign(hi_n - lo_c);
+                    // certified n >= c <=>  lo_n >= hi_c <=> !sign(lo_n - hi_c)
+                    // (float subtraction is exactly sign-correct; lo, hi > -0
+                    // except lo = -0, which only makes the test more cautious)
+                    lt = (lt << 1) | static_cast<BitsT>(__float_as_uint(n.y - c.x) >> 31);
+                    nge = (nge << 1) | static_cast<BitsT>(__float_as_uint(n.x - c.y) >> 31);
                 }
             constexpr BitsT kAll = static_cast<BitsT>(~BitsT(0)) >> (sizeof(BitsT) * 8 - (WW * WH - 1));
-            const BitsT u = ~sure & kAll;
-            bits[m] = b;
+            const BitsT u = ~lt & nge & kAll;
+            bits[m] = lt;
             uns[m] = u;
             if (u)
                 my_items += 1 + popcount_bits(u);
