@@ -265,20 +265,24 @@ __device__ __forceinline__ uint32_t group_min(uint32_t v) {
 // Operands of one pixel of a scanline, staged in registers ahead of its step.
 template <int K, typename V>
 struct LinePx {
-    // stage 1: raw loads only (no arithmetic on a value in flight, which
-    // would wait for it)
+    // stage 1: raw loads only, each landing in its final register as loaded
+    // (no conversion or arithmetic on a value in flight: any instruction that
+    // touches it, even a zero-extension, waits for the load)
     uint64_t rb;     // row base of the pixel's row
     dev::VolMeta m;  // {offset in row, first | count << 16}
-    int img;         // reference intensity
-    int off;         // SN shift of the canonical direction (unsigned-extended raw)
+    uint32_t img4;   // aligned 32-bit word holding the reference intensity
+    uint32_t off2;   // aligned 32-bit word holding the SN shift (int16)
+    int img_sh;      // bit offset of the intensity in img4
     bool v;          // inside the image
     // stage 2
     uint64_t base;   // entry index of hypothesis 0
+    int img;         // reference intensity
     V phi2;          // phi2 of the transition from the previous pixel
     uint32_t s[K];   // costs of the first pass
 };
 
-constexpr int kSgmSlots = 6;  // register pipeline depth (pixels in flight per line)
+constexpr int kSgmSlots = 8;  // register pipeline depth (pixels in flight per line)
+constexpr int kGap = 3;       // steps between a pixel's meta load and its cost loads
 constexpr int kSent = 3;      // sentinel slots on each side of a path buffer
 constexpr uint32_t kSentinel = 0x3FFFFFFFu;
 
@@ -292,10 +296,10 @@ constexpr uint32_t kSentinel = 0x3FFFFFFFu;
 // latency of one step. The operands are therefore staged through a
 // kSgmSlots-deep register pipeline, unrolled so that no slot is ever copied (a
 // register copy would wait for its pending load): at the step of pixel k the
-// meta / image / SN shift of pixel k+5 are loaded, the first-pass costs of
-// pixel k+3 (whose meta arrived two steps ago) are loaded and its phi2 is
-// looked up, and pixel k is computed from operands requested 3-5 steps
-// earlier.
+// meta / image / SN shift of pixel k+7 are loaded, the first-pass costs of
+// pixel k+4 (whose meta was requested kGap = 3 steps earlier) are loaded and
+// its phi2 is looked up, and pixel k is computed from operands requested 4-7
+// steps earlier.
 //
 // Path buffers: a per-line shared-memory double buffer (line stride padded so
 // the 32/G lines of a warp start in distinct banks); pixels wider than `caps`
@@ -362,46 +366,44 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
         }
     }
 
-    int slot = 0, sign = 1;
-    if (VARIANT == FMVS_SGM_SURFACE_NORMAL) {
-        const int cd[4][2] = {{1, 0}, {0, 1}, {1, 1}, {1, -1}};
-        for (int c = 0; c < 4; ++c) {
-            if (cd[c][0] == dx && cd[c][1] == dy) {
-                slot = c;
-                sign = 1;
-            } else if (cd[c][0] == -dx && cd[c][1] == -dy) {
-                slot = c;
-                sign = -1;
-            }
-        }
-    }
+    // SN: canonical slot of +-(dx, dy) among (1,0), (0,1), (1,1), (1,-1) and the
+    // sign of the direction (sgm.cpp:72-87), in closed form
+    const int slot = dy == 0 ? 0 : (dx == 0 ? 1 : (dx == dy ? 2 : 3));
+    const int sign = (dy == 0 || dx == 0) ? dx + dy : dx;
     const bool sn = VARIANT == FMVS_SGM_SURFACE_NORMAL && a.offsets != nullptr;
     const V phi1 = static_cast<V>(a.phi1);
     auto inside = [&](int xx, int yy) { return xx >= 0 && yy >= 0 && xx < w && yy < h; };
 
     using Px = LinePx<K, V>;
     Px P[S];
-    // stage 1: meta, row base, image, SN shift (raw)
+    // stage 1: meta, row base, image word, SN shift word (raw)
+    const int off_sh = (slot & 1) * 16;
     auto load_meta = [&](Px& q, int xx, int yy, bool valid) {
         q.v = valid;
         q.m = dev::VolMeta{0u, 0u};
         q.rb = 0;
-        q.img = 0;
-        q.off = 0;
+        q.img4 = 0;
+        q.off2 = 0;
+        q.img_sh = 0;
         if (valid) {
             const size_t p = static_cast<size_t>(yy) * w + xx;
             q.m = a.meta[p];
             q.rb = a.row_base[yy];
-            q.img = a.image[p];
+            // the aligned word holding the byte (never crosses the 256-byte
+            // aligned allocation it lies in)
+            const uintptr_t ia = reinterpret_cast<uintptr_t>(a.image + p);
+            q.img4 = __ldg(reinterpret_cast<const uint32_t*>(ia & ~uintptr_t(3)));
+            q.img_sh = static_cast<int>(ia & 3) * 8;
             if (sn)
-                q.off = a.offsets[4 * p + slot];
+                q.off2 = __ldg(reinterpret_cast<const uint32_t*>(a.offsets + 4 * p) + (slot >> 1));
         }
     };
-    // stage 2: entry base, first-pass costs, phi2 of the transition from the
-    // previous pixel
+    // stage 2: entry base, intensity, first-pass costs, phi2 of the
+    // transition from the previous pixel
     auto load_costs = [&](Px& q, const Px& qprev) {
         const int c = meta_count(q.m.fc);
         q.base = q.rb + q.m.rel;
+        q.img = static_cast<int>((q.img4 >> q.img_sh) & 0xFFu);
         const uint16_t* cp = a.costs + q.base;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -421,8 +423,10 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
         }
         P[S - 1].v = false;
         P[S - 1].img = 0;
+        P[S - 1].img4 = 0;
+        P[S - 1].img_sh = 0;
 #pragma unroll
-        for (int j = 0; j < S - 3; ++j)
+        for (int j = 0; j < S - 1 - kGap; ++j)
             load_costs(P[j], P[(j + S - 1) % S]);
     }
 
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
                 const Px& pl = P[(u + S - 2) % S];
                 load_meta(pn, x + (S - 1) * dx, y + (S - 1) * dy,
                           pl.v && inside(x + (S - 1) * dx, y + (S - 1) * dy));
-                load_costs(P[(u + S - 3) % S], P[(u + S - 4) % S]);
+                load_costs(P[(u + S - 1 - kGap) % S], P[(u + S - 2 - kGap) % S]);
             }
             // recurrence of pixel k (walk_line, sgm.cpp:97-195)
             const int f = meta_first(cur_px.m.fc);
@@ -453,7 +457,8 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
             if (c > 0) {
                 cur = c <= caps ? (prev == sA ? sB : sA) : (prev == gA ? gB : gA);
                 const V phi2 = has_prev ? cur_px.phi2 : V(0);
-                const int shift = (has_prev && sn) ? sign * static_cast<int>(static_cast<int16_t>(cur_px.off)) : 0;
+                const int shift =
+                    (has_prev && sn) ? sign * static_cast<int>(static_cast<int16_t>(cur_px.off2 >> off_sh)) : 0;
                 const V base_best = prev_min + phi2;
                 const int toff = f + shift - prev_first;
                 const uint16_t* cp = a.costs + cur_px.base;
@@ -462,16 +467,26 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         const int i = i0 + gl + G * k;
-                        if (i < c) {
+                        const bool act = i < c;
+                        if (SENT) {
+                            // branch-free: the clamped window reads sentinels
+                            // (or stale slots) for inactive lanes, whose result
+                            // is discarded; no previous pixel adds nothing
+                            const uint32_t sc = i0 == 0 ? cur_px.s[k] : (act ? cp[i] : 0u);
+                            const int t = min(max(toff + i, -2), prev_count + 1);
+                            const V b3 = min(static_cast<V>(prev[t - 1]), static_cast<V>(prev[t + 1])) + phi1;
+                            const V best = min(min(base_best, static_cast<V>(prev[t])), b3);
+                            const uint32_t v = sc + (has_prev ? static_cast<uint32_t>(best - prev_min) : 0u);
+                            if (act) {
+                                cur[i] = v;
+                                atomicAdd(ap + i, v);
+                            }
+                            run_min = min(run_min, act ? v : 0xFFFFFFFFu);
+                        } else if (act) {
                             const uint32_t sc = i0 == 0 ? cur_px.s[k] : cp[i];
                             uint32_t v;
                             if (!has_prev) {
                                 v = sc;
-                            } else if (SENT) {
-                                const int t = min(max(toff + i, -2), prev_count + 1);
-                                const V b3 = min(static_cast<V>(prev[t - 1]), static_cast<V>(prev[t + 1])) + phi1;
-                                const V best = min(min(base_best, static_cast<V>(prev[t])), b3);
-                                v = static_cast<uint32_t>(static_cast<V>(sc) + best - prev_min);
                             } else {
                                 const int t = toff + i;
                                 V best = base_best;
