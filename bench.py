@@ -64,6 +64,15 @@ WORKLOADS = {
                 step=0.59, texture=0.1, stream_frames=516),
            dict(d_min=4.0, d_max=40.0, levels=3, max_planes=128, cost="census5", variant="sn", paths=8),
            "C5: stream of 512 C2 bundles (516-frame lateral track, max overlap), sharded over GPUs"),
+    # C2 scene with the other SGM variants / the NCC matcher (variant coverage)
+    "c2pg": (dict(kind="slanted", width=1920, height=1080, focal=1920.0, depth=10.0, tilt=30.0,
+                  step=0.59, texture=0.1),
+             dict(d_min=4.0, d_max=40.0, levels=3, max_planes=128, cost="census5", variant="pg", paths=8),
+             "C2 with SGM pi-pg (path gradient) 8 paths"),
+    "c2ncc": (dict(kind="slanted", width=1920, height=1080, focal=1920.0, depth=10.0, tilt=30.0,
+                   step=0.59, texture=0.1),
+              dict(d_min=4.0, d_max=40.0, levels=3, max_planes=128, cost="ncc5", variant="sn", paths=8),
+              "C2 with the NCC 5x5 matcher, SGM pi-sn 8 paths"),
     "c4": (dict(kind="slanted", width=3840, height=2160, focal=3840.0, depth=10.0, tilt=30.0,
                 step=0.59, texture=0.05),
            dict(d_min=4.0, d_max=40.0, levels=3, max_planes=192, cost="ncc5", variant="plane", paths=8),

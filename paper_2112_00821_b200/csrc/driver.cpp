@@ -580,8 +580,6 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
             ga.group = 32;
             ga.kper = 4;
         }
-        if (variant == FMVS_SGM_PATH_GRADIENT)
-            ga.group = 0;
         ga.group_caps = l == L - 1 ? std::min(np, 1024) : 32;
         ga.scratch = (ga.group > 0 || np > pmax_smem_limit) ? sgm_scratch : nullptr;
         ctx->timed(l == 0 ? "sgm_l0" : "sgm", [&] { k::sgm(ga, s); });
@@ -1217,8 +1215,6 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         }
         ga.pmax = pmax;
         sgm_blocking(&ga.group, &ga.kper);
-        if (cfg->variant == FMVS_SGM_PATH_GRADIENT)
-            ga.group = 0;
         ga.group_caps = 32;
         const int limit = (200 * 1024) / (4 * 2 * 4);
         if (pmax > limit || ga.group > 0) {

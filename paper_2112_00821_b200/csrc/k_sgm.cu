@@ -249,6 +249,33 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
     }
 }
 
+// PlaneStack::nearest_index (geometry.cpp:75-98) with the bracketing index
+// found by a local search from `hint` instead of bisection: for a strictly
+// decreasing stack the bracket d[lo] >= delta > d[lo + 1] is unique, so the
+// result is identical, and along a smooth path it is within a few planes of
+// the previous winner.
+__device__ __forceinline__ int nearest_index_from(const double* __restrict__ d, int n, double delta,
+                                                  int hint) {
+    using namespace dev;
+    double f;
+    if (n <= 1) {
+        f = 0.0;
+    } else if (delta >= d[0]) {
+        f = div(-sub(delta, d[0]), sub(d[0], d[1]));
+    } else if (delta <= d[n - 1]) {
+        f = add(double(n - 1), div(sub(d[n - 1], delta), sub(d[n - 2], d[n - 1])));
+    } else {
+        int lo = min(max(hint, 0), n - 2);
+        while (!(d[lo] >= delta))
+            --lo;
+        while (d[lo + 1] >= delta)
+            ++lo;
+        f = add(double(lo), div(sub(d[lo], delta), sub(d[lo], d[lo + 1])));
+    }
+    const int i = static_cast<int>(llround(f));
+    return i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
+}
+
 // Minimum over the G-lane group of the calling lane (G a power of two): a
 // full-warp REDUX for G = 32, an xor butterfly otherwise (a group-masked
 // REDUX with per-group masks serialises into one pass per group).
@@ -434,6 +461,12 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
     int prev_first = 0, prev_count = 0;
     V prev_min = 0;
     const uint32_t* prev = sA;
+    // PG history of the line (sgm.cpp:28-43): the two previous winners' scene
+    // points; every lane of the group carries an identical copy
+    constexpr bool PG = VARIANT == FMVS_SGM_PATH_GRADIENT;
+    bool h1 = false, h2 = false;
+    D3 p1{0, 0, 0}, p2{0, 0, 0};
+    int h1_index = 0;
 
     for (;;) {
 #pragma unroll
@@ -453,12 +486,21 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
             const int f = meta_first(cur_px.m.fc);
             const int c = cur_px.v ? meta_count(cur_px.m.fc) : 0;
             uint32_t run_min = 0xFFFFFFFFu;
+            int run_arg = 0x7FFFFFFF;
             uint32_t* cur = nullptr;
             if (c > 0) {
                 cur = c <= caps ? (prev == sA ? sB : sA) : (prev == gA ? gB : gA);
                 const V phi2 = has_prev ? cur_px.phi2 : V(0);
-                const int shift =
+                int shift =
                     (has_prev && sn) ? sign * static_cast<int>(static_cast<int16_t>(cur_px.off2 >> off_sh)) : 0;
+                if (PG && has_prev && h1 && h2) {  // sgm.cpp:131-140
+                    const D3 pred = add3(p1, sub3(p1, p2));
+                    const double delta_pred = -dot3(D3{a.nx, a.ny, a.nz}, pred);
+                    if (delta_pred > 0.0) {
+                        const int pi = nearest_index_from(a.planes, a.nplanes, delta_pred, h1_index);
+                        shift = min(max(h1_index - pi, -3), 3);
+                    }
+                }
                 const V base_best = prev_min + phi2;
                 const int toff = f + shift - prev_first;
                 const uint16_t* cp = a.costs + cur_px.base;
@@ -481,7 +523,14 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
                                 cur[i] = v;
                                 atomicAdd(ap + i, v);
                             }
-                            run_min = min(run_min, act ? v : 0xFFFFFFFFu);
+                            if (PG) {
+                                if (act && v < run_min) {  // lanes scan ascending i
+                                    run_min = v;
+                                    run_arg = i;
+                                }
+                            } else {
+                                run_min = min(run_min, act ? v : 0xFFFFFFFFu);
+                            }
                         } else if (act) {
                             const uint32_t sc = i0 == 0 ? cur_px.s[k] : cp[i];
                             uint32_t v;
@@ -500,7 +549,10 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
                             }
                             cur[i] = v;
                             atomicAdd(ap + i, v);
-                            run_min = min(run_min, v);
+                            if (v < run_min) {
+                                run_min = v;
+                                run_arg = i;
+                            }
                         }
                     }
                 }
@@ -508,6 +560,26 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
                     cur[c + gl] = kSentinel;
             }
             const uint32_t nmin = group_min<G>(run_min);
+            if (PG) {
+                // lowest index attaining the minimum (sgm.cpp:166-174), then
+                // its scene point (sgm.cpp:176-185, scene_point :46-58)
+                const int arg = static_cast<int>(
+                    group_min<G>(run_min == nmin ? static_cast<uint32_t>(run_arg) : 0x7FFFFFFFu));
+                if (c > 0) {
+                    D3 pt;
+                    if (scene_point(a.intr, a.nx, a.ny, a.nz, a.planes[f + arg], x, y, &pt)) {
+                        h2 = h1;
+                        p2 = p1;
+                        h1 = true;
+                        p1 = pt;
+                        h1_index = f + arg;
+                    } else {
+                        h1 = h2 = false;
+                    }
+                } else {
+                    h1 = h2 = false;  // empty pixel resets the path (sgm.cpp:101-106)
+                }
+            }
             __syncwarp();
             if (c > 0) {
                 prev_min = static_cast<V>(nmin);
@@ -639,9 +711,14 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
     // path values <= 65535 + phi2_max, candidates <= value + max(phi1, phi2).
     const bool fast32 = a.phi1 >= 0 && a.phi2_max >= 0 && a.phi1 < (1ll << 28) &&
                         a.phi2_max < (1ll << 28);
-    if (a.group > 0 && a.variant != FMVS_SGM_PATH_GRADIENT) {
-        // grouped kernel; scratch (global overflow buffers) is mandatory here
-        if (a.variant == FMVS_SGM_SURFACE_NORMAL) {
+    if (a.group > 0) {
+        // lane-blocked kernel; scratch (global overflow buffers) is mandatory here
+        if (a.variant == FMVS_SGM_PATH_GRADIENT) {
+            if (fast32)
+                launch_group_g<FMVS_SGM_PATH_GRADIENT, int>(a, total, s);
+            else
+                launch_group_g<FMVS_SGM_PATH_GRADIENT, long long>(a, total, s);
+        } else if (a.variant == FMVS_SGM_SURFACE_NORMAL) {
             if (fast32)
                 launch_group_g<FMVS_SGM_SURFACE_NORMAL, int>(a, total, s);
             else
