@@ -17,7 +17,6 @@
 // 2 B per hypothesis written plus the (L2-resident) images.
 #include <type_traits>
 
-#include <cub/block/block_scan.cuh>
 
 #include "host.hpp"
 #include "kernels.hpp"
@@ -937,7 +936,6 @@ __device__ __forceinline__ int ncc_tail(double sb, double sbb, double sab, doubl
 template <int WW, int WH, int NM>
 __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a) {
     using namespace dev;
-    using Scan = cub::BlockScan<int, kTiledThreads>;
     constexpr int RX = WW / 2, RY = WH / 2, NS = WW * WH;
     constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
     extern __shared__ float2 s_tile[];  // [NM][SH][SW] (value, bound)
@@ -948,11 +946,12 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
     __shared__ TileParams64 s_tp[kPlaneChunk][NM];
     __shared__ ViewConst s_vc[NM];
     __shared__ int s_pmin, s_pmax;
-    __shared__ typename Scan::TempStorage s_scan;
+    __shared__ int s_count;  // exact samples listed for the current plane
     __shared__ uint32_t s_items[kNccItemCap];
     __shared__ double s_vals[kNccItemCap];
-    __shared__ int s_vcost[kNccItemCap / NS + 1];          // pass 2b results
+    __shared__ int s_vcost[kNccItemCap / NS + 1];  // pass 2b results
     __shared__ double s_rmean[kTiledThreads], s_rvar[kTiledThreads];
+    constexpr int kTPV = kTiledThreads / NM;  // tile-build threads per view
 
     const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
@@ -978,6 +977,7 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
     if (threadIdx.x == 0) {
         s_pmin = 0x7FFFFFFF;
         s_pmax = -1;
+        s_count = 0;
     }
     if (threadIdx.x < NM) {
         const int m = threadIdx.x;
@@ -1023,26 +1023,45 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
         const bool need = count > 0 && p >= first && p < first + count;
         const int slot = (p - pmin) % kPlaneChunk;
         if (slot == 0) {
-            __syncthreads();
+            // tile parameters of the next kPlaneChunk planes x NM views (the
+            // previous chunk's were last read in pass 1 of the previous plane,
+            // before its barrier I)
             for (int k = threadIdx.x; k < kPlaneChunk * NM; k += kTiledThreads) {
                 const int pp = p + k / NM, m = k % NM;
                 if (pp <= pmax)
                     s_tp[k / NM][m] = make_tile_params64(s_vc[m].homs + static_cast<size_t>(pp) * 9,
                                                          x0 - RX, y0 - RY, SW - 1, SH - 1);
             }
+            __syncthreads();
         }
-        if (!__syncthreads_or(need))
-            continue;
-        for (int s = threadIdx.x; s < NM * SN; s += kTiledThreads) {
-            const int m = s / SN, r = s - m * SN;
-            const int dv = r / SW, du = r - dv * SW;
-            const TileParams64& tp = s_tp[slot][m];
-            uint8_t fl = 2;
-            s_tile[s] = tp.exact ? make_float2(0.0f, 1e30f)
-                                 : tile_sample64(tp, s_vc[m], double(du), double(dv), &fl);
-            s_in[s] = fl;
+        // Four barriers per plane: tile complete (T), exact-sample list
+        // complete (I), exact samples taken (P), view costs resolved (B); the tile of plane p+1 may be
+        // built while slower warps finish pass 3 of plane p (pass 3 reads
+        // neither the tile nor the inside flags; every warp finished pass 1
+        // before barrier I of plane p).
+        // ---- tile build: each thread serves one view (parameters in
+        // registers); inside flags only for the interior (window centres)
+        if (threadIdx.x < NM * kTPV) {
+            const int m = threadIdx.x / kTPV;
+            const TileParams64 tp = s_tp[slot][m];
+            const ViewConst vc = s_vc[m];
+            float2* t = s_tile + m * SN;
+            uint8_t* fl = s_in + m * SN;
+            int r = threadIdx.x - m * kTPV;
+            int dv = r / SW, du = r - dv * SW;
+            for (; r < SN; r += kTPV) {
+                uint8_t f = 2;
+                t[r] = tp.exact ? make_float2(0.0f, 1e30f) : tile_sample64(tp, vc, double(du), double(dv), &f);
+                fl[r] = f;
+                du += kTPV % SW;
+                dv += kTPV / SW;
+                if (du >= SW) {
+                    du -= SW;
+                    ++dv;
+                }
+            }
         }
-        __syncthreads();
+        __syncthreads();  // T
         // ---- pass 1: certified NCC cost per view, or NS exact work items
         int cost[NM];
         uint32_t view_unsure = 0, view_exact = 0;
@@ -1127,8 +1146,11 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
                     atomicAdd(a.stats + 1, 1ull);
             }
         }
-        int off, total;
-        Scan(s_scan).ExclusiveSum(my_items, off, total);
+        // CTA-wide list of the exact samples (slots from a shared-memory
+        // atomic; each thread reads back exactly its own slots)
+        int off = 0;
+        if (my_items)
+            off = atomicAdd(&s_count, my_items);
         if (my_items) {
             int k = off;
 #pragma unroll
@@ -1140,8 +1162,11 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
                         s_items[k] = threadIdx.x | (m << 8) | (s << 12);
             }
         }
-        __syncthreads();
+        __syncthreads();  // I
+        const int total = s_count;
         const int nitems = min(total, kNccItemCap);
+        if (a.stats && threadIdx.x == 0)
+            atomicAdd(a.stats + 6, static_cast<unsigned long long>(total));
         for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
             const uint32_t item = s_items[it];
             const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = item >> 12;
@@ -1150,7 +1175,7 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
                                              vc.h, double(x0 + t % kTW), double(y0 + t / kTW), RX,
                                              RY, pos / WW, pos % WW);
         }
-        __syncthreads();
+        __syncthreads();  // P
         // ---- pass 2b: the reference's sums and NCC of each undecided view
         // (matching.cpp:265-279, same order), one thread per view
         const int nviews_u = nitems / NS;
@@ -1168,8 +1193,10 @@ __global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a)
             }
             s_vcost[v] = ncc_tail<NS>(sb, sbb, sab, s_rmean[t], s_rvar[t]);
         }
-        __syncthreads();
-        // ---- pass 3: costs of undecided views from pass 2b, per-side sums
+        __syncthreads();  // B
+        if (threadIdx.x == 0)
+            s_count = 0;  // next plane allocates after its barrier T
+        // ---- pass 3: costs of undecided views from their exact samples, per-side sums
         if (need) {
             int sum_l = 0, sum_r = 0, k = off;
 #pragma unroll
