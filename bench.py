@@ -221,12 +221,20 @@ def shard(n_items: int, rank: int, world: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+# Test hook: FMVS_BENCH_SHARE_DEVICE=1 runs every rank on cuda:0 with the gloo
+# backend, so the N>1 code path (sharding, barriers, max-over-ranks) can be
+# exercised on a single-GPU box. Never used for reported numbers.
+SHARE_DEVICE = os.environ.get("FMVS_BENCH_SHARE_DEVICE") == "1"
+
+
 def reduce_max(value: float, world: int, device: str = "cpu") -> float:
     """Max over ranks of a per-rank time (the timing rule); plumbing only."""
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
+    if SHARE_DEVICE:
+        device = "cpu"
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -514,8 +522,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if SHARE_DEVICE:
+            local = 0
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     result = run_b200(args, rank, world, local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

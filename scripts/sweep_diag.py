@@ -9,7 +9,7 @@ import paper_2112_00821_b200 as pkg
 from paper_2112_00821_b200 import Backend
 import bench
 
-b = Backend.b200()
+b = Backend(os.environ["FMVS_LIB"], "fmvs_") if os.environ.get("FMVS_LIB") else Backend.b200()
 wl = sys.argv[1] if len(sys.argv) > 1 else "c2"
 scene, cfgkw, _ = bench.WORKLOADS[wl]
 frames = bench.render_frames(b, scene, scene.get("views", 5))
