@@ -134,6 +134,15 @@ void sgm_blocking(int* g, int* k) {
         *k = std::atoi(e);
 }
 
+// Per-context budget of cost-volume entries for worst-case arenas
+// (FMVS_ARENA_ENTRIES overrides; default 2^30 entries = 6 GB of costs +
+// aggregate, which covers Full-HD at 511 planes).
+size_t arena_budget_entries() {
+    if (const char* e = std::getenv("FMVS_ARENA_ENTRIES"))
+        return static_cast<size_t>(std::strtoull(e, nullptr, 10));
+    return size_t(1) << 30;
+}
+
 fmvs::dev::Intr intr_of(const fmvs_intrinsics& k) { return fmvs::dev::make_intr(k); }
 
 // Host plan of one level (everything data-independent).
@@ -428,8 +437,19 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
     auto* meta = ctx->buf("meta").as<fmvs::dev::VolMeta>(max_px);
     auto* row_total = ctx->buf("row_total").as<uint32_t>(max_h);
     auto* row_base = ctx->buf("row_base").as<uint64_t>(static_cast<size_t>(L) * (max_h + 1));
-    auto* costs = ctx->buf("costs").as<uint16_t>(max_entries);
-    auto* agg = ctx->buf("agg").as<uint32_t>(max_entries);
+    // Cost-volume arenas (u16 costs + u32 aggregate). Worst case W*H*P per
+    // level, allocated once, keeps the whole bundle one asynchronous launch
+    // sequence. When that exceeds the per-context budget (4K inputs: 51 GB),
+    // each level is sized to its actual entry count instead: one host
+    // synchronisation after the level's range kernels.
+    const size_t arena_budget = arena_budget_entries();
+    const bool compact = max_entries > arena_budget;
+    uint16_t* costs = nullptr;
+    uint32_t* agg = nullptr;
+    if (!compact) {
+        costs = ctx->buf("costs").as<uint16_t>(max_entries);
+        agg = ctx->buf("agg").as<uint32_t>(max_entries);
+    }
     auto* offs = ctx->buf("offsets").as<int16_t>(4 * max_px);
     auto* depth_raw = ctx->buf("depth_raw").as<float>(max_px);
     auto* nraw = ctx->buf("normals_raw").as<float>(3 * max_px);
@@ -498,6 +518,14 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
             k::scan_rows(row_total, P.h, rb, s);
         });
         launches += 2;
+        if (compact) {
+            uint64_t entries = 0;
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(&entries, rb + P.h, sizeof(entries), cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+            const size_t need = std::max<size_t>(entries, 1);
+            costs = ctx->buf("costs").as<uint16_t>(need);
+            agg = ctx->buf("agg").as<uint32_t>(need);
+        }
 
         k::SweepArgs sa{};
         sa.w = P.w;

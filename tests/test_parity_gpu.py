@@ -352,10 +352,13 @@ E2E = [
 ]
 
 
-@pytest.mark.parametrize("group", ["4x4", "8x2"])
+@pytest.mark.parametrize("group,arena", [("4x4", None), ("8x2", None), ("4x4", "1000")])
 @pytest.mark.parametrize("name,scene,cfg", E2E, ids=[e[0] for e in E2E])
-def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg, group, monkeypatch):
+def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg, group, arena, monkeypatch):
+    """arena="1000": per-level compact cost-volume arenas (the 4K path)."""
     _blocking(monkeypatch, group)
+    if arena:
+        monkeypatch.setenv("FMVS_ARENA_ENTRIES", arena)
     scene = dict(scene)
     kind = scene.pop("kind")
     bundle, _, _ = render(oracle, kind, **scene)
