@@ -323,6 +323,22 @@ int fmvs_estimate_sequence(fmvs_ctx* ctx, const fmvs_view* frames, int32_t n_fra
                            float* depth, float* normals_xyz, float* confidence,
                            int32_t* ref_frames, int32_t capacity, int32_t* n_results);
 
+/* ------------------------------------- output stage -- */
+/* colorize_depth / colorize_normals / colorize_confidence (colorize.hpp:9-15,
+ * colorize.cpp:32-70): rgb = 3*width*height bytes. */
+int fmvs_colorize_depth(fmvs_ctx* ctx, const float* depth, int32_t width, int32_t height,
+                        double lo, double hi, uint8_t* rgb);
+int fmvs_colorize_normals(fmvs_ctx* ctx, const float* normals_xyz, int32_t width, int32_t height,
+                          uint8_t* rgb);
+int fmvs_colorize_confidence(fmvs_ctx* ctx, const float* confidence, int32_t width,
+                             int32_t height, uint8_t* rgb);
+/* write_pfm (map_io.hpp:25-26, map_io.cpp:34-44,95-113): channels 1 ("Pf",
+ * depth / confidence) or 3 ("PF", normals xyz); rows written bottom to top,
+ * little endian, byte-identical to the reference. InvalidInputError if the
+ * file cannot be written. */
+int fmvs_write_pfm(const char* path, const float* data, int32_t width, int32_t height,
+                   int32_t channels);
+
 #ifdef __cplusplus
 }
 #endif

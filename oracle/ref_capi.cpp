@@ -13,7 +13,9 @@
 #include <vector>
 
 #include "fassmvs/errors.hpp"
+#include "fassmvs/colorize.hpp"
 #include "fassmvs/geometry.hpp"
+#include "fassmvs/map_io.hpp"
 #include "fassmvs/matching.hpp"
 #include "fassmvs/parallel.hpp"
 #include "fassmvs/pipeline.hpp"
@@ -597,6 +599,27 @@ int ref_estimate_sequence(void*, const fmvs_view* frames_c, int32_t n_frames, in
             ref_frames[r] = results[r].frame;
         }
     });
+}
+
+// --- output stage: colorize.hpp / map_io.hpp ---------------------------
+
+void write_rgb(const RgbImage& img, uint8_t* rgb) {
+    for (std::size_t p = 0; p < img.size(); ++p)
+        for (int c = 0; c < 3; ++c)
+            rgb[3 * p + c] = img.data()[p][c];
+}
+
+int ref_colorize_depth(void*, const float* depth, int32_t w, int32_t h, double lo, double hi,
+                       uint8_t* rgb) {
+    return guard([&] { write_rgb(colorize_depth(to_depth(depth, w, h), lo, hi), rgb); });
+}
+
+int ref_colorize_normals(void*, const float* normals_xyz, int32_t w, int32_t h, uint8_t* rgb) {
+    return guard([&] { write_rgb(colorize_normals(to_normals(normals_xyz, w, h)), rgb); });
+}
+
+int ref_colorize_confidence(void*, const float* conf, int32_t w, int32_t h, uint8_t* rgb) {
+    return guard([&] { write_rgb(colorize_confidence(to_depth(conf, w, h)), rgb); });
 }
 
 }  // extern "C"

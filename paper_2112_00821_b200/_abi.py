@@ -124,6 +124,10 @@ SIGNATURES = {
                                              C.POINTER(GeomFilterConfig_c), P]),
     "estimate_sequence": (C.c_int, [P, C.POINTER(View_c), I32, I32, C.POINTER(Config_c), I32, P, P,
                                     P, P, I32, C.POINTER(I32)]),
+    "colorize_depth": (C.c_int, [P, P, I32, I32, D, D, P]),
+    "colorize_normals": (C.c_int, [P, P, I32, I32, P]),
+    "colorize_confidence": (C.c_int, [P, P, I32, I32, P]),
+    "write_pfm": (C.c_int, [C.c_char_p, P, I32, I32, I32]),
 }
 
 # Entry points only the oracle library has.

@@ -11,6 +11,7 @@
 // The stage entry points (fmvs_sweep_cost_volume, fmvs_aggregate, ...) run the
 // same kernels on host-provided inputs for stage-wise parity tests.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1673,6 +1674,62 @@ int fmvs_estimate_sequence(fmvs_ctx* ctx, const fmvs_view* frames, int32_t n_fra
             ref_frames[r] = refs[r];
         finish_stats(ctx);
         ctx->collect();
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------ output stage (§8f) --
+extern "C" {
+
+namespace {
+int colorize_host(fmvs_ctx* ctx, int kind, const float* in, int w, int h, double lo, double hi,
+                  uint8_t* rgb) {
+    return guarded([&] {
+        ctx->use();
+        const size_t px = static_cast<size_t>(std::max(w, 0)) * std::max(h, 0);
+        if (!px)
+            return;
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const float* d_in = t.upload(in, px * (kind == 1 ? 3 : 1), s);
+        uint8_t* d_rgb = t.alloc<uint8_t>(3 * px);
+        k::colorize(kind, d_in, static_cast<int>(px), lo, hi, d_rgb, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(rgb, d_rgb, 3 * px, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+}  // namespace
+
+int fmvs_colorize_depth(fmvs_ctx* ctx, const float* depth, int32_t w, int32_t h, double lo, double hi,
+                        uint8_t* rgb) {
+    return colorize_host(ctx, 0, depth, w, h, lo, hi, rgb);
+}
+
+int fmvs_colorize_normals(fmvs_ctx* ctx, const float* normals_xyz, int32_t w, int32_t h, uint8_t* rgb) {
+    return colorize_host(ctx, 1, normals_xyz, w, h, 0.0, 0.0, rgb);
+}
+
+int fmvs_colorize_confidence(fmvs_ctx* ctx, const float* conf, int32_t w, int32_t h, uint8_t* rgb) {
+    return colorize_host(ctx, 2, conf, w, h, 0.0, 0.0, rgb);
+}
+
+int fmvs_write_pfm(const char* path, const float* data, int32_t w, int32_t h, int32_t channels) {
+    return guarded([&] {
+        if (channels != 1 && channels != 3)
+            fmvs::fail_input("write_pfm: channels must be 1 or 3");
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f)
+            fmvs::fail_input(std::string("cannot open for writing: ") + path);  // map_io.cpp:20-25
+        const std::string hdr = std::string(channels == 1 ? "Pf" : "PF") + "\n" + std::to_string(w) +
+                                " " + std::to_string(h) + "\n-1.0\n";
+        bool ok = std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
+        const size_t row = static_cast<size_t>(w) * channels;
+        for (int y = h - 1; y >= 0 && ok; --y)  // bottom-to-top rows
+            ok = std::fwrite(data + static_cast<size_t>(y) * row, sizeof(float), row, f) == row;
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok)
+            fmvs::fail_input("short write on float map file");
     });
 }
 

@@ -181,6 +181,11 @@ struct GeomArgs {
 };
 void geometric_mask(const GeomArgs& a, int w, int h, cudaStream_t s);
 
+// ---- output stage (colorize.cpp) -------------------------------------------
+// kind 0: viridis depth in [lo, hi]; 1: (n + 1) / 2 normals (xyz input);
+// 2: gray confidence. rgb: 3 bytes per pixel.
+void colorize(int kind, const float* in, int n, double lo, double hi, uint8_t* rgb, cudaStream_t s);
+
 // ---- synthetic input: render_scene for one textured plane ------------------
 struct RenderArgs {
     int w, h;

@@ -642,6 +642,37 @@ class Backend:
         return [FrameResult(int(refs[r]), BundleResult(depth[r], normals[r], conf[r]))
                 for r in range(nres.value)]
 
+    # ------------------------------------------- output stage (§8f)
+    def colorize_depth(self, depth: np.ndarray, lo: float, hi: float) -> np.ndarray:
+        """colorize_depth (colorize.hpp:9): uint8 (h, w, 3) viridis."""
+        d = _f32(depth)
+        h, w = d.shape
+        out = np.zeros((h, w, 3), np.uint8)
+        self._check(self.fn["colorize_depth"](self.ctx, _ptr(d), w, h, float(lo), float(hi), _ptr(out)))
+        return out
+
+    def colorize_normals(self, normals: np.ndarray) -> np.ndarray:
+        """colorize_normals (colorize.hpp:12): uint8 (h, w, 3)."""
+        n = _f32(normals)
+        h, w = n.shape[:2]
+        out = np.zeros((h, w, 3), np.uint8)
+        self._check(self.fn["colorize_normals"](self.ctx, _ptr(n), w, h, _ptr(out)))
+        return out
+
+    def colorize_confidence(self, confidence: np.ndarray) -> np.ndarray:
+        """colorize_confidence (colorize.hpp:15): uint8 (h, w, 3) gray."""
+        c = _f32(confidence)
+        h, w = c.shape
+        out = np.zeros((h, w, 3), np.uint8)
+        self._check(self.fn["colorize_confidence"](self.ctx, _ptr(c), w, h, _ptr(out)))
+        return out
+
+    def write_pfm(self, path: str, data: np.ndarray) -> None:
+        """write_pfm (map_io.hpp:25-26): (h, w) -> "Pf", (h, w, 3) -> "PF"."""
+        a = _f32(data)
+        ch = 1 if a.ndim == 2 else a.shape[2]
+        self._check(self.fn["write_pfm"](path.encode(), _ptr(a), a.shape[1], a.shape[0], ch))
+
     # ------------------------------------------------- synthetic scenes
     def render_plane_scene(self, kind: str, width: int, height: int, focal: float, depth: float,
                            views: int, baseline_step: float, seed: int = 1, tilt_deg: float = 0.0,
