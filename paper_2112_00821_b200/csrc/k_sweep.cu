@@ -806,6 +806,45 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                 }
             }
         }
+        // ---- pass 1a: only undecided views that can change min(sum_l, sum_r)
+        // need resolving. A view's cost lies in [lut[h_sure], lut[h_sure +
+        // #undecided]] (the census LUT is monotone); a side whose lower bound
+        // reaches the other side's upper bound is never the strict minimum's
+        // only source, so its undecided bits may take any completion (the
+        // FP32 guess) without changing the u16 cost.
+        if (my_items && !a.plane_slicing) {  // refined levels (measured: no gain on dense ones)
+            int lo_l = 0, hi_l = 0, lo_r = 0, hi_r = 0;
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                int lo, hi;
+                if ((view_exact >> m) & 1u) {
+                    lo = 0;
+                    hi = 255;
+                } else if ((view_out >> m) & 1u) {
+                    lo = hi = 255;
+                } else {
+                    const int hs = popcount_bits((bits[m] ^ ref_bits) & ~uns[m]);
+                    lo = a.census_lut[hs];
+                    hi = a.census_lut[hs + popcount_bits(uns[m])];
+                }
+                if (s_vc[m].left) {
+                    lo_l += lo;
+                    hi_l += hi;
+                } else {
+                    lo_r += lo;
+                    hi_r += hi;
+                }
+            }
+            const bool rel_l = lo_l < hi_r, rel_r = lo_r < hi_l;
+            my_items = 0;
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                if (!(s_vc[m].left ? rel_l : rel_r))
+                    uns[m] = 0;
+                if (uns[m])
+                    my_items += 1 + popcount_bits(uns[m]);
+            }
+        }
         // ---- pass 1b: CTA-wide list of the samples that need the exact walk
         // (slots allocated with a shared-memory atomic: the list order varies,
         // each thread reads back exactly its own slots)
