@@ -339,6 +339,30 @@ int fmvs_colorize_confidence(fmvs_ctx* ctx, const float* confidence, int32_t wid
 int fmvs_write_pfm(const char* path, const float* data, int32_t width, int32_t height,
                    int32_t channels);
 
+/* --------------------------------------- accuracy scoring -- */
+/* L1Result + AccCplF (evaluation.hpp:11-30). */
+typedef struct fmvs_l1_result {
+    double l1_abs, l1_rel;
+    uint64_t valid_both;
+} fmvs_l1_result;
+typedef struct fmvs_acc_cpl_f {
+    double acc, cpl, f;
+    uint64_t valid_both, valid_est, valid_gt;
+} fmvs_acc_cpl_f;
+/* evaluate (evaluation.hpp:48-49, evaluation.cpp:28-71,110-118): l1_metrics
+ * + acc_cpl_f for n_thetas (<= 16) thresholds. Counts and ratios are exact;
+ * the L1 means are FP64 tree sums (equal to the reference's sequential sum
+ * up to FP64 rounding). InvalidInputError for empty / unequal maps or no
+ * pixel valid in both. */
+int fmvs_evaluate(fmvs_ctx* ctx, const float* est, const float* gt, int32_t width, int32_t height,
+                  const double* thetas, int32_t n_thetas, fmvs_l1_result* l1,
+                  fmvs_acc_cpl_f* scores);
+/* roc_curve (evaluation.hpp:36-41, evaluation.cpp:73-108): densities and
+ * error rates at 0.05, 0.10, ..., 1.00 (20 each), bit-identical. */
+int fmvs_roc_curve(fmvs_ctx* ctx, const float* est, const float* gt, const float* confidence,
+                   int32_t width, int32_t height, double theta, double* densities,
+                   double* error_rates);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,10 @@
 
 #include "fassmvs/errors.hpp"
 #include "fassmvs/colorize.hpp"
+#if __has_include(<json.hpp>)
+#include "fassmvs/evaluation.hpp"
+#define FMVS_REF_HAS_EVALUATION 1
+#endif
 #include "fassmvs/geometry.hpp"
 #include "fassmvs/map_io.hpp"
 #include "fassmvs/matching.hpp"
@@ -621,5 +625,33 @@ int ref_colorize_normals(void*, const float* normals_xyz, int32_t w, int32_t h, 
 int ref_colorize_confidence(void*, const float* conf, int32_t w, int32_t h, uint8_t* rgb) {
     return guard([&] { write_rgb(colorize_confidence(to_depth(conf, w, h)), rgb); });
 }
+
+#ifdef FMVS_REF_HAS_EVALUATION
+// --- accuracy scoring (evaluation.hpp) -------------------------------------
+int ref_evaluate(void*, const float* est, const float* gt, int32_t w, int32_t h,
+                 const double* thetas, int32_t n_thetas, fmvs_l1_result* l1, fmvs_acc_cpl_f* scores) {
+    return guard([&] {
+        const MetricReport r = evaluate(to_depth(est, w, h), to_depth(gt, w, h),
+                                        std::vector<double>(thetas, thetas + n_thetas));
+        l1->l1_abs = r.l1.l1_abs;
+        l1->l1_rel = r.l1.l1_rel;
+        l1->valid_both = r.l1.valid_both;
+        for (int i = 0; i < n_thetas; ++i)
+            scores[i] = {r.scores[i].acc, r.scores[i].cpl, r.scores[i].f, r.scores[i].valid_both,
+                         r.scores[i].valid_est, r.scores[i].valid_gt};
+    });
+}
+
+int ref_roc_curve(void*, const float* est, const float* gt, const float* conf, int32_t w, int32_t h,
+                  double theta, double* densities, double* error_rates) {
+    return guard([&] {
+        const RocCurve c = roc_curve(to_depth(est, w, h), to_depth(gt, w, h), to_depth(conf, w, h), theta);
+        for (std::size_t i = 0; i < c.densities.size(); ++i) {
+            densities[i] = c.densities[i];
+            error_rates[i] = c.error_rates[i];
+        }
+    });
+}
+#endif
 
 }  // extern "C"

@@ -59,6 +59,15 @@ class GeomFilterConfig_c(C.Structure):
     _fields_ = [("eta_r", C.c_double), ("eta_h", C.c_int32), ("lookup", C.c_int32)]
 
 
+class L1Result_c(C.Structure):
+    _fields_ = [("l1_abs", C.c_double), ("l1_rel", C.c_double), ("valid_both", C.c_uint64)]
+
+
+class AccCplF_c(C.Structure):
+    _fields_ = [("acc", C.c_double), ("cpl", C.c_double), ("f", C.c_double), ("valid_both", C.c_uint64),
+                ("valid_est", C.c_uint64), ("valid_gt", C.c_uint64)]
+
+
 class LevelStats_c(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("planes", C.c_int32),
                 ("entries", C.c_uint64)]
@@ -128,6 +137,8 @@ SIGNATURES = {
     "colorize_normals": (C.c_int, [P, P, I32, I32, P]),
     "colorize_confidence": (C.c_int, [P, P, I32, I32, P]),
     "write_pfm": (C.c_int, [C.c_char_p, P, I32, I32, I32]),
+    "evaluate": (C.c_int, [P, P, P, I32, I32, PD, I32, C.POINTER(L1Result_c), C.POINTER(AccCplF_c)]),
+    "roc_curve": (C.c_int, [P, P, P, P, I32, I32, D, PD, PD]),
 }
 
 # Entry points only the oracle library has.

@@ -1734,3 +1734,101 @@ int fmvs_write_pfm(const char* path, const float* data, int32_t w, int32_t h, in
 }
 
 }  // extern "C"
+
+// ------------------------------------------- accuracy scoring (§8f) --
+extern "C" {
+
+int fmvs_evaluate(fmvs_ctx* ctx, const float* est, const float* gt, int32_t w, int32_t h,
+                  const double* thetas, int32_t n_thetas, fmvs_l1_result* l1, fmvs_acc_cpl_f* scores) {
+    return guarded([&] {
+        ctx->use();
+        if (w <= 0 || h <= 0)
+            fmvs::fail_input("metrics: maps must be non-empty and equal size");  // evaluation.cpp:17-20
+        if (n_thetas < 0 || n_thetas > 16)
+            fmvs::fail_input("evaluate: at most 16 thresholds");
+        const size_t px = static_cast<size_t>(w) * h;
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const float* d_est = t.upload(est, px, s);
+        const float* d_gt = t.upload(gt, px, s);
+        k::EvalThetas th{};
+        th.n = n_thetas;
+        for (int i = 0; i < n_thetas; ++i)
+            th.theta[i] = thetas[i];
+        auto* counts = t.alloc<unsigned long long>(3 + 16);
+        const size_t nb = (px + 255) / 256;
+        auto* partials = t.alloc<double>(2 * nb);
+        auto* sums = t.alloc<double>(2);
+        k::evaluate_counts(d_est, d_gt, static_cast<int>(px), th, counts, partials, sums, s);
+        unsigned long long hc[19] = {};
+        double hs[2] = {};
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(hc, counts, sizeof(unsigned long long) * (3 + n_thetas),
+                                        cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(hs, sums, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+        const unsigned long long valid_est = hc[0], valid_gt = hc[1], both = hc[2];
+        if (both == 0)
+            fmvs::fail_input("metrics: no pixel is valid in both maps");
+        l1->valid_both = both;
+        l1->l1_abs = hs[0] / static_cast<double>(both);
+        l1->l1_rel = hs[1] / static_cast<double>(both);
+        for (int i = 0; i < n_thetas; ++i) {  // evaluation.cpp:67-70
+            fmvs_acc_cpl_f& r = scores[i];
+            const unsigned long long pass = hc[3 + i];
+            r.valid_both = both;
+            r.valid_est = valid_est;
+            r.valid_gt = valid_gt;
+            r.acc = valid_est ? static_cast<double>(pass) / valid_est : 0.0;
+            r.cpl = valid_gt ? static_cast<double>(pass) / valid_gt : 0.0;
+            r.f = (r.acc + r.cpl) > 0.0 ? 2.0 * r.acc * r.cpl / (r.acc + r.cpl) : 0.0;
+        }
+    });
+}
+
+int fmvs_roc_curve(fmvs_ctx* ctx, const float* est, const float* gt, const float* conf, int32_t w,
+                   int32_t h, double theta, double* densities, double* error_rates) {
+    return guarded([&] {
+        ctx->use();
+        if (w <= 0 || h <= 0)
+            fmvs::fail_input("metrics: maps must be non-empty and equal size");
+        const size_t px = static_cast<size_t>(w) * h;
+        const int n = static_cast<int>(px);
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const float* d_est = t.upload(est, px, s);
+        const float* d_gt = t.upload(gt, px, s);
+        const float* d_conf = t.upload(conf, px, s);
+        float* keys = t.alloc<float>(px);
+        float* keys_sorted = t.alloc<float>(px);
+        uint8_t* pass = t.alloc<uint8_t>(px);
+        uint8_t* pass_sorted = t.alloc<uint8_t>(px);
+        auto* count = t.alloc<unsigned long long>(1);
+        auto* prefix = t.alloc<unsigned long long>(20);
+        k::roc_entries(d_est, d_gt, d_conf, n, theta, keys, pass, count, s);
+        unsigned long long entries = 0;
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(&entries, count, sizeof(entries), cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (entries == 0)
+            fmvs::fail_input("roc: no valid estimates");  // evaluation.cpp:92-93
+        k::RocSteps steps{};
+        for (int step = 1; step <= 20; ++step) {  // evaluation.cpp:99-106
+            const double density = step * 0.05;
+            steps.m[step - 1] = static_cast<long long>(std::min<unsigned long long>(
+                entries, static_cast<unsigned long long>(std::ceil(density * static_cast<double>(entries)))));
+        }
+        const size_t tb = k::roc_scratch_bytes(n);
+        void* temp = t.alloc<uint8_t>(tb);
+        k::roc_sort_prefix(keys, keys_sorted, pass, pass_sorted, n, temp, tb, steps, prefix, s);
+        unsigned long long hp[20] = {};
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(hp, prefix, sizeof(hp), cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (int step = 1; step <= 20; ++step) {
+            const double density = step * 0.05;
+            const unsigned long long m = static_cast<unsigned long long>(steps.m[step - 1]);
+            densities[step - 1] = density;
+            error_rates[step - 1] = 1.0 - static_cast<double>(hp[step - 1]) / m;
+        }
+    });
+}
+
+}  // extern "C"

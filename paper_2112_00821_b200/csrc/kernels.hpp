@@ -186,6 +186,25 @@ void geometric_mask(const GeomArgs& a, int w, int h, cudaStream_t s);
 // 2: gray confidence. rgb: 3 bytes per pixel.
 void colorize(int kind, const float* in, int n, double lo, double hi, uint8_t* rgb, cudaStream_t s);
 
+// ---- accuracy scoring (evaluation.cpp:28-124) -------------------------------
+struct EvalThetas {
+    int n;                           // <= 16
+    double theta[16];
+};
+// counts: [valid_est, valid_gt, valid_both, pass(theta_0..n-1)];
+// partials: 2 doubles per 256-pixel block; sums: {sum |e-g|, sum |e-g|/g}
+void evaluate_counts(const float* est, const float* gt, int n, const EvalThetas& th,
+                     unsigned long long* counts, double* partials, double* sums, cudaStream_t s);
+struct RocSteps {
+    long long m[20];                 // retained prefix length per density step
+};
+size_t roc_scratch_bytes(int n);
+void roc_entries(const float* est, const float* gt, const float* conf, int n, double theta,
+                 float* keys, uint8_t* pass, unsigned long long* count, cudaStream_t s);
+void roc_sort_prefix(const float* keys, float* keys_sorted, const uint8_t* pass, uint8_t* pass_sorted,
+                     int n, void* temp, size_t temp_bytes, const RocSteps& steps,
+                     unsigned long long* prefix, cudaStream_t s);
+
 // ---- synthetic input: render_scene for one textured plane ------------------
 struct RenderArgs {
     int w, h;

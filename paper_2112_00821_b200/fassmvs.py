@@ -673,6 +673,36 @@ class Backend:
         ch = 1 if a.ndim == 2 else a.shape[2]
         self._check(self.fn["write_pfm"](path.encode(), _ptr(a), a.shape[1], a.shape[0], ch))
 
+    # ------------------------------------------ accuracy scoring (§8f)
+    def evaluate(self, est: np.ndarray, gt: np.ndarray, thetas=(1.25, 1.1, 1.05, 1.01)):
+        """evaluate (evaluation.hpp:48-49): ({l1_abs, l1_rel, valid_both},
+        [{acc, cpl, f, valid_both, valid_est, valid_gt} per theta])."""
+        e, g = _f32(est), _f32(gt)
+        if e.shape != g.shape or e.size == 0:
+            raise InvalidInputError("metrics: maps must be non-empty and equal size")
+        h, w = e.shape
+        th = np.ascontiguousarray(thetas, np.float64)
+        l1 = _abi.L1Result_c()
+        sc = (_abi.AccCplF_c * max(1, len(th)))()
+        self._check(self.fn["evaluate"](self.ctx, _ptr(e), _ptr(g), w, h, _pd(th), len(th), C.byref(l1), sc))
+        keys = ("acc", "cpl", "f", "valid_both", "valid_est", "valid_gt")
+        return ({"l1_abs": l1.l1_abs, "l1_rel": l1.l1_rel, "valid_both": int(l1.valid_both)},
+                [{k: getattr(sc[i], k) for k in keys} for i in range(len(th))])
+
+    def roc_curve(self, est: np.ndarray, gt: np.ndarray, confidence: np.ndarray, theta: float = 1.05):
+        """roc_curve (evaluation.hpp:36-41): (densities[20], error_rates[20])."""
+        e, g, c = _f32(est), _f32(gt), _f32(confidence)
+        if e.shape != g.shape or e.size == 0:
+            raise InvalidInputError("metrics: maps must be non-empty and equal size")
+        if c.shape != e.shape:
+            raise InvalidInputError("roc: confidence map size differs")
+        h, w = e.shape
+        dens = np.zeros(20, np.float64)
+        errs = np.zeros(20, np.float64)
+        self._check(self.fn["roc_curve"](self.ctx, _ptr(e), _ptr(g), _ptr(c), w, h, float(theta),
+                                         _pd(dens), _pd(errs)))
+        return dens, errs
+
     # ------------------------------------------------- synthetic scenes
     def render_plane_scene(self, kind: str, width: int, height: int, focal: float, depth: float,
                            views: int, baseline_step: float, seed: int = 1, tilt_deg: float = 0.0,
