@@ -297,7 +297,7 @@ struct LinePx {
     // touches it, even a zero-extension, waits for the load)
     uint64_t rb;     // row base of the pixel's row
     dev::VolMeta m;  // {offset in row, first | count << 16}
-    uint32_t img4;   // aligned 32-bit word holding the reference intensity
+    uint32_t img4;   // 32-bit word (or zero-extended byte) holding the intensity
     uint32_t off2;   // aligned 32-bit word holding the SN shift (int16)
     int img_sh;      // bit offset of the intensity in img4
     bool v;          // inside the image
@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
             gB[-kSent + gl] = kSentinel;
         }
     }
+    __syncwarp();  // sentinels visible to the group before its first window read
 
     // SN: canonical slot of +-(dx, dy) among (1,0), (0,1), (1,1), (1,-1) and the
     // sign of the direction (sgm.cpp:72-87), in closed form
@@ -404,6 +405,8 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
     using Px = LinePx<K, V>;
     Px P[S];
     // stage 1: meta, row base, image word, SN shift word (raw)
+    const uintptr_t img_lo = reinterpret_cast<uintptr_t>(a.image);
+    const uintptr_t img_hi = img_lo + static_cast<uintptr_t>(w) * h;
     const int off_sh = (slot & 1) * 16;
     auto load_meta = [&](Px& q, int xx, int yy, bool valid) {
         q.v = valid;
@@ -416,11 +419,17 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
             const size_t p = static_cast<size_t>(yy) * w + xx;
             q.m = a.meta[p];
             q.rb = a.row_base[yy];
-            // the aligned word holding the byte (never crosses the 256-byte
-            // aligned allocation it lies in)
+            // aligned 32-bit word holding the byte when it lies inside the
+            // image (a byte load otherwise); either lands in the slot register
+            // with no conversion
             const uintptr_t ia = reinterpret_cast<uintptr_t>(a.image + p);
-            q.img4 = __ldg(reinterpret_cast<const uint32_t*>(ia & ~uintptr_t(3)));
-            q.img_sh = static_cast<int>(ia & 3) * 8;
+            const uintptr_t wa = ia & ~uintptr_t(3);
+            if (wa >= img_lo && wa + 4 <= img_hi) {
+                q.img4 = __ldg(reinterpret_cast<const uint32_t*>(wa));
+                q.img_sh = static_cast<int>(ia - wa) * 8;
+            } else {
+                q.img4 = __ldg(a.image + p);
+            }
             if (sn)
                 q.off2 = __ldg(reinterpret_cast<const uint32_t*>(a.offsets + 4 * p) + (slot >> 1));
         }
