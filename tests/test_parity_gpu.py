@@ -349,6 +349,25 @@ E2E = [
     ("ncc9_sn_7views", dict(kind="slanted", w=120, h=90, focal=120.0, depth=10.0, tilt=20.0, step=0.4,
                             views=7), dict(d_min=6.0, d_max=20.0, levels=2, cost="ncc9",
                                            variant=SgmVariant.SurfaceNormal)),
+    # tilted sweep normal (test_pipeline.cpp:170-182), 3 levels, census + SN
+    ("tilted_sweep_census", dict(kind="slanted", w=120, h=90, focal=120.0, depth=8.0, tilt=30.0, step=0.6,
+                                 texture=0.4), dict(d_min=5.0, d_max=13.0, levels=2, cost="census5",
+                                                    variant=SgmVariant.SurfaceNormal,
+                                                    sweep_normal=(0.0, -0.5, -0.8660254037844386))),
+    # fixed range policy, fixed phi2, smoothing radius 3, PG
+    ("fixed_range_pg", dict(kind="slanted", w=128, h=96, focal=128.0, depth=10.0, tilt=25.0, step=0.5,
+                            texture=0.3), dict(d_min=4.0, d_max=30.0, levels=3, cost="census5",
+                                               variant=SgmVariant.PathGradient,
+                                               range_policy=RangePolicy(RangeKind.Fixed, 0.9),
+                                               normal_smoothing_radius=3)),
+    # full range policy (every refined pixel sweeps the whole stack: wide pixels)
+    ("full_range_ncc", dict(kind="fronto", w=96, h=72, focal=96.0, depth=10.0, step=0.5, texture=0.35),
+     dict(d_min=7.0, d_max=15.0, levels=2, cost="ncc5", range_policy=RangePolicy(RangeKind.Full, 0.0))),
+    # fixed phi2, 4 paths, 9 views
+    ("fixed_phi2_9views", dict(kind="slanted", w=112, h=84, focal=112.0, depth=10.0, tilt=15.0, step=0.3,
+                               views=9), dict(d_min=6.0, d_max=18.0, levels=2, cost="census5",
+                                              sgm=SgmConfig(SgmVariant.Plane, 4, 80.0, False, 300.0,
+                                                            8.0, 10.0, 1), bundle_size=9)),
 ]
 
 
