@@ -200,6 +200,16 @@ def roofline_entry(stage, st, peak, peak_src):
         e["traffic_source"] = (f"{os.path.relpath(NCU_SUMMARY, ROOT)}: dram__bytes_read.sum + "
                                f"dram__bytes_write.sum of one ncu --set full launch")
         e["sm_throughput_pct"] = m.get("sm__throughput.avg.pct_of_peak_sustained_elapsed")
+        # the binding resource of these kernels is instruction issue, not HBM
+        # (SURVEY §8d / BASELINE.md §3): its fraction from the same capture
+        e["compute_roofline"] = {
+            "resource": "SM issue slots (warp-instructions / cycle / SMSP)",
+            "frac": round(float(m.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0.0)) / 100, 4),
+            "fp64_pipe_frac": round(float(m.get(
+                "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", 0.0)) / 100, 4),
+            "alu_pipe_frac": round(float(m.get(
+                "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", 0.0)) / 100, 4),
+            "source": "ncu --set full capture (profiles/r1/ncu_c2_full.json)"}
     except (OSError, KeyError, ValueError):
         pass
     if stage.startswith("sweep"):
