@@ -605,9 +605,9 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         // coarsest level: dense ranges, one line per warp-wide group; refined
         // levels: ~12 hypotheses per pixel, 32/G lines per warp
         sgm_blocking(&ga.group, &ga.kper);
-        if (l == L - 1) {
+        if (l == L - 1) {  // dense coarsest level: one line per warp, one pass up to 256 planes
             ga.group = 32;
-            ga.kper = 4;
+            ga.kper = np > 128 ? 8 : 4;
         }
         ga.group_caps = l == L - 1 ? std::min(np, 1024) : 32;
         ga.scratch = (ga.group > 0 || np > pmax_smem_limit) ? sgm_scratch : nullptr;

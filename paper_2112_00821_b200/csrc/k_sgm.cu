@@ -308,8 +308,14 @@ struct LinePx {
     uint32_t s[K];   // costs of the first pass
 };
 
-constexpr int kSgmSlots = 8;  // register pipeline depth (pixels in flight per line)
-constexpr int kGap = 3;       // steps between a pixel's meta load and its cost loads
+#ifndef FMVS_SGM_SLOTS
+#define FMVS_SGM_SLOTS 8
+#endif
+#ifndef FMVS_SGM_GAP
+#define FMVS_SGM_GAP 3
+#endif
+constexpr int kSgmSlots = FMVS_SGM_SLOTS;  // register pipeline depth (pixels in flight per line)
+constexpr int kGap = FMVS_SGM_GAP;         // steps between a pixel's meta load and its cost loads
 constexpr int kSent = 3;      // sentinel slots on each side of a path buffer
 constexpr uint32_t kSentinel = 0x3FFFFFFFu;
 
@@ -343,7 +349,10 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
     constexpr bool SENT = sizeof(V) == 4;
     constexpr int LPW = 32 / G;
     constexpr int PASS = G * K;
-    constexpr int S = kSgmSlots;
+    // wide passes (dense coarsest levels, K = 8) keep fewer pixels in flight:
+    // each step is longer, and the slots' cost registers scale with K
+    constexpr int S = K >= 8 ? 4 : kSgmSlots;
+    constexpr int GAP = K >= 8 ? 1 : kGap;
     extern __shared__ uint32_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / G, gl = lane % G;
@@ -462,7 +471,7 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
         P[S - 1].img4 = 0;
         P[S - 1].img_sh = 0;
 #pragma unroll
-        for (int j = 0; j < S - 1 - kGap; ++j)
+        for (int j = 0; j < S - 1 - GAP; ++j)
             load_costs(P[j], P[(j + S - 1) % S]);
     }
 
@@ -489,7 +498,7 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
                 const Px& pl = P[(u + S - 2) % S];
                 load_meta(pn, x + (S - 1) * dx, y + (S - 1) * dy,
                           pl.v && inside(x + (S - 1) * dx, y + (S - 1) * dy));
-                load_costs(P[(u + S - 1 - kGap) % S], P[(u + S - 2 - kGap) % S]);
+                load_costs(P[(u + S - 1 - GAP) % S], P[(u + S - 2 - GAP) % S]);
             }
             // recurrence of pixel k (walk_line, sgm.cpp:97-195)
             const int f = meta_first(cur_px.m.fc);
@@ -704,6 +713,8 @@ void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
         launch_lanes<VARIANT, V, 32, 1>(a, total, s);
     else if (g == 32 && k == 4)
         launch_lanes<VARIANT, V, 32, 4>(a, total, s);
+    else if (g == 32 && k == 8)
+        launch_lanes<VARIANT, V, 32, 8>(a, total, s);
     else
         throw Error(FMVS_ERR_CONFIG, "sgm: unsupported lane blocking");
 }

@@ -266,7 +266,7 @@ def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths, group, m
     assert_same(b200.wta(a), oracle.wta(b), "wta")
 
 
-@pytest.mark.parametrize("group", ["4x4", "8x4", "32x1", "32x4"])
+@pytest.mark.parametrize("group", ["4x4", "8x4", "32x1", "32x4", "32x8"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.PathGradient])
 def test_aggregate_dense_wide(b200, oracle, rng, group, variant, monkeypatch):
     """Dense coarsest-level shape: >32 hypotheses per pixel (multi-pass lanes,
@@ -363,6 +363,10 @@ E2E = [
     # full range policy (every refined pixel sweeps the whole stack: wide pixels)
     ("full_range_ncc", dict(kind="fronto", w=96, h=72, focal=96.0, depth=10.0, step=0.5, texture=0.35),
      dict(d_min=7.0, d_max=15.0, levels=2, cost="ncc5", range_policy=RangePolicy(RangeKind.Full, 0.0))),
+    # dense single level with > 128 planes (coarsest-level SGM with K = 8 lanes)
+    ("dense_216_planes", dict(kind="slanted", w=96, h=64, focal=400.0, depth=10.0, tilt=20.0, step=1.2,
+                              texture=0.3), dict(d_min=4.0, d_max=40.0, levels=1, cost="census5",
+                                                 max_planes=256)),
     # fixed phi2, 4 paths, 9 views
     ("fixed_phi2_9views", dict(kind="slanted", w=112, h=84, focal=112.0, depth=10.0, tilt=15.0, step=0.3,
                                views=9), dict(d_min=6.0, d_max=18.0, levels=2, cost="census5",
