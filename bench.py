@@ -502,7 +502,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--ring", type=int, default=16, help="distinct bundles cycled through")
-    ap.add_argument("--inflight", type=int, default=3, help="bundles in flight (contexts/streams)")
+    ap.add_argument("--inflight", type=int, default=5, help="bundles in flight (contexts/streams; also the e2e host threads)")
     ap.add_argument("--cpu-baseline-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
