@@ -177,7 +177,7 @@ def alg_bytes(stage, stats, n_views, paths):
         elif stage.startswith("sweep"):
             if (stage == "sweep_l0") != (lv is stats[0]):
                 continue
-            tot += e * 2 + px * (8 + n_views)
+            tot += e * (2 + 4) + px * (8 + n_views)  # u16 cost + zeroed u32 aggregate
     return tot
 
 
@@ -213,8 +213,9 @@ def roofline_entry(stage, st, peak, peak_src):
     except (OSError, KeyError, ValueError):
         pass
     if stage.startswith("sweep"):
-        e["note"] = ("achieved = algorithmic bytes (2 B cost per hypothesis + 8 B meta + 1 B per "
-                     "view per pixel) / CUDA-event launch time; the sweep is ALU-issue-bound "
+        e["note"] = ("achieved = algorithmic bytes (2 B cost + 4 B zeroed aggregate per hypothesis "
+                     "+ 8 B meta + 1 B per view per pixel) / CUDA-event launch time; the sweep is "
+                     "ALU-issue-bound "
                      "(FP32 certified census + FP64 tie fallback), not HBM-bound: see "
                      "DESIGN.md section 5")
     else:
