@@ -363,6 +363,31 @@ int fmvs_roc_curve(fmvs_ctx* ctx, const float* est, const float* gt, const float
                    int32_t width, int32_t height, double theta, double* densities,
                    double* error_rates);
 
+/* ------------------------------------- remaining reference helpers -- */
+/* gaussian_blur (pipeline.hpp:54, pipeline.cpp:32-75): float raster, radius
+ * <= 7. */
+int fmvs_gaussian_blur(fmvs_ctx* ctx, const uint8_t* image, int32_t width, int32_t height,
+                       int32_t radius, double sigma, float* out);
+/* census_transform (matching.hpp:58, matching.cpp:44-55): u64 per pixel;
+ * ConfigError for even windows or > 64 bits. */
+int fmvs_census_transform(fmvs_ctx* ctx, const uint8_t* image, int32_t width, int32_t height,
+                          int32_t window_w, int32_t window_h, uint64_t* out);
+/* census_bits_at (matching.hpp:60, matching.cpp:28-42), host. */
+uint64_t fmvs_census_bits_at(const uint8_t* image, int32_t width, int32_t height, int32_t x,
+                             int32_t y, int32_t window_w, int32_t window_h);
+/* ncc_cost (matching.hpp:64, matching.cpp:57-77), host: the standalone NCC
+ * of two equal-size patches (the sweep uses its own two-pass form). */
+int fmvs_ncc_cost(const float* patch_ref, const float* patch_other, int32_t n, int32_t* cost);
+/* apply_homography (geometry.hpp:102, geometry.cpp:116-119), host. */
+void fmvs_apply_homography(const double h[9], double x, double y, double out[2]);
+/* cross_ratio (geometry.hpp:120-123, geometry.cpp:157-181), host: dims 2 or
+ * 3, points packed p1..p4. InvalidInputError on coincident points. */
+int fmvs_cross_ratio(const double* points, int32_t dims, double* out);
+/* require_centers_in_front (geometry.hpp:115-116, geometry.cpp:147-153),
+ * host: GeometryError when a camera centre lies behind the near plane. */
+int fmvs_require_centers_in_front(const double normal[3], double delta_min,
+                                  const double* centers_xyz, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

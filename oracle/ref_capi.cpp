@@ -9,6 +9,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <exception>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -296,7 +297,7 @@ int ref_build_pyramids(void*, const fmvs_view* views, int32_t n_views, int32_t l
     });
 }
 
-int ref_gaussian_blur(const uint8_t* image, int32_t w, int32_t h, int32_t radius, double sigma,
+int ref_gaussian_blur(void*, const uint8_t* image, int32_t w, int32_t h, int32_t radius, double sigma,
                       float* out) {
     return guard([&] {
         const Raster<float> r = gaussian_blur(to_image(image, w, h), radius, sigma);
@@ -653,5 +654,57 @@ int ref_roc_curve(void*, const float* est, const float* gt, const float* conf, i
     });
 }
 #endif
+
+// --- remaining reference helpers (matching.hpp / geometry.hpp) -----------
+
+int ref_census_transform(void*, const uint8_t* image, int32_t w, int32_t h, int32_t ww, int32_t wh,
+                         uint64_t* out) {
+    return guard([&] {
+        const Raster<std::uint64_t> r = census_transform(to_image(image, w, h), ww, wh);
+        std::memcpy(out, r.data(), sizeof(uint64_t) * r.size());
+    });
+}
+
+uint64_t ref_census_bits_at(const uint8_t* image, int32_t w, int32_t h, int32_t x, int32_t y, int32_t ww,
+                            int32_t wh) {
+    return census_bits_at(to_image(image, w, h), x, y, ww, wh);
+}
+
+int ref_ncc_cost(const float* a, const float* b, int32_t n, int32_t* cost) {
+    return guard([&] {
+        *cost = ncc_cost(std::span<const float>(a, static_cast<std::size_t>(std::max(n, 0))),
+                         std::span<const float>(b, static_cast<std::size_t>(std::max(n, 0))));
+    });
+}
+
+void ref_apply_homography(const double h[9], double x, double y, double out[2]) {
+    Eigen::Matrix3d m;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            m(r, c) = h[3 * r + c];
+    const Eigen::Vector2d q = apply_homography(m, Eigen::Vector2d(x, y));
+    out[0] = q.x();
+    out[1] = q.y();
+}
+
+int ref_cross_ratio(const double* p, int32_t dims, double* out) {
+    return guard([&] {
+        if (dims == 2)
+            *out = cross_ratio(Eigen::Vector2d(p[0], p[1]), Eigen::Vector2d(p[2], p[3]),
+                               Eigen::Vector2d(p[4], p[5]), Eigen::Vector2d(p[6], p[7]));
+        else
+            *out = cross_ratio(Eigen::Vector3d(p[0], p[1], p[2]), Eigen::Vector3d(p[3], p[4], p[5]),
+                               Eigen::Vector3d(p[6], p[7], p[8]), Eigen::Vector3d(p[9], p[10], p[11]));
+    });
+}
+
+int ref_require_centers_in_front(const double normal[3], double delta_min, const double* c, int32_t n) {
+    return guard([&] {
+        std::vector<Eigen::Vector3d> cs;
+        for (int i = 0; i < n; ++i)
+            cs.emplace_back(c[3 * i], c[3 * i + 1], c[3 * i + 2]);
+        require_centers_in_front(Eigen::Vector3d(normal[0], normal[1], normal[2]), delta_min, cs);
+    });
+}
 
 }  // extern "C"

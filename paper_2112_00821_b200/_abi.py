@@ -139,12 +139,18 @@ SIGNATURES = {
     "write_pfm": (C.c_int, [C.c_char_p, P, I32, I32, I32]),
     "evaluate": (C.c_int, [P, P, P, I32, I32, PD, I32, C.POINTER(L1Result_c), C.POINTER(AccCplF_c)]),
     "roc_curve": (C.c_int, [P, P, P, P, I32, I32, D, PD, PD]),
+    "gaussian_blur": (C.c_int, [P, P, I32, I32, I32, D, P]),
+    "census_transform": (C.c_int, [P, P, I32, I32, I32, I32, P]),
+    "census_bits_at": (U64, [P, I32, I32, I32, I32, I32, I32]),
+    "ncc_cost": (C.c_int, [P, P, I32, C.POINTER(I32)]),
+    "apply_homography": (None, [PD, D, D, PD]),
+    "cross_ratio": (C.c_int, [PD, I32, PD]),
+    "require_centers_in_front": (C.c_int, [PD, D, PD, I32]),
 }
 
 # Entry points only the oracle library has.
 ORACLE_EXTRAS = {
     "worker_count": (C.c_int, []),
-    "gaussian_blur": (C.c_int, [P, I32, I32, I32, D, P]),
 }
 
 

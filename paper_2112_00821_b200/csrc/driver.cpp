@@ -1832,3 +1832,133 @@ int fmvs_roc_curve(fmvs_ctx* ctx, const float* est, const float* gt, const float
 }
 
 }  // extern "C"
+
+// --------------------------------------- remaining reference helpers --
+extern "C" {
+
+int fmvs_gaussian_blur(fmvs_ctx* ctx, const uint8_t* image, int32_t w, int32_t h, int32_t radius,
+                       double sigma, float* out) {
+    return guarded([&] {
+        ctx->use();
+        if (radius < 0 || radius > 7)
+            fmvs::fail_config("gaussian_blur: radius must be in 0..7");
+        const size_t px = static_cast<size_t>(std::max(w, 0)) * std::max(h, 0);
+        if (!px)
+            return;
+        const std::vector<double> kw = fmvs::blur_kernel(radius, sigma);
+        k::BlurKernel bk{};
+        bk.radius = radius;
+        for (size_t i = 0; i < kw.size(); ++i)
+            bk.w[i] = kw[i];
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const uint8_t* d_img = t.upload(image, px, s);
+        float* tmp = t.alloc<float>(px);
+        float* d_out = t.alloc<float>(px);
+        k::gaussian_blur(d_img, w, h, bk, tmp, d_out, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out, d_out, px * 4, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int fmvs_census_transform(fmvs_ctx* ctx, const uint8_t* image, int32_t w, int32_t h, int32_t ww,
+                          int32_t wh, uint64_t* out) {
+    return guarded([&] {
+        ctx->use();
+        if (ww < 1 || wh < 1 || ww % 2 == 0 || wh % 2 == 0)  // matching.cpp:45-48
+            fmvs::fail_config("census transform: window dimensions must be odd");
+        if (ww * wh - 1 > 64)
+            fmvs::fail_config("census transform: bit string exceeds 64 bits");
+        const size_t px = static_cast<size_t>(std::max(w, 0)) * std::max(h, 0);
+        if (!px)
+            return;
+        cudaStream_t s = ctx->stream;
+        Tmp t;
+        const uint8_t* d_img = t.upload(image, px, s);
+        uint64_t* d_out = t.alloc<uint64_t>(px);
+        k::census_transform(d_img, w, h, ww, wh, d_out, s);
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(out, d_out, px * 8, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+uint64_t fmvs_census_bits_at(const uint8_t* image, int32_t w, int32_t h, int32_t x, int32_t y,
+                             int32_t ww, int32_t wh) {
+    const int rx = ww / 2, ry = wh / 2;  // matching.cpp:28-42
+    const uint8_t c = image[static_cast<size_t>(y) * w + x];
+    uint64_t bits = 0;
+    for (int dy = -ry; dy <= ry; ++dy)
+        for (int dx = -rx; dx <= rx; ++dx) {
+            if (dx == 0 && dy == 0)
+                continue;
+            const int xx = std::min(std::max(x + dx, 0), w - 1), yy = std::min(std::max(y + dy, 0), h - 1);
+            bits = (bits << 1) | (image[static_cast<size_t>(yy) * w + xx] < c ? 1u : 0u);
+        }
+    return bits;
+}
+
+int fmvs_ncc_cost(const float* a_in, const float* b_in, int32_t n, int32_t* cost) {
+    return guarded([&] {
+        if (n <= 0)  // matching.cpp:57-59
+            fmvs::fail_input("ncc: patches must be non-empty and equal size");
+        const double nn = static_cast<double>(n);
+        double sa = 0, sb = 0, saa = 0, sbb = 0, sab = 0;
+        for (int i = 0; i < n; ++i) {
+            const double a = a_in[i], b = b_in[i];
+            sa += a;
+            sb += b;
+            saa += a * a;
+            sbb += b * b;
+            sab += a * b;
+        }
+        const double var_a = saa - sa * sa / nn;
+        const double var_b = sbb - sb * sb / nn;
+        if (var_a <= 0.0 || var_b <= 0.0) {
+            *cost = 255;
+            return;
+        }
+        const double ncc = (sab - sa * sb / nn) / std::sqrt(var_a * var_b);
+        const double c = 255.0 * std::min(1.0 - ncc, 1.0);
+        *cost = static_cast<int32_t>(std::lround(std::clamp(c, 0.0, 255.0)));
+    });
+}
+
+void fmvs_apply_homography(const double h[9], double x, double y, double out[2]) {
+    // q = h * (x, y, 1), rows reduced left to right (the shim's order)
+    const double qx = (h[0] * x + h[1] * y) + h[2] * 1.0;
+    const double qy = (h[3] * x + h[4] * y) + h[5] * 1.0;
+    const double qz = (h[6] * x + h[7] * y) + h[8] * 1.0;
+    out[0] = qx / qz;
+    out[1] = qy / qz;
+}
+
+int fmvs_cross_ratio(const double* p, int32_t dims, double* out) {
+    return guarded([&] {
+        if (dims != 2 && dims != 3)
+            fmvs::fail_input("cross ratio: points must be 2D or 3D");
+        auto dist = [&](int a, int b) {  // (p_b - p_a).norm()
+            double acc = 0.0;
+            for (int k2 = 0; k2 < dims; ++k2) {
+                const double d = p[b * dims + k2] - p[a * dims + k2];
+                acc = k2 == 0 ? d * d : acc + d * d;
+            }
+            return std::sqrt(acc);
+        };
+        const double d14 = dist(0, 3), d23 = dist(1, 2);  // geometry.cpp:159-165
+        if (d14 == 0.0 || d23 == 0.0)
+            fmvs::fail_input("cross ratio: coincident points p1=p4 or p2=p3");
+        *out = dist(0, 2) * dist(1, 3) / (d14 * d23);
+    });
+}
+
+int fmvs_require_centers_in_front(const double normal[3], double delta_min, const double* c, int32_t n) {
+    return guarded([&] {
+        for (int i = 0; i < n; ++i) {  // geometry.cpp:147-153
+            const double d = (normal[0] * c[3 * i] + normal[1] * c[3 * i + 1]) + normal[2] * c[3 * i + 2];
+            if (!(d + delta_min > 0.0))
+                fmvs::fail_geometry("sweep geometry: camera center behind the near bounding plane");
+        }
+    });
+}
+
+}  // extern "C"

@@ -68,6 +68,41 @@ __global__ void blur_cols_dog_kernel(const float* __restrict__ tmp, const uint8_
     mask[p] = fabsf(__fsub_rn(float(img[p]), smooth)) > 0.5f ? 1 : 0;
 }
 
+__global__ void blur_cols_kernel(const float* __restrict__ tmp, int w, int h, BlurKernel k,
+                                 float* __restrict__ out) {
+    using namespace dev;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    double acc = 0.0;
+    for (int i = -k.radius; i <= k.radius; ++i)
+        acc = add(acc, mul(k.w[i + k.radius],
+                           double(__ldg(tmp + static_cast<size_t>(reflect_i(y + i, h)) * w + x))));
+    out[static_cast<size_t>(y) * w + x] = __double2float_rn(acc);
+}
+
+// census_transform / census_bits_at (matching.cpp:28-55): neighbour < centre,
+// row-major, MSB first, centre skipped, edge-clamped.
+__global__ void census_kernel(const uint8_t* __restrict__ img, int w, int h, int ww, int wh,
+                              uint64_t* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    const int rx = ww / 2, ry = wh / 2;
+    const uint8_t c = img[static_cast<size_t>(y) * w + x];
+    uint64_t bits = 0;
+    for (int dy = -ry; dy <= ry; ++dy)
+        for (int dx = -rx; dx <= rx; ++dx) {
+            if (dx == 0 && dy == 0)
+                continue;
+            const int xx = min(max(x + dx, 0), w - 1), yy = min(max(y + dy, 0), h - 1);
+            bits = (bits << 1) | (__ldg(img + static_cast<size_t>(yy) * w + xx) < c ? 1u : 0u);
+        }
+    out[static_cast<size_t>(y) * w + x] = bits;
+}
+
 __device__ __forceinline__ int uf_find(const int* labels, int p) {
     for (;;) {
         const int q = __ldcg(labels + p);
@@ -286,6 +321,18 @@ void gaussian_blur_dog(const uint8_t* img, int w, int h, const BlurKernel& k, fl
                        uint8_t* mask, cudaStream_t s) {
     blur_rows_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(img, w, h, k, tmp);
     blur_cols_dog_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(tmp, img, w, h, k, mask);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void gaussian_blur(const uint8_t* img, int w, int h, const BlurKernel& k, float* tmp, float* out,
+                   cudaStream_t s) {
+    blur_rows_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(img, w, h, k, tmp);
+    blur_cols_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(tmp, w, h, k, out);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void census_transform(const uint8_t* img, int w, int h, int ww, int wh, uint64_t* out, cudaStream_t s) {
+    census_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(img, w, h, ww, wh, out);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

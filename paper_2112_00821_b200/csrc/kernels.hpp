@@ -157,6 +157,11 @@ struct BlurKernel {
 // (postfilter.cpp:68-74); tmp: w*h floats
 void gaussian_blur_dog(const uint8_t* img, int w, int h, const BlurKernel& k, float* tmp,
                        uint8_t* mask, cudaStream_t s);
+// gaussian_blur (pipeline.cpp:32-75) -> float raster; tmp: w*h floats
+void gaussian_blur(const uint8_t* img, int w, int h, const BlurKernel& k, float* tmp, float* out,
+                   cudaStream_t s);
+// census_transform (matching.cpp:44-55)
+void census_transform(const uint8_t* img, int w, int h, int ww, int wh, uint64_t* out, cudaStream_t s);
 // remove_speckles (postfilter.cpp:14-51): labels, sizes: w*h ints each
 void remove_speckles(uint8_t* mask, int w, int h, uint8_t value, int min_size, int* labels,
                      int* sizes, cudaStream_t s);

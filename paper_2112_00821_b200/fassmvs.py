@@ -673,6 +673,58 @@ class Backend:
         ch = 1 if a.ndim == 2 else a.shape[2]
         self._check(self.fn["write_pfm"](path.encode(), _ptr(a), a.shape[1], a.shape[0], ch))
 
+    # -------------------------------------- remaining reference helpers
+    def gaussian_blur(self, image: np.ndarray, radius: int, sigma: float) -> np.ndarray:
+        """gaussian_blur (pipeline.hpp:54): float32 (h, w)."""
+        img = np.ascontiguousarray(image, np.uint8)
+        h, w = img.shape
+        out = np.zeros((h, w), np.float32)
+        self._check(self.fn["gaussian_blur"](self.ctx, _ptr(img), w, h, radius, float(sigma), _ptr(out)))
+        return out
+
+    def census_transform(self, image: np.ndarray, window_w: int, window_h: int) -> np.ndarray:
+        """census_transform (matching.hpp:58): uint64 (h, w)."""
+        img = np.ascontiguousarray(image, np.uint8)
+        h, w = img.shape
+        out = np.zeros((h, w), np.uint64)
+        self._check(self.fn["census_transform"](self.ctx, _ptr(img), w, h, window_w, window_h, _ptr(out)))
+        return out
+
+    def census_bits_at(self, image: np.ndarray, x: int, y: int, window_w: int, window_h: int) -> int:
+        """census_bits_at (matching.hpp:60)."""
+        img = np.ascontiguousarray(image, np.uint8)
+        h, w = img.shape
+        return int(self.fn["census_bits_at"](_ptr(img), w, h, x, y, window_w, window_h))
+
+    def ncc_cost(self, patch_ref, patch_other) -> int:
+        """ncc_cost (matching.hpp:64)."""
+        a, b = _f32(patch_ref).ravel(), _f32(patch_other).ravel()
+        if a.size != b.size:
+            raise InvalidInputError("ncc: patches must be non-empty and equal size")
+        out = C.c_int32(0)
+        self._check(self.fn["ncc_cost"](_ptr(a), _ptr(b), a.size, C.byref(out)))
+        return out.value
+
+    def apply_homography(self, hom, x: float, y: float):
+        """apply_homography (geometry.hpp:102)."""
+        h = np.ascontiguousarray(hom, np.float64).ravel()
+        out = np.zeros(2, np.float64)
+        self.fn["apply_homography"](_pd(h), float(x), float(y), _pd(out))
+        return out
+
+    def cross_ratio(self, p1, p2, p3, p4) -> float:
+        """cross_ratio (geometry.hpp:120-123), 2D or 3D points."""
+        pts = np.ascontiguousarray([p1, p2, p3, p4], np.float64)
+        out = C.c_double(0.0)
+        self._check(self.fn["cross_ratio"](_pd(pts), pts.shape[1], C.byref(out)))
+        return out.value
+
+    def require_centers_in_front(self, normal, delta_min: float, centers) -> None:
+        """require_centers_in_front (geometry.hpp:115-116): GeometryError if violated."""
+        n = np.ascontiguousarray(normal, np.float64)
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        self._check(self.fn["require_centers_in_front"](_pd(n), float(delta_min), _pd(c), len(c)))
+
     # ------------------------------------------ accuracy scoring (§8f)
     def evaluate(self, est: np.ndarray, gt: np.ndarray, thetas=(1.25, 1.1, 1.05, 1.01)):
         """evaluate (evaluation.hpp:48-49): ({l1_abs, l1_rel, valid_both},
