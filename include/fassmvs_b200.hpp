@@ -14,6 +14,9 @@
 // B200 library -- the drop-in used by INTEGRATION.md (the reference's CPU
 // definition is compiled under another name with
 // -Destimate_bundle=estimate_bundle_cpu on pipeline.cpp only).
+// FASSMVS_B200_DEFINE_POSTFILTER does the same for dog_mask and
+// geometric_consistency_mask (postfilter.cpp compiled with the two names
+// renamed).
 #pragma once
 
 #include <cstring>
@@ -205,6 +208,19 @@ namespace fassmvs {
 // The drop-in: the reference's entry point, served by the B200 library.
 BundleResult estimate_bundle(const std::vector<CalibratedView>& bundle, const PipelineConfig& config) {
     return fassmvs_b200::estimate_bundle(bundle, config);
+}
+}  // namespace fassmvs
+#endif
+
+#ifdef FASSMVS_B200_DEFINE_POSTFILTER
+namespace fassmvs {
+// The post-filter entry points (postfilter.hpp:18,44-45) served by the B200
+// library (postfilter.cpp compiled with -Ddog_mask=dog_mask_cpu
+// -Dgeometric_consistency_mask=geometric_consistency_mask_cpu).
+TextureMask dog_mask(const ImageU8& image) { return fassmvs_b200::dog_mask(image); }
+TextureMask geometric_consistency_mask(const std::vector<ConsistencyView>& window, int ref_index,
+                                       const GeomFilterConfig& config) {
+    return fassmvs_b200::geometric_consistency_mask(window, ref_index, config);
 }
 }  // namespace fassmvs
 #endif

@@ -1,5 +1,6 @@
 """Drop-in proof: the reference's OWN unit suite and acceptance program,
-linked so that fassmvs::estimate_bundle is served by the B200 library through
+linked so that fassmvs::estimate_bundle, dog_mask and
+geometric_consistency_mask are served by the B200 library through
 include/fassmvs_b200.hpp (oracle/Makefile target `dropin`), pass on the GPU,
 and the acceptance run prints exactly the golden numbers of
 proj/test_output.txt:13-22 (the B200 path is bit-exact with the reference)."""
