@@ -421,3 +421,30 @@ def test_estimate_bundle_errors_match(b200, oracle):
     for be in (b200, oracle):
         with pytest.raises(GeometryError):
             be.estimate_bundle(flat, config(8.0, 14.0))
+
+
+@pytest.mark.parametrize("case", ["cropped_views", "tiny_3lvl", "odd_sizes"])
+def test_estimate_bundle_shapes(b200, oracle, case):
+    """Matching views of different sizes than the reference (cropped
+    right/bottom, intrinsics kept), tiny images whose coarsest level is a few
+    pixels, and odd sizes (ceil-halving pyramid)."""
+    import dataclasses
+    if case == "cropped_views":
+        bundle, _, _ = render(oracle, "slanted", 120, 90, tilt=25.0, step=0.5, texture=0.3)
+        for k in (0, 1, 3, 4):
+            v = bundle[k]
+            cw, ch = 120 - 7 * (k + 1), 90 - 3 * k
+            v.image = np.ascontiguousarray(v.image[:ch, :cw])
+            v.intrinsics = dataclasses.replace(v.intrinsics, width=cw, height=ch)
+        c = config(4.0, 40.0, levels=2, cost="census5", variant=SgmVariant.SurfaceNormal, max_planes=64)
+    elif case == "tiny_3lvl":
+        bundle, _, _ = render(oracle, "fronto", 13, 9, focal=13.0, step=0.3, texture=0.5)
+        c = config(6.0, 16.0, levels=3, cost="ncc5", max_planes=32)
+    else:
+        bundle, _, _ = render(oracle, "slanted", 101, 77, tilt=20.0, step=0.45, texture=0.3)
+        c = config(4.0, 30.0, levels=3, cost="census97", variant=SgmVariant.PathGradient, max_planes=48)
+    a = b200.estimate_bundle(bundle, c)
+    b = oracle.estimate_bundle(bundle, c)
+    assert_same(a.depth, b.depth, "depth")
+    assert_same(a.normals, b.normals, "normals")
+    assert_same(a.confidence, b.confidence, "confidence")
