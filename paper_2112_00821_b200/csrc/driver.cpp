@@ -402,27 +402,44 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
     const double* d_swt = d_blob + off_swt;
     const uint16_t* d_clut = reinterpret_cast<const uint16_t*>(d_blob + off_clut);
 
-    // ---- K1: pyramid + quads ------------------------------------------------
+    // ---- K1: pyramid + quads (one launch per pyramid level, one per quad
+    // batch: blockIdx.z selects the view) ------------------------------------
     for (int l = 1; l < L; ++l)
-        for (int k2 = 0; k2 < n; ++k2) {
-            const fmvs_intrinsics& a = lv[l - 1].intr[k2];
-            const fmvs_intrinsics& b = lv[l].intr[k2];
-            ctx->timed("pyramid", [&] {
-                k::blur_halve(img_ptr[(l - 1) * n + k2], a.width, a.height,
-                              const_cast<uint8_t*>(img_ptr[l * n + k2]), b.width, b.height, k3, s);
-            });
+        for (int k0 = 0; k0 < n; k0 += k::kImgBatch) {
+            k::ImgBatch b{};
+            const int m = std::min(n - k0, k::kImgBatch);
+            for (int i = 0; i < m; ++i) {
+                const fmvs_intrinsics& a = lv[l - 1].intr[k0 + i];
+                const fmvs_intrinsics& c = lv[l].intr[k0 + i];
+                b.job[i] = k::ImgJob{img_ptr[(l - 1) * n + k0 + i], const_cast<uint8_t*>(img_ptr[l * n + k0 + i]),
+                                     nullptr, a.width, a.height, c.width, c.height};
+            }
+            ctx->timed("pyramid", [&] { k::blur_halve_batch(b, m, k3, s); });
             ++launches;
         }
-    for (int l = 0; l < L; ++l) {
-        size_t q = lv[l].quad_off;
-        for (int k2 = 0; k2 < n; ++k2) {
-            const fmvs_intrinsics& a = lv[l].intr[k2];
-            if (k2 != ref) {
-                ctx->timed("quads", [&] { k::pack_quads(img_ptr[l * n + k2], a.width, a.height, d_quad + q, s); });
-                ++launches;
+    {
+        k::ImgBatch b{};
+        int m = 0;
+        auto flush = [&] {
+            if (m == 0)
+                return;
+            ctx->timed("quads", [&] { k::pack_quads_batch(b, m, s); });
+            ++launches;
+            m = 0;
+        };
+        for (int l = 0; l < L; ++l) {
+            size_t q = lv[l].quad_off;
+            for (int k2 = 0; k2 < n; ++k2) {
+                const fmvs_intrinsics& a = lv[l].intr[k2];
+                if (k2 != ref) {
+                    b.job[m++] = k::ImgJob{img_ptr[l * n + k2], nullptr, d_quad + q, a.width, a.height, 0, 0};
+                    if (m == k::kImgBatch)
+                        flush();
+                }
+                q += static_cast<size_t>(a.width) * a.height;
             }
-            q += static_cast<size_t>(a.width) * a.height;
         }
+        flush();
     }
 
     // ---- per-level buffers ---------------------------------------------------

@@ -73,7 +73,74 @@ __global__ void pack_quads_kernel(const uint8_t* __restrict__ img, int w, int h,
                                            (uint32_t(__ldg(r1 + x1)) << 24);
 }
 
+// Batched forms: blockIdx.z selects the image (one launch for all views of a
+// pyramid level / all quad images of a bundle instead of one per image).
+__global__ void blur_halve_batch_kernel(ImgBatch b, double k0, double k1, double k2) {
+    const ImgJob& j = b.job[blockIdx.z];
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= j.wout || y >= j.hout)
+        return;
+    using namespace dev;
+    const double c_k3[3] = {k0, k1, k2};
+    const int X = 2 * x, Y = 2 * y;
+    const int xm = reflect(X - 1, j.win), xp = reflect(X + 1, j.win);
+    float tmp[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int yy = reflect(Y + r - 1, j.hin);
+        const uint8_t* row = j.in + static_cast<size_t>(yy) * j.win;
+        double acc = 0.0;
+        acc = add(acc, mul(c_k3[0], double(__ldg(row + xm))));
+        acc = add(acc, mul(c_k3[1], double(__ldg(row + X))));
+        acc = add(acc, mul(c_k3[2], double(__ldg(row + xp))));
+        tmp[r] = __double2float_rn(acc);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+        acc = add(acc, mul(c_k3[r], double(tmp[r])));
+    long v = lroundf(__double2float_rn(acc));
+    v = v < 0 ? 0 : (v > 255 ? 255 : v);
+    j.out[static_cast<size_t>(y) * j.wout + x] = static_cast<uint8_t>(v);
+}
+
+__global__ void pack_quads_batch_kernel(ImgBatch b) {
+    const ImgJob& j = b.job[blockIdx.z];
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= j.win || y >= j.hin)
+        return;
+    const int w = j.win, h = j.hin;
+    const int x1 = min(x + 1, w - 1), y1 = min(y + 1, h - 1);
+    const uint8_t* r0 = j.in + static_cast<size_t>(y) * w;
+    const uint8_t* r1 = j.in + static_cast<size_t>(y1) * w;
+    j.quad[static_cast<size_t>(y) * w + x] = uint32_t(__ldg(r0 + x)) | (uint32_t(__ldg(r0 + x1)) << 8) |
+                                             (uint32_t(__ldg(r1 + x)) << 16) |
+                                             (uint32_t(__ldg(r1 + x1)) << 24);
+}
+
 }  // namespace
+
+void blur_halve_batch(const ImgBatch& b, int n, const double k3[3], cudaStream_t s) {
+    int mw = 1, mh = 1;
+    for (int i = 0; i < n; ++i) {
+        mw = max(mw, b.job[i].wout);
+        mh = max(mh, b.job[i].hout);
+    }
+    blur_halve_batch_kernel<<<dim3((mw + 31) / 32, (mh + 7) / 8, n), dim3(32, 8), 0, s>>>(b, k3[0], k3[1], k3[2]);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
+void pack_quads_batch(const ImgBatch& b, int n, cudaStream_t s) {
+    int mw = 1, mh = 1;
+    for (int i = 0; i < n; ++i) {
+        mw = max(mw, b.job[i].win);
+        mh = max(mh, b.job[i].hin);
+    }
+    pack_quads_batch_kernel<<<dim3((mw + 31) / 32, (mh + 7) / 8, n), dim3(32, 8), 0, s>>>(b);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
 
 void blur_halve(const uint8_t* in, int win, int hin, uint8_t* out, int wout, int hout,
                 const double k3[3], cudaStream_t s) {

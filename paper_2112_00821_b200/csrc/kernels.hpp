@@ -19,6 +19,21 @@ void blur_halve(const uint8_t* in, int win, int hin, uint8_t* out, int wout, int
 // the four bilinear taps of raster.hpp:71-84 in one 32-bit load.
 void pack_quads(const uint8_t* img, int w, int h, uint32_t* quad, cudaStream_t s);
 
+// Batched launches (blockIdx.z = image): pyramid halving of up to kImgBatch
+// images (in -> out) and quad packing (in -> quad, in sizes win x hin).
+constexpr int kImgBatch = 32;
+struct ImgJob {
+    const uint8_t* in;
+    uint8_t* out;
+    uint32_t* quad;
+    int win, hin, wout, hout;
+};
+struct ImgBatch {
+    ImgJob job[kImgBatch];
+};
+void blur_halve_batch(const ImgBatch& b, int n, const double k3[3], cudaStream_t s);
+void pack_quads_batch(const ImgBatch& b, int n, cudaStream_t s);
+
 // ---- K3: per-pixel sampling range + plane interval + row prefix sums -----
 struct RangeArgs {
     dev::Intr intr;
