@@ -15,6 +15,7 @@
 // first (same sequential walk) so the window need not be stored.
 // Roofline: FP64-issue-bound (~50 DP ops per bilinear sample); HBM traffic is
 // 2 B per hypothesis written plus the (L2-resident) images.
+#include <algorithm>
 #include <type_traits>
 
 
@@ -167,11 +168,16 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
     __shared__ float s_patch[kSeg][NSP];
     __shared__ uint64_t s_base;
 
-    const int y = blockIdx.y;
-    const int x0 = blockIdx.x * kSeg;
-    const int npx = min(kSeg, a.w - x0);
     const int t = threadIdx.x;
     const uint8_t* ref = a.ref_img;
+    // grid-stride over 32-pixel row segments: when every pixel is narrow (the
+    // tiled kernel owns them) a fixed-size grid only scans the metadata
+    const int segs_per_row = (a.w + kSeg - 1) / kSeg;
+    const int nseg = segs_per_row * a.h;
+    for (int seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+    const int y = seg / segs_per_row;
+    const int x0 = (seg - y * segs_per_row) * kSeg;
+    const int npx = min(kSeg, a.w - x0);
 
     if (t < 32) {
         int cnt = 0;
@@ -267,6 +273,8 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
         a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
         if (a.agg_zero)
             a.agg_zero[o] = 0u;
+    }
+    __syncthreads();  // the segment's shared state is rewritten next iteration
     }
 }
 
@@ -1336,7 +1344,8 @@ int sweep(const SweepArgs& a_in, cudaStream_t s) {
     // the exact per-hypothesis kernel. Uniform levels set narrow_max to the
     // stack size (every pixel shares the range).
     a.exact_above = tiled ? (a.narrow_max > 0 ? a.narrow_max : kNarrowMax) : 0;
-    const dim3 grid((a.w + kSeg - 1) / kSeg, a.h);
+    const int nseg = ((a.w + kSeg - 1) / kSeg) * a.h;
+    const dim3 grid(std::max(1, std::min(nseg, 148 * 16)));
     if (a.kind == FMVS_COST_CENSUS && a.ww == 5)
         sweep_kernel<FMVS_COST_CENSUS, 5, 5><<<grid, kThreads, 0, s>>>(a);
     else if (a.kind == FMVS_COST_CENSUS)
