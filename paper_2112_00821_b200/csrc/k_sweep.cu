@@ -296,9 +296,16 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
 // ===================================================================
 
 constexpr int kTW = 32, kTH = 8, kTiledThreads = kTW * kTH;
-// resident CTAs per SM the census kernel is compiled for (register budget)
+// resident CTAs per SM the census / NCC kernels are compiled for (register
+// budget). Measured on B200 (C2): 3 CTAs (80 regs, few spills) 155 maps/s,
+// 4 (64 regs) 164, 5 (48 regs, heavy but L1-resident spills) 165.6, 6 worse:
+// latency hiding across the per-plane barriers beats spill traffic. NCC
+// (c2ncc): 2 CTAs 111.4, 3 118.7, 4 117.5.
 #ifndef FMVS_CENSUS_MINB5
-#define FMVS_CENSUS_MINB5 3
+#define FMVS_CENSUS_MINB5 5
+#endif
+#ifndef FMVS_NCC_MINB
+#define FMVS_NCC_MINB 3
 #endif
 #define FMVS_CENSUS_MINB(n) ((n) > 25 ? 2 : FMVS_CENSUS_MINB5)
 constexpr int kNarrowMax = 192;
@@ -981,7 +988,7 @@ __device__ __forceinline__ int ncc_tail(double sb, double sbb, double sab, doubl
 }
 
 template <int WW, int WH, int NM>
-__global__ void __launch_bounds__(kTiledThreads, 2) sweep_ncc_tiled(SweepArgs a) {
+__global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(SweepArgs a) {
     using namespace dev;
     constexpr int RX = WW / 2, RY = WH / 2, NS = WW * WH;
     constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
