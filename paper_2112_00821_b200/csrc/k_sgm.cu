@@ -15,6 +15,8 @@
 // reference's determinism contract, README.md:87-88).
 // Roofline: HBM/L2-bound -- per hypothesis and path: 2 B cost read + 4 B
 // atomic add; per pixel and path: 8 B meta + 1 B image.
+#include <type_traits>
+
 #include "host.hpp"
 #include "kernels.hpp"
 
@@ -523,16 +525,22 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
                 const int toff = f + shift - prev_first;
                 const uint16_t* cp = a.costs + cur_px.base;
                 uint32_t* ap = a.agg + cur_px.base;
-                for (int i0 = 0; i0 < c; i0 += PASS) {
+                if (SENT) {
+                    // branch-free: the clamped window reads sentinels (or stale
+                    // slots) for inactive lanes, whose result is discarded; no
+                    // previous pixel adds nothing. The first pass (the only one
+                    // at refined levels) is straight-line code on the
+                    // prefetched costs; further passes load theirs.
+                    auto pass = [&](int i0, auto first) {
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const int i = i0 + gl + G * k;
-                        const bool act = i < c;
-                        if (SENT) {
-                            // branch-free: the clamped window reads sentinels
-                            // (or stale slots) for inactive lanes, whose result
-                            // is discarded; no previous pixel adds nothing
-                            const uint32_t sc = i0 == 0 ? cur_px.s[k] : (act ? cp[i] : 0u);
+                        for (int k = 0; k < K; ++k) {
+                            const int i = i0 + gl + G * k;
+                            const bool act = i < c;
+                            uint32_t sc;
+                            if constexpr (decltype(first)::value)
+                                sc = cur_px.s[k];
+                            else
+                                sc = act ? cp[i] : 0u;
                             const int t = min(max(toff + i, -2), prev_count + 1);
                             const V b3 = min(static_cast<V>(prev[t - 1]), static_cast<V>(prev[t + 1])) + phi1;
                             const V best = min(min(base_best, static_cast<V>(prev[t])), b3);
@@ -549,7 +557,18 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
                             } else {
                                 run_min = min(run_min, act ? v : 0xFFFFFFFFu);
                             }
-                        } else if (act) {
+                        }
+                    };
+                    pass(0, std::true_type{});
+                    for (int i0 = PASS; i0 < c; i0 += PASS)
+                        pass(i0, std::false_type{});
+                } else {
+                    for (int i0 = 0; i0 < c; i0 += PASS) {
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const int i = i0 + gl + G * k;
+                            if (i >= c)
+                                continue;
                             const uint32_t sc = i0 == 0 ? cur_px.s[k] : cp[i];
                             uint32_t v;
                             if (!has_prev) {
