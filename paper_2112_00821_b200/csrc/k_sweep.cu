@@ -611,6 +611,17 @@ __device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const Vi
     return make_float2(f, fmaf(gx, ddx, fmaf(gy, ddy, 4.0e-5f)));
 }
 
+// Exact FP64 census cost of one view (views whose tile certification is
+// impossible; rare). Out of line so its registers do not weigh on the tiled
+// kernel's hot loop.
+template <int WW, int WH>
+__device__ __noinline__ int census_view_exact(const uint32_t* __restrict__ quad, int vw, int vh,
+                                              const double* __restrict__ hp, double xd, double yd,
+                                              uint64_t ref_bits, const uint16_t* __restrict__ lut) {
+    return view_cost<FMVS_COST_CENSUS, WW, WH>(quad, vw, vh, hp, xd, yd, ref_bits, nullptr, 0.0, 0.0,
+                                               lut);
+}
+
 template <int WW, int WH, int NM>
 __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) sweep_census_tiled(SweepArgs a) {
     using namespace dev;
@@ -912,10 +923,9 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                 if ((view_exact >> m) & 1u) {
                     if (a.stats)
                         atomicAdd(a.stats + 3, 1ull);
-                    cost = view_cost<FMVS_COST_CENSUS, WW, WH>(vc.quad, vc.w, vc.h,
-                                                              vc.homs + static_cast<size_t>(p) * 9,
-                                                              xd, yd, ref_bits, nullptr, 0.0, 0.0,
-                                                              a.census_lut);
+                    cost = census_view_exact<WW, WH>(vc.quad, vc.w, vc.h,
+                                                     vc.homs + static_cast<size_t>(p) * 9, xd, yd,
+                                                     ref_bits, a.census_lut);
                 } else if ((view_out >> m) & 1u) {
                     cost = 255;
                 } else {
