@@ -997,6 +997,21 @@ __device__ __forceinline__ int ncc_tail(double sb, double sbb, double sab, doubl
     return static_cast<int>(lround(cc));
 }
 
+// Exact FP64 NCC cost of one view (tile certification impossible; rare), out
+// of line so its registers do not weigh on the tiled kernel. `ref` points at
+// the pixel's window in the shared reference tile (row stride `sw`).
+template <int WW, int WH>
+__device__ __noinline__ int ncc_view_exact(const uint32_t* __restrict__ quad, int vw, int vh,
+                                           const double* __restrict__ hp, double xd, double yd,
+                                           const float* ref, int sw, double ref_mean, double ref_var,
+                                           const uint16_t* __restrict__ lut) {
+    float patch[WW * WH];
+    for (int i = 0; i < WH; ++i)
+        for (int j = 0; j < WW; ++j)
+            patch[i * WW + j] = ref[i * sw + j];
+    return view_cost<FMVS_COST_NCC, WW, WH>(quad, vw, vh, hp, xd, yd, 0ull, patch, ref_mean, ref_var, lut);
+}
+
 template <int WW, int WH, int NM>
 __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(SweepArgs a) {
     using namespace dev;
@@ -1269,16 +1284,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
                 const double* hp = vc.homs + static_cast<size_t>(p) * 9;
                 int c = cost[m];
                 if ((view_exact >> m) & 1u) {
-                    const float* rp = nullptr;
-                    float patch[NS];
-#pragma unroll
-                    for (int i = 0; i < WH; ++i)
-#pragma unroll
-                        for (int j = 0; j < WW; ++j)
-                            patch[i * WW + j] = s_ref[(ty + i) * SW + tx + j];
-                    rp = patch;
-                    c = view_cost<FMVS_COST_NCC, WW, WH>(vc.quad, vc.w, vc.h, hp, xd, yd, 0ull, rp,
-                                                        ref_mean, ref_var, a.census_lut);
+                    c = ncc_view_exact<WW, WH>(vc.quad, vc.w, vc.h, hp, xd, yd, s_ref + ty * SW + tx, SW,
+                                               ref_mean, ref_var, a.census_lut);
                 } else if ((view_unsure >> m) & 1u) {
                     if (k + NS <= kNccItemCap) {
                         c = s_vcost[k / NS];  // resolved by pass 2b
