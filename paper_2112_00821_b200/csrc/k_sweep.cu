@@ -298,11 +298,12 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
 constexpr int kTW = 32, kTH = 8, kTiledThreads = kTW * kTH;
 // resident CTAs per SM the census / NCC kernels are compiled for (register
 // budget). Measured on B200 (C2): 3 CTAs (80 regs, few spills) 155 maps/s,
-// 4 (64 regs) 164, 5 (48 regs, heavy but L1-resident spills) 165.6, 6 worse:
-// latency hiding across the per-plane barriers beats spill traffic. NCC
-// (c2ncc): 2 CTAs 111.4, 3 118.7, 4 117.5.
+// 4 (64 regs) 164, 5 (48 regs, heavy spills) 165.6, 6 worse: latency hiding
+// across the per-plane barriers beats spill traffic; with the exact-view
+// path out of line, 4 and 5 tie (169-170) and 4 spills less. NCC (c2ncc):
+// 2 CTAs 111.4, 3 118.7, 4 117.5.
 #ifndef FMVS_CENSUS_MINB5
-#define FMVS_CENSUS_MINB5 5
+#define FMVS_CENSUS_MINB5 4
 #endif
 #ifndef FMVS_NCC_MINB
 #define FMVS_NCC_MINB 3
