@@ -200,6 +200,80 @@ __device__ __forceinline__ float conf_of(float nx, float ny, float nz, double co
 }
 
 // smooth_normals (surface.cpp:41-81) + confidence_map of the smoothed normal.
+// Shared-memory tiled form (radius <= 4): the 32x8 block stages its
+// (32+2r)x(8+2r) window of raw normals, validity and intensities once instead
+// of every thread re-loading its 5x5 neighbourhood from L1. Same arithmetic,
+// same order as smooth_conf_kernel below.
+constexpr int kSmMaxR = 4;
+__global__ void smooth_conf_tiled_kernel(const float* __restrict__ raw, const uint8_t* __restrict__ img,
+                                         int w, int h, int radius, const double* __restrict__ wt,
+                                         float* __restrict__ out, float* __restrict__ conf,
+                                         double cos_rho, double pdv, double sx, double sy, double sz) {
+    using namespace dev;
+    constexpr int TW = 32 + 2 * kSmMaxR, TH = 8 + 2 * kSmMaxR;
+    __shared__ float s_n[3][TH][TW];
+    __shared__ int s_i[TH][TW];  // intensity, or -1 where the normal is invalid / outside
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 8;
+    const int tw = 32 + 2 * radius, th = 8 + 2 * radius;
+    for (int k = threadIdx.y * 32 + threadIdx.x; k < tw * th; k += 256) {
+        const int ty = k / tw, tx = k - ty * tw;
+        const int gx = bx + tx - radius, gy = by + ty - radius;
+        float nx = 0.0f, ny = 0.0f, nz = 0.0f;
+        int iv = -1;
+        if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
+            const size_t q = static_cast<size_t>(gy) * w + gx;
+            nx = raw[3 * q];
+            ny = raw[3 * q + 1];
+            nz = raw[3 * q + 2];
+            if (normal_ok(nx, ny, nz))
+                iv = img[q];
+        }
+        s_n[0][ty][tx] = nx;
+        s_n[1][ty][tx] = ny;
+        s_n[2][ty][tx] = nz;
+        s_i[ty][tx] = iv;
+    }
+    __syncthreads();
+    const int x = bx + threadIdx.x, y = by + threadIdx.y;
+    if (x >= w || y >= h)
+        return;
+    const size_t p = static_cast<size_t>(y) * w + x;
+    const int cx0 = threadIdx.x + radius, cy0 = threadIdx.y + radius;
+    const float cx = s_n[0][cy0][cx0], cy = s_n[1][cy0][cx0], cz = s_n[2][cy0][cx0];
+    float ox = 0.0f, oy = 0.0f, oz = 0.0f;
+    if (s_i[cy0][cx0] >= 0) {
+        double sx_ = double(cx), sy_ = double(cy), sz_ = double(cz);
+        const int ic = s_i[cy0][cx0];
+        for (int dy = -radius; dy <= radius; ++dy)
+            for (int dx = -radius; dx <= radius; ++dx) {
+                if (dx == 0 && dy == 0)
+                    continue;
+                const int iq = s_i[cy0 + dy][cx0 + dx];
+                if (iq < 0)
+                    continue;  // outside the image or invalid normal (surface.cpp:63-67)
+                const double wq = __ldg(wt + (dx * dx + dy * dy) * 256 + abs(iq - ic));
+                sx_ = add(sx_, mul(wq, double(s_n[0][cy0 + dy][cx0 + dx])));
+                sy_ = add(sy_, mul(wq, double(s_n[1][cy0 + dy][cx0 + dx])));
+                sz_ = add(sz_, mul(wq, double(s_n[2][cy0 + dy][cx0 + dx])));
+            }
+        const double len = norm3(D3{sx_, sy_, sz_});
+        if (len > 1e-15) {
+            ox = __double2float_rn(div(sx_, len));
+            oy = __double2float_rn(div(sy_, len));
+            oz = __double2float_rn(div(sz_, len));
+        } else {
+            ox = cx;
+            oy = cy;
+            oz = cz;
+        }
+    }
+    out[3 * p] = ox;
+    out[3 * p + 1] = oy;
+    out[3 * p + 2] = oz;
+    if (conf)
+        conf[p] = conf_of(ox, oy, oz, cos_rho, pdv, sx, sy, sz);
+}
+
 __global__ void smooth_conf_kernel(const float* __restrict__ raw, const uint8_t* __restrict__ img,
                                    int w, int h, int radius, const double* __restrict__ wt,
                                    float* __restrict__ out, float* __restrict__ conf,
@@ -296,9 +370,14 @@ void normals_raw(const float* depth, int w, int h, dev::Intr intr, float* out_xy
 void smooth_conf(const float* raw_xyz, const uint8_t* img, int w, int h, int radius,
                  const double* weights, float* out_xyz, float* conf, double cos_rho,
                  double plane_dot_view, double nx, double ny, double nz, cudaStream_t s) {
-    smooth_conf_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(raw_xyz, img, w, h, radius, weights,
-                                                            out_xyz, conf, cos_rho,
-                                                            plane_dot_view, nx, ny, nz);
+    if (radius <= kSmMaxR)
+        smooth_conf_tiled_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(raw_xyz, img, w, h, radius, weights,
+                                                                      out_xyz, conf, cos_rho,
+                                                                      plane_dot_view, nx, ny, nz);
+    else
+        smooth_conf_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(raw_xyz, img, w, h, radius, weights,
+                                                                out_xyz, conf, cos_rho,
+                                                                plane_dot_view, nx, ny, nz);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 
