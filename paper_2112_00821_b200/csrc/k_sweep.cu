@@ -318,8 +318,36 @@ struct TileParams {
     float az, bz, cz;  // q.z(du, dv)
     float dx, dy;      // certified coordinate error bounds (pixels)
     int xa, ya;        // integer anchors
-    int exact;         // certification impossible: exact FP64 for this view
+    int exact;         // kTileExact: certification impossible, exact FP64 for this view;
+                       // kTileInterior: the whole tile + halo warps strictly inside the view
 };
+
+constexpr int kTileExact = 1, kTileInterior = 2;
+
+// kTileInterior test of a certified tile: a linear-fractional map with a
+// positive denominator over a rectangle attains its coordinate extrema at the
+// corners (its level sets are lines), so if the four corners land strictly
+// inside [0, vw-1) x [0, vh-1) with the certified margins, no sample of the
+// tile is clamped (pipeline bilinear, raster.hpp:71-84) and every window
+// centre passes the reference's inside test (matching.cpp:224-231).
+__device__ __forceinline__ bool tile_interior(const double* H, double U, double V, double DU, double DV,
+                                              double dx, double dy, int vw, int vh) {
+    double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const double uu = U + ((c & 1) ? DU : 0.0), vv = V + ((c & 2) ? DV : 0.0);
+        const double qz = H[6] * uu + H[7] * vv + H[8];
+        const double X = (H[0] * uu + H[1] * vv + H[2]) / qz;
+        const double Y = (H[3] * uu + H[4] * vv + H[5]) / qz;
+        xmin = fmin(xmin, X);
+        xmax = fmax(xmax, X);
+        ymin = fmin(ymin, Y);
+        ymax = fmax(ymax, Y);
+    }
+    const double mx = dx + 1e-6, my = dy + 1e-6;  // + FP64 corner rounding (<< 1e-6)
+    return xmin - mx > 0.0 && ymin - my > 0.0 && xmax + mx < double(vw - 1) &&
+           ymax + my < double(vh - 1);
+}
 
 // FP64 sample of window position (i, j) of pixel (x, y), exactly as the
 // reference computes it (matching.cpp:222-248).
@@ -365,7 +393,7 @@ __device__ __noinline__ bool exact_inside(const double* __restrict__ hp, int vw,
 
 // Per-(tile, plane, view) residual coefficients and error bounds (FP64).
 __device__ TileParams make_tile_params(const double* __restrict__ hp, int u0, int v0, int du_max,
-                                       int dv_max) {
+                                       int dv_max, int vw, int vh) {
     TileParams tp{};
     double H[9];
     for (int k = 0; k < 9; ++k)
@@ -430,7 +458,7 @@ __device__ TileParams make_tile_params(const double* __restrict__ hp, int u0, in
     tp.dy = __double2float_ru(dy);
     tp.xa = static_cast<int>(xa);
     tp.ya = static_cast<int>(ya);
-    tp.exact = 0;
+    tp.exact = tile_interior(H, U, V, DU, DV, double(tp.dx), double(tp.dy), vw, vh) ? kTileInterior : 0;
     return tp;
 }
 
@@ -623,6 +651,24 @@ __device__ __noinline__ int census_view_exact(const uint32_t* __restrict__ quad,
                                                lut);
 }
 
+// Interval [lo, hi] of every FP64 walk value of one tile sample (outward
+// rounded): FP32 bilinear of the cell quad q at (ax, ay) widened by the cell's
+// Lipschitz constant times the certified coordinate error (255 when the
+// sample is within the error of a cell edge).
+__device__ __forceinline__ float2 census_sample(uint32_t q, float ax, float ay, float dx, float dy) {
+    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
+    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
+    const float top = fmaf(ax, i10 - i00, i00);
+    const float bot = fmaf(ax, i11 - i01, i01);
+    const float f = fmaf(ay, bot - top, top);
+    const bool near_x = ax < dx || ax > 1.0f - dx;
+    const bool near_y = ay < dy || ay > 1.0f - dy;
+    const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
+    const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
+    const float e = fmaf(gx, dx, fmaf(gy, dy, 2.0e-4f));
+    return make_float2(__fsub_rd(f, e), __fadd_ru(f, e));
+}
+
 template <int WW, int WH, int NM>
 __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) sweep_census_tiled(SweepArgs a) {
     using namespace dev;
@@ -702,7 +748,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                 const int pp = p + k / NM, m = k % NM;
                 if (pp <= pmax)
                     s_tp[k / NM][m] = make_tile_params(s_vc[m].homs + static_cast<size_t>(pp) * 9,
-                                                       x0 - RX, y0 - RY, SW - 1, SH - 1);
+                                                       x0 - RX, y0 - RY, SW - 1, SH - 1, s_vc[m].w,
+                                                       s_vc[m].h);
             }
             __syncthreads();
         }
@@ -722,9 +769,29 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
             const TileParams tp = s_tp[slot][m];
             float2* t = s_tile + m * SN;
             uint8_t* fl = s_inflag + m * (kTW * kTH);
-            if (tp.exact) {
+            if (tp.exact == kTileExact) {
                 for (int r = threadIdx.x - m * kTPV; r < SN; r += kTPV)
                     t[r] = make_float2(0.0f, 1e30f);
+            } else if (tp.exact == kTileInterior) {
+                // no clamping, no inside flags (tile_interior)
+                const uint32_t* quad = s_vc[m].quad;
+                const int vw = s_vc[m].w;
+                int r = threadIdx.x - m * kTPV;
+                int dv = r / SW, du = r - dv * SW;
+                for (; r < SN; r += kTPV) {
+                    float tcx, tcy;
+                    tile_coords_fast(tp, float(du), float(dv), &tcx, &tcy);
+                    const float fx = floorf(tcx), fy = floorf(tcy);
+                    const int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
+                    const float ax = tcx - fx, ay = tcy - fy;
+                    t[r] = census_sample(__ldg(quad + (Y0 * vw + X0)), ax, ay, tp.dx, tp.dy);
+                    du += kTPV % SW;
+                    dv += kTPV / SW;
+                    if (du >= SW) {
+                        du -= SW;
+                        ++dv;
+                    }
+                }
             } else {
                 const uint32_t* quad = s_vc[m].quad;
                 const int vw = s_vc[m].w, vh = s_vc[m].h;
@@ -752,20 +819,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                     else if (X0 >= vw - 1) { X0 = vw - 1; ax = 0.0f; }
                     if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
                     else if (Y0 >= vh - 1) { Y0 = vh - 1; ay = 0.0f; }
-                    const uint32_t q = __ldg(quad + (Y0 * vw + X0));
-                    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
-                    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
-                    const float top = fmaf(ax, i10 - i00, i00);
-                    const float bot = fmaf(ax, i11 - i01, i01);
-                    const float f = fmaf(ay, bot - top, top);
-                    const bool near_x = ax < tp.dx || ax > 1.0f - tp.dx;
-                    const bool near_y = ay < tp.dy || ay > 1.0f - tp.dy;
-                    const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
-                    const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
-                    // interval [lo, hi] of every FP64 walk value of this sample
-                    // (outward rounded)
-                    const float e = fmaf(gx, tp.dx, fmaf(gy, tp.dy, 2.0e-4f));
-                    t[r] = make_float2(__fsub_rd(f, e), __fadd_ru(f, e));
+                    t[r] = census_sample(__ldg(quad + (Y0 * vw + X0)), ax, ay, tp.dx, tp.dy);
                     du += kTPV % SW;
                     dv += kTPV / SW;
                     if (du >= SW) {
@@ -787,17 +841,20 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
             uns[m] = 0;
             if (!need)
                 continue;
-            const TileParams& tp = s_tp[slot][m];
-            if (tp.exact) {
+            const int tpe = s_tp[slot][m].exact;
+            if (tpe == kTileExact) {
                 view_exact |= 1u << m;
                 continue;
             }
             const ViewConst& vc = s_vc[m];
             // inside test of the window centre (matching.cpp:224-231), certified
             // in the tile build; undecided -> the reference's exact FP64 test
-            const uint8_t fl = s_inflag[m * (kTW * kTH) + threadIdx.x];
-            const bool inside = fl == 2 ? exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd)
-                                        : fl == 1;
+            bool inside = true;
+            if (tpe != kTileInterior) {
+                const uint8_t fl = s_inflag[m * (kTW * kTH) + threadIdx.x];
+                inside = fl == 2 ? exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd)
+                                 : fl == 1;
+            }
             if (!inside) {
                 view_out |= 1u << m;
                 continue;
