@@ -524,7 +524,7 @@ struct TileParams64 {
 };
 
 __device__ TileParams64 make_tile_params64(const double* __restrict__ hp, int u0, int v0,
-                                           int du_max, int dv_max) {
+                                           int du_max, int dv_max, int vw, int vh) {
     TileParams64 tp{};
     double H[9];
     for (int k = 0; k < 9; ++k)
@@ -584,7 +584,7 @@ __device__ TileParams64 make_tile_params64(const double* __restrict__ hp, int u0
     tp.dy = __double2float_ru(dy);
     tp.xa = static_cast<int>(xa);
     tp.ya = static_cast<int>(ya);
-    tp.exact = 0;
+    tp.exact = tile_interior(H, U, V, DU, DV, double(tp.dx), double(tp.dy), vw, vh) ? kTileInterior : 0;
     return tp;
 }
 
@@ -596,6 +596,26 @@ __device__ __forceinline__ void tile_coords64(const TileParams64& tp, double du,
     const double r = __drcp_rn(rz);
     *tx = rx * r;
     *ty = ry * r;
+}
+
+// (value, bound) of one FP64-coordinate tile sample: FP32 bilinear of the
+// cell quad q at (ax, ay); the bound is the cell's Lipschitz constant times
+// the coordinate error (255 within the error of a cell edge) plus the FP32
+// bilinear rounding.
+__device__ __forceinline__ float2 ncc_sample(uint32_t q, float ax, float ay, float dx, float dy) {
+    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
+    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
+    const float top = fmaf(ax, i10 - i00, i00);
+    const float bot = fmaf(ax, i11 - i01, i01);
+    const float f = fmaf(ay, bot - top, top);
+    // the float cast of (t - floor t) adds 2^-24 to the coordinate error
+    const float ddx = dx + 6.0e-8f, ddy = dy + 6.0e-8f;
+    const bool near_x = ax < ddx || ax > 1.0f - ddx;
+    const bool near_y = ay < ddy || ay > 1.0f - ddy;
+    const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
+    const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
+    // FP32 bilinear: 3 FMA + 2 SUB roundings on values <= 255 (< 4e-5)
+    return make_float2(f, fmaf(gx, ddx, fmaf(gy, ddy, 4.0e-5f)));
 }
 
 // Sample of the tile at (du, dv): FP64 residual coordinates, FP32 bilinear;
@@ -624,20 +644,18 @@ __device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const Vi
     else if (X0 >= vc.w - 1) { X0 = vc.w - 1; ax = 0.0f; }
     if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
     else if (Y0 >= vc.h - 1) { Y0 = vc.h - 1; ay = 0.0f; }
-    const uint32_t q = __ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0);
-    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
-    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
-    const float top = fmaf(ax, i10 - i00, i00);
-    const float bot = fmaf(ax, i11 - i01, i01);
-    const float f = fmaf(ay, bot - top, top);
-    // the float cast of (t - floor t) adds 2^-24 to the coordinate error
-    const float ddx = tp.dx + 6.0e-8f, ddy = tp.dy + 6.0e-8f;
-    const bool near_x = ax < ddx || ax > 1.0f - ddx;
-    const bool near_y = ay < ddy || ay > 1.0f - ddy;
-    const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
-    const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
-    // FP32 bilinear: 3 FMA + 2 SUB roundings on values <= 255 (< 4e-5)
-    return make_float2(f, fmaf(gx, ddx, fmaf(gy, ddy, 4.0e-5f)));
+    return ncc_sample(__ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0), ax, ay, tp.dx, tp.dy);
+}
+
+// tile_sample64 of a kTileInterior tile: no clamping, no inside flag.
+__device__ __forceinline__ float2 tile_sample64_interior(const TileParams64& tp, const ViewConst& vc,
+                                                         double du, double dv) {
+    double tx, ty;
+    tile_coords64(tp, du, dv, &tx, &ty);
+    const double fx = floor(tx), fy = floor(ty);
+    const int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
+    const float ax = __double2float_rn(tx - fx), ay = __double2float_rn(ty - fy);
+    return ncc_sample(__ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0), ax, ay, tp.dx, tp.dy);
 }
 
 // Exact FP64 census cost of one view (views whose tile certification is
@@ -1167,7 +1185,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
                 const int pp = p + k / NM, m = k % NM;
                 if (pp <= pmax)
                     s_tp[k / NM][m] = make_tile_params64(s_vc[m].homs + static_cast<size_t>(pp) * 9,
-                                                         x0 - RX, y0 - RY, SW - 1, SH - 1);
+                                                         x0 - RX, y0 - RY, SW - 1, SH - 1, s_vc[m].w,
+                                                         s_vc[m].h);
             }
             __syncthreads();
         }
@@ -1186,15 +1205,28 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
             uint8_t* fl = s_in + m * SN;
             int r = threadIdx.x - m * kTPV;
             int dv = r / SW, du = r - dv * SW;
-            for (; r < SN; r += kTPV) {
-                uint8_t f = 2;
-                t[r] = tp.exact ? make_float2(0.0f, 1e30f) : tile_sample64(tp, vc, double(du), double(dv), &f);
-                fl[r] = f;
-                du += kTPV % SW;
-                dv += kTPV / SW;
-                if (du >= SW) {
-                    du -= SW;
-                    ++dv;
+            if (tp.exact == kTileInterior) {
+                for (; r < SN; r += kTPV) {
+                    t[r] = tile_sample64_interior(tp, vc, double(du), double(dv));
+                    du += kTPV % SW;
+                    dv += kTPV / SW;
+                    if (du >= SW) {
+                        du -= SW;
+                        ++dv;
+                    }
+                }
+            } else {
+                for (; r < SN; r += kTPV) {
+                    uint8_t f = 2;
+                    t[r] = tp.exact ? make_float2(0.0f, 1e30f)
+                                    : tile_sample64(tp, vc, double(du), double(dv), &f);
+                    fl[r] = f;
+                    du += kTPV % SW;
+                    dv += kTPV / SW;
+                    if (du >= SW) {
+                        du -= SW;
+                        ++dv;
+                    }
                 }
             }
         }
@@ -1208,16 +1240,18 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
             cost[m] = 255;
             if (!need)
                 continue;
-            const TileParams64& tp = s_tp[slot][m];
-            if (tp.exact) {
+            const int tpe = s_tp[slot][m].exact;
+            if (tpe == kTileExact) {
                 view_exact |= 1u << m;
                 continue;
             }
             const ViewConst& vc = s_vc[m];
-            const uint8_t fl = s_in[m * SN + (ty + RY) * SW + tx + RX];
-            const bool inside =
-                fl == 2 ? exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd)
-                        : fl == 1;
+            bool inside = true;
+            if (tpe != kTileInterior) {
+                const uint8_t fl = s_in[m * SN + (ty + RY) * SW + tx + RX];
+                inside = fl == 2 ? exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd)
+                                 : fl == 1;
+            }
             if (!inside || ref_var <= 0.0)
                 continue;  // 255 (matching.cpp:224-232, 262-263)
             const float2* t = s_tile + m * SN;
