@@ -391,6 +391,28 @@ __device__ __noinline__ bool exact_inside(const double* __restrict__ hp, int vw,
     return cxw >= 0.0 && cyw >= 0.0 && cxw <= double(vw) - 1.0 && cyw <= double(vh) - 1.0;
 }
 
+// Byte k of q as a float, exactly (2^23 + b built by a byte permute, minus
+// 2^23): two full-rate ALU/FMA instructions instead of a conversion.
+template <int K>
+__device__ __forceinline__ float byte_f(uint32_t q) {
+    return __uint_as_float(__byte_perm(q, 0x4B000000u, 0x7540 | K)) - 8388608.0f;
+}
+
+// floor(t) for |t| < 2^22 without conversions: t + 1.5*2^23 rounded down has
+// an ulp of 1, so its low mantissa bits are floor(t) (offset 0x4B400000).
+__device__ __forceinline__ float floor_small(float t, int* it) {
+    const float s = __fadd_rd(t, 12582912.0f);
+    *it = __float_as_int(s) - 0x4B400000;
+    return s - 12582912.0f;  // exact
+}
+
+// Same for doubles, |t| < 2^31: t + 1.5*2^52 rounded down, low word = floor(t).
+__device__ __forceinline__ double floor_small(double t, int* it) {
+    const double s = __dadd_rd(t, 6755399441055744.0);
+    *it = __double2loint(s);
+    return s - 6755399441055744.0;  // exact
+}
+
 // Per-(tile, plane, view) residual coefficients and error bounds (FP64).
 __device__ TileParams make_tile_params(const double* __restrict__ hp, int u0, int v0, int du_max,
                                        int dv_max, int vw, int vh) {
@@ -603,8 +625,7 @@ __device__ __forceinline__ void tile_coords64(const TileParams64& tp, double du,
 // the coordinate error (255 within the error of a cell edge) plus the FP32
 // bilinear rounding.
 __device__ __forceinline__ float2 ncc_sample(uint32_t q, float ax, float ay, float dx, float dy) {
-    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
-    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
+    const float i00 = byte_f<0>(q), i10 = byte_f<1>(q), i01 = byte_f<2>(q), i11 = byte_f<3>(q);
     const float top = fmaf(ax, i10 - i00, i00);
     const float bot = fmaf(ax, i11 - i01, i01);
     const float f = fmaf(ay, bot - top, top);
@@ -652,8 +673,9 @@ __device__ __forceinline__ float2 tile_sample64_interior(const TileParams64& tp,
                                                          double du, double dv) {
     double tx, ty;
     tile_coords64(tp, du, dv, &tx, &ty);
-    const double fx = floor(tx), fy = floor(ty);
-    const int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
+    int ix, iy;  // |tx|, |ty| < view size (interior tile)
+    const double fx = floor_small(tx, &ix), fy = floor_small(ty, &iy);
+    const int X0 = tp.xa + ix, Y0 = tp.ya + iy;
     const float ax = __double2float_rn(tx - fx), ay = __double2float_rn(ty - fy);
     return ncc_sample(__ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0), ax, ay, tp.dx, tp.dy);
 }
@@ -674,8 +696,7 @@ __device__ __noinline__ int census_view_exact(const uint32_t* __restrict__ quad,
 // Lipschitz constant times the certified coordinate error (255 when the
 // sample is within the error of a cell edge).
 __device__ __forceinline__ float2 census_sample(uint32_t q, float ax, float ay, float dx, float dy) {
-    const float i00 = float(q & 0xFFu), i10 = float((q >> 8) & 0xFFu);
-    const float i01 = float((q >> 16) & 0xFFu), i11 = float(q >> 24);
+    const float i00 = byte_f<0>(q), i10 = byte_f<1>(q), i01 = byte_f<2>(q), i11 = byte_f<3>(q);
     const float top = fmaf(ax, i10 - i00, i00);
     const float bot = fmaf(ax, i11 - i01, i01);
     const float f = fmaf(ay, bot - top, top);
@@ -799,8 +820,9 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                 for (; r < SN; r += kTPV) {
                     float tcx, tcy;
                     tile_coords_fast(tp, float(du), float(dv), &tcx, &tcy);
-                    const float fx = floorf(tcx), fy = floorf(tcy);
-                    const int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
+                    int ix, iy;  // |tcx|, |tcy| < view size (interior tile)
+                    const float fx = floor_small(tcx, &ix), fy = floor_small(tcy, &iy);
+                    const int X0 = tp.xa + ix, Y0 = tp.ya + iy;
                     const float ax = tcx - fx, ay = tcy - fy;
                     t[r] = census_sample(__ldg(quad + (Y0 * vw + X0)), ax, ay, tp.dx, tp.dy);
                     du += kTPV % SW;
