@@ -1064,14 +1064,22 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
 }
 
 // ===================================================================
-// Tiled certified NCC sweep. Same tile warp as the census kernel; per
-// (pixel, plane, view) the window sums are taken in FP32 on centred samples,
-// and the sample bounds E are propagated rigorously to an interval of the
-// reference's FP64 cov = sab - mean*sb and var_b = sbb - sb^2/n (including
-// its own FP64 rounding), hence to an interval of 255*min(1 - ncc, 1). When
-// both ends round to the same integer the cost is certified; otherwise the
-// whole window is recomputed with the reference's exact FP64 walk (NS work
-// items, one sample per thread) and the reference's exact sum order.
+// Tiled certified NCC sweep. Same tile warp as the census kernel (FP64 tile
+// coordinates). Each tile sample is quantised exactly to F = rint(f * 2^16)
+// (|F / 2^16 - f_ref| <= E + 2^-17, E the certified sample bound), so the
+// window sums sum F, sum F^2 and sum r*F are EXACT integers and can be formed
+// as separable box sums: one thread per (view, tile column, half column)
+// slides a WW x WH window down 4 pixel rows (WH + 3 row sums instead of 4 x WH).
+// From the exact quantised var_q and cov_q the reference's FP64 values are
+// bracketed rigorously: the centred sample vector moves by at most
+// ||e|| <= sqrt(n) * e_max, so sqrt(var) moves by at most ||e|| (centring is
+// an orthogonal projection) and cov by at most sqrt(ref_var) * ||e||
+// (Cauchy-Schwarz); the reference's own FP64 rounding (< 1e-7 absolute) is
+// covered by requiring var_q >= 1 and the relative slack of the FP32 bound
+// arithmetic. When both ends of 255*min(1 - ncc, 1) round to the same
+// integer the cost is certified; otherwise the whole window is recomputed
+// with the reference's exact FP64 walk (NS work items, one sample per thread)
+// and the reference's exact sum order.
 // ===================================================================
 
 constexpr int kNccItemCap = 2048;
@@ -1101,13 +1109,58 @@ __device__ __forceinline__ int ncc_tail(double sb, double sbb, double sab, doubl
 template <int WW, int WH>
 __device__ __noinline__ int ncc_view_exact(const uint32_t* __restrict__ quad, int vw, int vh,
                                            const double* __restrict__ hp, double xd, double yd,
-                                           const float* ref, int sw, double ref_mean, double ref_var,
+                                           const int* ref, int sw, double ref_mean, double ref_var,
                                            const uint16_t* __restrict__ lut) {
     float patch[WW * WH];
     for (int i = 0; i < WH; ++i)
         for (int j = 0; j < WW; ++j)
-            patch[i * WW + j] = ref[i * sw + j];
+            patch[i * WW + j] = float(ref[i * sw + j]);
     return view_cost<FMVS_COST_NCC, WW, WH>(quad, vw, vh, hp, xd, yd, 0ull, patch, ref_mean, ref_var, lut);
+}
+
+// Exact integer window sums of the quantised samples (see the header above).
+struct NccSums {
+    uint32_t f;   // sum F            < NS * 2^24
+    uint64_t ff;  // sum F^2          < NS * 2^48
+    uint64_t rf;  // sum r * F        < NS * 2^32
+};
+
+// Certified NCC cost of one window from its exact sums, or -1.
+template <int NS>
+__device__ __forceinline__ int ncc_certify(const NccSums& S, int rsum, float rho, float e_norm) {
+    // n^2 * var_q * 2^32 and n * cov_q * 2^16, exact
+    const long long nv = static_cast<long long>(NS) * static_cast<long long>(S.ff) -
+                         static_cast<long long>(static_cast<unsigned long long>(S.f) * S.f);
+    const long long nc = static_cast<long long>(NS) * static_cast<long long>(S.rf) -
+                         static_cast<long long>(rsum) * static_cast<long long>(S.f);
+    constexpr float inv_nv = 1.0f / (float(NS) * 4294967296.0f);  // relative error < 1e-7
+    constexpr float inv_nc = 1.0f / (float(NS) * 65536.0f);
+    const float var_q = float(nv) * inv_nv;
+    if (!(var_q >= 1.0f))
+        return -1;  // near-flat window: the reference's FP64 rounding is not negligible
+    const float sv = var_q * rsqrtf(var_q);         // sqrt(var_q), rel. error < 4e-7
+    const float s_lo = sv * 0.999999f - e_norm;    // bounds of sqrt(var_b)
+    const float s_hi = sv * 1.000001f + e_norm;
+    if (!(s_lo > 0.5f))
+        return -1;
+    const float c_q = float(nc) * inv_nc;
+    const float dc = rho * e_norm + 1e-6f * fabsf(c_q) + 1e-6f;
+    const float c_lo = c_q - dc, c_hi = c_q + dc;
+    const float r_lo = __frcp_rn(rho * s_lo), r_hi = __frcp_rn(rho * s_hi);  // 1/(rho s)
+    float n_hi = c_hi * (c_hi >= 0.0f ? r_lo : r_hi);
+    float n_lo = c_lo * (c_lo >= 0.0f ? r_hi : r_lo);
+    // FP32 bound arithmetic (conversions, products, MUFU rsqrt; < 1e-6 rel.)
+    // and the reference's FP64 rounding (< 1e-7 abs. with var >= 1)
+    const float slack = 2e-6f * (fabsf(n_hi) + fabsf(n_lo)) + 1e-6f;
+    n_hi += slack;
+    n_lo -= slack;
+    float t_lo = 255.0f * fminf(1.0f - n_hi, 1.0f);
+    float t_hi = 255.0f * fminf(1.0f - n_lo, 1.0f);
+    t_lo = fminf(fmaxf(t_lo, 0.0f), 255.0f) - 1e-4f;
+    t_hi = fminf(fmaxf(t_hi, 0.0f), 255.0f) + 1e-4f;
+    const int k_lo = static_cast<int>(floorf(fmaxf(t_lo, 0.0f) + 0.5f));
+    const int k_hi = static_cast<int>(floorf(fminf(t_hi, 255.0f) + 0.5f));
+    return k_lo == k_hi ? k_lo : -1;
 }
 
 template <int WW, int WH, int NM>
@@ -1115,15 +1168,22 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
     using namespace dev;
     constexpr int RX = WW / 2, RY = WH / 2, NS = WW * WH;
     constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
-    extern __shared__ float2 s_tile[];  // [NM][SH][SW] (value, bound)
-    __shared__ float s_ref[SN];         // edge-clamped reference tile + halo
-    // certified inside flag of each tile sample as a window centre (dynamic,
-    // behind the tile)
-    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_tile + NM * SN);
+    constexpr int kRows = 4;                       // pixel rows per box-sum thread
+    static_assert(kTH == 2 * kRows, "box-sum thread map");
+    extern __shared__ int s_F[];  // [NM][SH][SW] quantised samples F = rint(f * 2^16)
+    // certified cost per (view, pixel) or -1, then the certified inside flag
+    // of each tile sample as a window centre (general tiles only)
+    int16_t* s_cost = reinterpret_cast<int16_t*>(s_F + NM * SN);  // [NM][kTiledThreads]
+    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_cost + NM * kTiledThreads);
+    __shared__ int s_ref[SN];  // edge-clamped reference tile + halo (u8 values)
     __shared__ TileParams64 s_tp[kPlaneChunk][NM];
     __shared__ ViewConst s_vc[NM];
     __shared__ int s_pmin, s_pmax;
     __shared__ int s_count;  // exact samples listed for the current plane
+    __shared__ unsigned s_emax[NM];                  // max sample bound of the tile (float bits)
+    __shared__ int s_rsum[kTiledThreads];            // sum r of each pixel's window
+    __shared__ float s_rho[kTiledThreads];           // sqrt(ref_var), 0 if ref_var <= 0
+    __shared__ int s_first[kTiledThreads], s_cnt[kTiledThreads];
     __shared__ uint32_t s_items[kNccItemCap];
     __shared__ double s_vals[kNccItemCap];
     __shared__ int s_vcost[kNccItemCap / NS + 1];  // pass 2b results
@@ -1139,7 +1199,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
         const int dv = r / SW, du = r - dv * SW;
         const int xx = min(max(x0 - RX + du, 0), a.w - 1);
         const int yy = min(max(y0 - RY + dv, 0), a.h - 1);
-        s_ref[r] = float(a.ref_img[static_cast<size_t>(yy) * a.w + xx]);
+        s_ref[r] = a.ref_img[static_cast<size_t>(yy) * a.w + xx];
     }
     int first = 0, count = 0;
     uint64_t base = 0;
@@ -1151,6 +1211,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
         if (count > a.exact_above)
             count = 0;  // wide pixel: the exact per-hypothesis kernel owns it
     }
+    s_first[threadIdx.x] = first;
+    s_cnt[threadIdx.x] = count;
     if (threadIdx.x == 0) {
         s_pmin = 0x7FFFFFFF;
         s_pmax = -1;
@@ -1161,35 +1223,38 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
         const int2 sz = a.sizes[m];
         s_vc[m] = ViewConst{a.quads[m], a.homs + static_cast<size_t>(m) * a.nplanes * 9, sz.x, sz.y,
                             m < a.nleft ? 1 : 0};
+        s_emax[m] = 0u;
     }
     __syncthreads();
     // reference patch mean and two-pass variance, exactly as matching.cpp:199-210
     double ref_mean = 0.0, ref_var = 0.0;
-    float mean_f = 0.0f, var_rf = 0.0f, sar = 0.0f;
+    int rsum = 0;
     if (count > 0) {
 #pragma unroll
         for (int i = 0; i < WH; ++i)
 #pragma unroll
-            for (int j = 0; j < WW; ++j)
-                ref_mean = add(ref_mean, double(s_ref[(ty + i) * SW + tx + j]));
+            for (int j = 0; j < WW; ++j) {
+                const int r = s_ref[(ty + i) * SW + tx + j];
+                ref_mean = add(ref_mean, double(r));
+                rsum += r;
+            }
         ref_mean = div(ref_mean, double(NS));
-        double sabs = 0.0;
 #pragma unroll
         for (int i = 0; i < WH; ++i)
 #pragma unroll
             for (int j = 0; j < WW; ++j) {
                 const double d = sub(double(s_ref[(ty + i) * SW + tx + j]), ref_mean);
                 ref_var = add(ref_var, mul(d, d));
-                sabs += fabs(d);
             }
-        mean_f = __double2float_rn(ref_mean);
-        var_rf = __double2float_rn(ref_var);
-        sar = __double2float_ru(sabs * 1.0001);
         s_rmean[threadIdx.x] = ref_mean;
         s_rvar[threadIdx.x] = ref_var;
         atomicMin(&s_pmin, first);
         atomicMax(&s_pmax, first + count - 1);
     }
+    s_rsum[threadIdx.x] = rsum;
+    // sqrt(ref_var) rounded down (|rel. error| of the FP32 path < 1e-6 is in
+    // the certification slack)
+    s_rho[threadIdx.x] = ref_var > 0.0 ? __double2float_rd(sqrt_(ref_var)) : 0.0f;
     __syncthreads();
     const int slice = (a.nplanes + gridDim.z - 1) / gridDim.z;
     const int pmin = max(s_pmin, static_cast<int>(blockIdx.z) * slice);
@@ -1201,8 +1266,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
         const int slot = (p - pmin) % kPlaneChunk;
         if (slot == 0) {
             // tile parameters of the next kPlaneChunk planes x NM views (the
-            // previous chunk's were last read in pass 1 of the previous plane,
-            // before its barrier I)
+            // previous chunk's were last read in the box pass of the previous
+            // plane, before its barrier C)
             for (int k = threadIdx.x; k < kPlaneChunk * NM; k += kTiledThreads) {
                 const int pp = p + k / NM, m = k % NM;
                 if (pp <= pmax)
@@ -1212,37 +1277,32 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
             }
             __syncthreads();
         }
-        // Four barriers per plane: tile complete (T), exact-sample list
-        // complete (I), exact samples taken (P), view costs resolved (B); the tile of plane p+1 may be
-        // built while slower warps finish pass 3 of plane p (pass 3 reads
-        // neither the tile nor the inside flags; every warp finished pass 1
-        // before barrier I of plane p).
+        // Five barriers per plane: tile complete (T), box costs complete (C),
+        // exact-sample list complete (I), exact samples taken (P), view costs
+        // resolved (B).
         // ---- tile build: each thread serves one view (parameters in
-        // registers); inside flags only for the interior (window centres)
+        // registers); quantised samples, the tile's max sample bound
         if (threadIdx.x < NM * kTPV) {
             const int m = threadIdx.x / kTPV;
             const TileParams64 tp = s_tp[slot][m];
             const ViewConst vc = s_vc[m];
-            float2* t = s_tile + m * SN;
+            int* t = s_F + m * SN;
             uint8_t* fl = s_in + m * SN;
             int r = threadIdx.x - m * kTPV;
             int dv = r / SW, du = r - dv * SW;
-            if (tp.exact == kTileInterior) {
+            float emax = 0.0f;
+            if (tp.exact != kTileExact) {
                 for (; r < SN; r += kTPV) {
-                    t[r] = tile_sample64_interior(tp, vc, double(du), double(dv));
-                    du += kTPV % SW;
-                    dv += kTPV / SW;
-                    if (du >= SW) {
-                        du -= SW;
-                        ++dv;
+                    float2 v;
+                    if (tp.exact == kTileInterior) {
+                        v = tile_sample64_interior(tp, vc, double(du), double(dv));
+                    } else {
+                        uint8_t f = 2;
+                        v = tile_sample64(tp, vc, double(du), double(dv), &f);
+                        fl[r] = f;
                     }
-                }
-            } else {
-                for (; r < SN; r += kTPV) {
-                    uint8_t f = 2;
-                    t[r] = tp.exact ? make_float2(0.0f, 1e30f)
-                                    : tile_sample64(tp, vc, double(du), double(dv), &f);
-                    fl[r] = f;
+                    t[r] = __float2int_rn(v.x * 65536.0f);  // exact scaling, |F/2^16 - f| <= 2^-17
+                    emax = fmaxf(emax, v.y);
                     du += kTPV % SW;
                     dv += kTPV / SW;
                     if (du >= SW) {
@@ -1251,9 +1311,73 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
                     }
                 }
             }
+            // tile maximum of the bounds (positive floats: their bit patterns
+            // order like them); lanes of one warp may serve different views
+            const unsigned grp = __match_any_sync(__activemask(), m);
+            const unsigned eb = __reduce_max_sync(grp, __float_as_uint(emax));
+            if ((threadIdx.x & 31) == __ffs(grp) - 1)
+                atomicMax(&s_emax[m], eb);
         }
         __syncthreads();  // T
-        // ---- pass 1: certified NCC cost per view, or NS exact work items
+        // ---- box pass: exact window sums by sliding row sums, certified cost
+        // per (view, pixel) into s_cost; job = (view m, tile column bc,
+        // pixel rows bh*4 .. bh*4+3)
+        for (int job = threadIdx.x; job < NM * 2 * kTW; job += kTiledThreads) {
+            const int m = job / (2 * kTW), bc = job % kTW, bh = (job / kTW) & 1;
+            const int tpe = s_tp[slot][m].exact;
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < kRows; ++k) {
+                const int pix = (bh * kRows + k) * kTW + bc;
+                any |= p >= s_first[pix] && p < s_first[pix] + s_cnt[pix];
+            }
+            if (tpe != kTileExact && any) {
+                const int* F = s_F + m * SN;
+                // ||e|| <= sqrt(n) * (E_max + 2^-17), rounded up
+                const float e_norm =
+                    sqrtf(float(NS)) * (__uint_as_float(s_emax[m]) + 7.7e-6f) * 1.0001f;
+                auto row_sum = [&](int row) {
+                    NccSums R{0u, 0ull, 0ull};
+#pragma unroll
+                    for (int j = 0; j < WW; ++j) {
+                        const uint32_t f = static_cast<uint32_t>(F[row * SW + bc + j]);
+                        const uint32_t rv = static_cast<uint32_t>(s_ref[row * SW + bc + j]);
+                        R.f += f;
+                        R.ff += static_cast<uint64_t>(f) * f;
+                        R.rf += static_cast<uint64_t>(rv) * f;
+                    }
+                    return R;
+                };
+                const int row0 = bh * kRows;
+                NccSums S{0u, 0ull, 0ull}, keep[kRows - 1];
+#pragma unroll
+                for (int i = 0; i < WH; ++i) {
+                    const NccSums R = row_sum(row0 + i);
+                    if (i < kRows - 1)
+                        keep[i] = R;
+                    S.f += R.f;
+                    S.ff += R.ff;
+                    S.rf += R.rf;
+                }
+#pragma unroll
+                for (int k = 0; k < kRows; ++k) {
+                    if (k > 0) {
+                        const NccSums R = row_sum(row0 + k - 1 + WH);
+                        S.f += R.f - keep[k - 1].f;
+                        S.ff += R.ff - keep[k - 1].ff;
+                        S.rf += R.rf - keep[k - 1].rf;
+                    }
+                    const int pix = (row0 + k) * kTW + bc;
+                    const float rho = s_rho[pix];
+                    s_cost[m * kTiledThreads + pix] = static_cast<int16_t>(
+                        rho > 0.0f ? ncc_certify<NS>(S, s_rsum[pix], rho, e_norm) : -1);
+                }
+            }
+        }
+        __syncthreads();  // C
+        if (threadIdx.x < NM)
+            s_emax[threadIdx.x] = 0u;  // next written after this plane's barrier B
+        // ---- pass 1: certified costs, or NS exact work items per view
         int cost[NM];
         uint32_t view_unsure = 0, view_exact = 0;
         int my_items = 0;
@@ -1276,66 +1400,16 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
             }
             if (!inside || ref_var <= 0.0)
                 continue;  // 255 (matching.cpp:224-232, 262-263)
-            const float2* t = s_tile + m * SN;
-            const float fc = t[(ty + RY) * SW + tx + RX].x;
-            float su = 0.0f, suu = 0.0f, sru = 0.0f, emax = 0.0f;
-#pragma unroll
-            for (int i = 0; i < WH; ++i)
-#pragma unroll
-                for (int j = 0; j < WW; ++j) {
-                    const float2 n = t[(ty + i) * SW + tx + j];
-                    const float u = n.x - fc;
-                    su += u;
-                    suu = fmaf(u, u, suu);
-                    sru = fmaf(s_ref[(ty + i) * SW + tx + j] - mean_f, u, sru);
-                    emax = fmaxf(emax, n.y);
-                }
-            // rigorous intervals of the reference's cov and var_b (see header)
-            // (approximate MUFU sqrt/rsqrt, rel. error < 1e-6, absorbed by the
-            // 1.001 / 1.01 factors and the 1e-5 ncc slack below)
-            constexpr float nf = float(NS), invn = 1.0f / float(NS);
-            const float sqrt_n = sqrtf(nf);
-            const float g = float(NS + 4) * 1.0e-7f;                // FP32 summation + u rounding
-            const float abs_u = sqrt_up(nf * suu) * 1.001f + 1e-6f;  // >= sum |u_i|
-            const float e_su = g * abs_u;
-            const float e_suu = g * suu;
-            const float su2n = su * su * invn;
-            const float varf = suu - su2n;
-            const float sru_abs = sqrt_up(var_rf * suu) * 1.001f + 1e-6f;
-            const float e_sru = g * sru_abs + 3.2e-5f * abs_u;       // + centred-ref rounding
-            const float sqv = sqrt_up(fmaxf(varf, 0.0f)) * 1.001f;
-            // var(w) - var(f) = 2 sum(f_i - fbar) e_i + sum (e_i - ebar)^2
-            const float dv_ = 1.01f * (2.0f * emax * sqrt_n * sqv + nf * emax * emax + e_suu +
-                                       (2.0f * fabsf(su) * e_su + e_su * e_su) * invn +
-                                       3.0e-7f * (suu + su2n) + 1e-5f);
-            const float dc_ = 1.01f * (emax * sar + e_sru + 1e-5f);
-            const float v_lo = varf - dv_, v_hi = varf + dv_;
-            const float c_lo = sru - dc_, c_hi = sru + dc_;
-            bool certified = false;
-            if (v_lo > 0.0f) {
-                float n_hi = c_hi * rsqrtf(var_rf * (c_hi >= 0.0f ? v_lo : v_hi));
-                float n_lo = c_lo * rsqrtf(var_rf * (c_lo >= 0.0f ? v_hi : v_lo));
-                const float slack = 1e-5f * (fabsf(n_hi) + fabsf(n_lo)) + 1e-6f;
-                n_hi += slack;
-                n_lo -= slack;
-                float t_lo = 255.0f * fminf(1.0f - n_hi, 1.0f);
-                float t_hi = 255.0f * fminf(1.0f - n_lo, 1.0f);
-                t_lo = fminf(fmaxf(t_lo, 0.0f), 255.0f) - 1e-3f;
-                t_hi = fminf(fmaxf(t_hi, 0.0f), 255.0f) + 1e-3f;
-                const int k_lo = static_cast<int>(floorf(fmaxf(t_lo, 0.0f) + 0.5f));
-                const int k_hi = static_cast<int>(floorf(fminf(t_hi, 255.0f) + 0.5f));
-                if (k_lo == k_hi) {
-                    cost[m] = k_lo;
-                    certified = true;
-                }
-            }
-            if (!certified) {
+            const int c = s_cost[m * kTiledThreads + threadIdx.x];
+            if (c >= 0) {
+                cost[m] = c;
+            } else {
                 view_unsure |= 1u << m;
                 my_items += NS;
             }
             if (a.stats) {
                 atomicAdd(a.stats + 0, 1ull);
-                if (!certified)
+                if (c < 0)
                     atomicAdd(a.stats + 1, 1ull);
             }
         }
@@ -1388,7 +1462,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
         }
         __syncthreads();  // B
         if (threadIdx.x == 0)
-            s_count = 0;  // next plane allocates after its barrier T
+            s_count = 0;  // next plane allocates after its barrier C
         // ---- pass 3: costs of undecided views from their exact samples, per-side sums
         if (need) {
             int sum_l = 0, sum_r = 0, k = off;
@@ -1433,7 +1507,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
 
 template <int WW, int WH, int NM>
 void launch_ncc_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
-    const size_t smem = (sizeof(float2) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1);
+    const size_t smem = (sizeof(int) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1) +
+                        sizeof(int16_t) * NM * kTiledThreads;
     FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_ncc_tiled<WW, WH, NM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));

@@ -130,6 +130,35 @@ def test_sweep_certified_census_ties(b200, oracle, rng, texture, cost):
     assert_same(a.costs, b.costs, "costs")
 
 
+@pytest.mark.parametrize("texture", ["scene", "smooth"])
+@pytest.mark.parametrize("cost,w,h", [("census5", 640, 400), ("ncc5", 640, 400), ("ncc9", 320, 200)])
+def test_sweep_certified_large(b200, oracle, rng, texture, cost, w, h):
+    """Larger full-range volumes (millions of hypothesis-views) through the
+    certified tiled sweeps: the rendered scene, and smooth low-gradient
+    texture (blurred noise quantised to u8), whose many near-flat windows
+    sit close to the NCC certification thresholds (var >= 1, rounding
+    boundaries of the cost) and produce many exact census ties."""
+    bundle, stack = _level_inputs(oracle, w=w, h=h)
+    if texture == "smooth":
+        k = np.exp(-0.5 * (np.arange(-6, 7) / 3.0) ** 2)
+        k /= k.sum()
+        for v in bundle:
+            z = rng.normal(128.0, 60.0, v.image.shape)
+            z = np.apply_along_axis(lambda r: np.convolve(r, k, "same"), 1, z)
+            z = np.apply_along_axis(lambda c: np.convolve(c, k, "same"), 0, z)
+            v.image = np.clip(np.round(z), 0, 255).astype(np.uint8)
+    hh, ww = bundle[2].image.shape
+    lo = np.full((hh, ww), 6.0, np.float32)
+    hi = np.full((hh, ww), 16.0, np.float32)
+    spec = {"census5": (CostKind.CensusHamming, 5, 5), "ncc5": (CostKind.NccTruncated, 5, 5),
+            "ncc9": (CostKind.NccTruncated, 9, 9)}[cost]
+    cf = CostFunctionSpec(*spec)
+    a = b200.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    b = oracle.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    assert_same(a.costs, b.costs, "costs")
+    assert len(a.costs) > 2_000_000, len(a.costs)
+
+
 def test_sweep_mixed_wide_and_narrow(b200, oracle, rng):
     """Pixels with > 192 hypotheses (full-range, invalid prior) take the exact
     per-hypothesis kernel, the rest the tiled certified kernel, in one call."""
