@@ -300,13 +300,14 @@ constexpr int kTW = 32, kTH = 8, kTiledThreads = kTW * kTH;
 // budget). Measured on B200 (C2): 3 CTAs (80 regs, few spills) 155 maps/s,
 // 4 (64 regs) 164, 5 (48 regs, heavy spills) 165.6, 6 worse: latency hiding
 // across the per-plane barriers beats spill traffic; with the exact-view
-// path out of line, 4 and 5 tie (169-170) and 4 spills less. NCC (c2ncc):
-// 2 CTAs 111.4, 3 118.7, 4 117.5.
+// path out of line, 4 and 5 tie (169-170) and 4 spills less. NCC box-sum
+// kernel (c2ncc / C3): 2 CTAs 128.9 / 14.1, 3 137.6 / 15.8, 4 142.6 / 16.7
+// (smem allows 4 for 5x5 windows).
 #ifndef FMVS_CENSUS_MINB5
 #define FMVS_CENSUS_MINB5 4
 #endif
 #ifndef FMVS_NCC_MINB
-#define FMVS_NCC_MINB 3
+#define FMVS_NCC_MINB 4
 #endif
 #define FMVS_CENSUS_MINB(n) ((n) > 25 ? 2 : FMVS_CENSUS_MINB5)
 constexpr int kNarrowMax = 192;
