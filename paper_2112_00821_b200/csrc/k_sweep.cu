@@ -1147,10 +1147,12 @@ __device__ __forceinline__ int ncc_certify(const NccSums& S, int rsum, float rho
     const float c_q = float(nc) * inv_nc;
     const float dc = rho * e_norm + 1e-6f * fabsf(c_q) + 1e-6f;
     const float c_lo = c_q - dc, c_hi = c_q + dc;
-    const float r_lo = __frcp_rn(rho * s_lo), r_hi = __frcp_rn(rho * s_hi);  // 1/(rho s)
+    float r_lo, r_hi;  // 1/(rho s): MUFU reciprocal, rel. error < 2^-22 (in the slack)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r_lo) : "f"(rho * s_lo));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r_hi) : "f"(rho * s_hi));
     float n_hi = c_hi * (c_hi >= 0.0f ? r_lo : r_hi);
     float n_lo = c_lo * (c_lo >= 0.0f ? r_hi : r_lo);
-    // FP32 bound arithmetic (conversions, products, MUFU rsqrt; < 1e-6 rel.)
+    // FP32 bound arithmetic (conversions, products, MUFU rsqrt / rcp; < 1e-6 rel.)
     // and the reference's FP64 rounding (< 1e-7 abs. with var >= 1)
     const float slack = 2e-6f * (fabsf(n_hi) + fabsf(n_lo)) + 1e-6f;
     n_hi += slack;
@@ -1261,6 +1263,24 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
     const int pmin = max(s_pmin, static_cast<int>(blockIdx.z) * slice);
     const int pmax = min(s_pmax, static_cast<int>(blockIdx.z + 1) * slice - 1);
     const double xd = double(x), yd = double(y);
+    // plane union of the 4 pixels of each box-sum job this thread serves
+    constexpr int kJobs = (NM * 2 * kTW + kTiledThreads - 1) / kTiledThreads;
+    int job_lo[kJobs], job_hi[kJobs];
+#pragma unroll
+    for (int jj = 0; jj < kJobs; ++jj) {
+        const int job = threadIdx.x + jj * kTiledThreads;
+        const int bc = job % kTW, bh = (job / kTW) & 1;
+        job_lo[jj] = 0x7FFFFFFF;
+        job_hi[jj] = -1;
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+            const int pix = (bh * kRows + k) * kTW + bc;
+            if (s_cnt[pix] > 0) {
+                job_lo[jj] = min(job_lo[jj], s_first[pix]);
+                job_hi[jj] = max(job_hi[jj], s_first[pix] + s_cnt[pix] - 1);
+            }
+        }
+    }
 
     for (int p = pmin; p <= pmax; ++p) {
         const bool need = count > 0 && p >= first && p < first + count;
@@ -1323,16 +1343,16 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
         // ---- box pass: exact window sums by sliding row sums, certified cost
         // per (view, pixel) into s_cost; job = (view m, tile column bc,
         // pixel rows bh*4 .. bh*4+3)
-        for (int job = threadIdx.x; job < NM * 2 * kTW; job += kTiledThreads) {
+#pragma unroll
+        for (int jj = 0; jj < kJobs; ++jj) {
+            const int job = threadIdx.x + jj * kTiledThreads;
+            if (job >= NM * 2 * kTW)
+                break;
             const int m = job / (2 * kTW), bc = job % kTW, bh = (job / kTW) & 1;
             const int tpe = s_tp[slot][m].exact;
-            bool any = false;
-#pragma unroll
-            for (int k = 0; k < kRows; ++k) {
-                const int pix = (bh * kRows + k) * kTW + bc;
-                any |= p >= s_first[pix] && p < s_first[pix] + s_cnt[pix];
-            }
-            if (tpe != kTileExact && any) {
+            // (a pixel of the job needing another plane inside the union
+            // only costs a wasted certification)
+            if (tpe != kTileExact && p >= job_lo[jj] && p <= job_hi[jj]) {
                 const int* F = s_F + m * SN;
                 // ||e|| <= sqrt(n) * (E_max + 2^-17), rounded up
                 const float e_norm =
