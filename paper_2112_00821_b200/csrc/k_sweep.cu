@@ -595,8 +595,10 @@ __device__ TileParams64 make_tile_params64(const double* __restrict__ hp, int u0
         return tp;
     }
     const double Tx = (Rx + ex) / rzmin, Ty = (Ry + ey) / rzmin;
-    double dx = (ex + Tx * ez) / rzmin + two49 * Tx + 1e-12;
-    double dy = (ey + Ty * ez) / rzmin + two49 * Ty + 1e-12;
+    // reciprocal (Newton, < 2^-47) and product rounding of tile_coords64
+    const double two46 = 1.4210854715202004e-14;  // 2^-46
+    double dx = (ex + Tx * ez) / rzmin + two46 * Tx + 1e-12;
+    double dy = (ey + Ty * ez) / rzmin + two46 * Ty + 1e-12;
     dx *= 1.01;
     dy *= 1.01;
     if (!(dx < 1e-3) || !(dy < 1e-3)) {
@@ -616,7 +618,13 @@ __device__ __forceinline__ void tile_coords64(const TileParams64& tp, double du,
     const double rz = fma(tp.az, du, fma(tp.bz, dv, tp.cz));
     const double rx = fma(tp.ax, du, fma(tp.bx, dv, tp.cx));
     const double ry = fma(tp.ay, du, fma(tp.by, dv, tp.cy));
-    const double r = __drcp_rn(rz);
+    // 1/rz: MUFU seed + two Newton steps (relative error < 2^-47 for any
+    // seed error < 2^-12; budgeted in make_tile_params64) instead of the
+    // correctly rounded reciprocal's longer sequence
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(rz));
+    r = fma(r, fma(-rz, r, 1.0), r);
+    r = fma(r, fma(-rz, r, 1.0), r);
     *tx = rx * r;
     *ty = ry * r;
 }
