@@ -733,6 +733,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
     __shared__ int s_count;  // exact samples listed for the current plane
     __shared__ uint32_t s_items[kItemCap];  // (thread, view, window position)
     __shared__ double s_vals[kItemCap];     // their exact FP64 samples
+    __shared__ uint16_t s_lut[WW * WH];     // census cost LUT (popcount -> cost)
 
     const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
@@ -773,6 +774,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
         s_vc[m] = ViewConst{a.quads[m], a.homs + static_cast<size_t>(m) * a.nplanes * 9, sz.x, sz.y,
                             m < a.nleft ? 1 : 0};
     }
+    if (threadIdx.x < WW * WH)
+        s_lut[threadIdx.x] = a.census_lut[threadIdx.x];  // entries 0 .. WW*WH-1 (popcounts)
     __syncthreads();
     if (count > 0) {
         atomicMin(&s_pmin, first);
@@ -957,8 +960,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                     lo = hi = 255;
                 } else {
                     const int hs = popcount_bits((bits[m] ^ ref_bits) & ~uns[m]);
-                    lo = a.census_lut[hs];
-                    hi = a.census_lut[hs + popcount_bits(uns[m])];
+                    lo = s_lut[hs];
+                    hi = s_lut[hs + popcount_bits(uns[m])];
                 }
                 if (s_vc[m].left) {
                     lo_l += lo;
@@ -1057,7 +1060,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                             b = v < wc ? (b | (one << bi)) : (b & ~(one << bi));
                         }
                     }
-                    cost = a.census_lut[popcount_bits(b ^ ref_bits)];
+                    cost = s_lut[popcount_bits(b ^ ref_bits)];
                 }
                 if (vc.left)
                     sum_l += cost;
