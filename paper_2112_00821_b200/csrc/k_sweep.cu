@@ -963,7 +963,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                     lo = s_lut[hs];
                     hi = s_lut[hs + popcount_bits(uns[m])];
                 }
-                if (s_vc[m].left) {
+                if (m < a.nleft) {  // views 0..nleft-1 lie left of the reference
                     lo_l += lo;
                     hi_l += hi;
                 } else {
@@ -975,7 +975,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
             my_items = 0;
 #pragma unroll
             for (int m = 0; m < NM; ++m) {
-                if (!(s_vc[m].left ? rel_l : rel_r))
+                if (!(m < a.nleft ? rel_l : rel_r))
                     uns[m] = 0;
                 if (uns[m])
                     my_items += 1 + popcount_bits(uns[m]);
@@ -1062,7 +1062,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                     }
                     cost = s_lut[popcount_bits(b ^ ref_bits)];
                 }
-                if (vc.left)
+                if (m < a.nleft)
                     sum_l += cost;
                 else
                     sum_r += cost;
@@ -1524,7 +1524,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(
                     }
                     k += NS;
                 }
-                if (vc.left)
+                if (m < a.nleft)
                     sum_l += c;
                 else
                     sum_r += c;
