@@ -310,6 +310,9 @@ constexpr int kTW = 32, kTH = 8, kTiledThreads = kTW * kTH;
 #define FMVS_NCC_MINB 4
 #endif
 #define FMVS_CENSUS_MINB(n) ((n) > 25 ? 2 : FMVS_CENSUS_MINB5)
+// NCC 9x9 or > 4 matching views: shared memory admits only 2 / 3 CTAs per SM,
+// so compiling them for 4 would only add spills
+#define FMVS_NCC_MINB_OF(ns, nm) ((ns) > 25 ? 2 : ((nm) > 4 ? 3 : FMVS_NCC_MINB))
 constexpr int kNarrowMax = 192;
 constexpr int kMaxMatch = 8;
 
@@ -1178,7 +1181,7 @@ __device__ __forceinline__ int ncc_certify(const NccSums& S, int rsum, float rho
 }
 
 template <int WW, int WH, int NM>
-__global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB) sweep_ncc_tiled(SweepArgs a) {
+__global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) sweep_ncc_tiled(SweepArgs a) {
     using namespace dev;
     constexpr int RX = WW / 2, RY = WH / 2, NS = WW * WH;
     constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
