@@ -1609,8 +1609,13 @@ int sweep(const SweepArgs& a_in, cudaStream_t s) {
     // the launch covers >= ~4 waves of 148 SMs x 3 CTAs.
     const int tiles = ((a.w + kTW - 1) / kTW) * ((a.h + kTH - 1) / kTH);
     int slices = 1;
+#ifndef FMVS_SLICE_TARGET
+// measured on C2 L2 (510 tiles): 2 slices 179.4 maps/s, 4 slices 180.8, 8
+// slices 179.7 (lower single-bundle latency, more per-CTA prologues)
+#define FMVS_SLICE_TARGET (4 * 148 * 3)
+#endif
     if (a.plane_slicing)
-        while (slices < 64 && tiles * slices < 4 * 148 * 3 && a.nplanes / (2 * slices) >= 8)
+        while (slices < 64 && tiles * slices < FMVS_SLICE_TARGET && a.nplanes / (2 * slices) >= 8)
             slices *= 2;
     const dim3 tgrid((a.w + kTW - 1) / kTW, (a.h + kTH - 1) / kTH, slices);
     if (a.kind == FMVS_COST_CENSUS && a.ww == 5)
