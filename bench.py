@@ -224,6 +224,16 @@ def roofline_entry(stage, st, peak, peak_src):
     return e
 
 
+def output_digest(depth, normals, confidence) -> str:
+    """sha256 over the raw bytes of one bundle's depth, normals and confidence
+    maps (row-major float32, normals xyz-interleaved)."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in (depth, normals, confidence):
+        h.update(np.ascontiguousarray(a, dtype=np.float32).tobytes())
+    return h.hexdigest()
+
+
 def shard(n_items: int, rank: int, world: int) -> range:
     """Contiguous shard of a bundle stream for one rank (no collective needed:
     bundles are independent)."""
@@ -350,6 +360,11 @@ def run_b200(args, rank, world, device):
     ev1.record(master)
     ev1.synchronize()
     clocks.region(t_region, time.time())
+    # digest of the last timed bundle's outputs (tests/test_fullsize_gpu.py
+    # recomputes it with the oracle on the same frames)
+    last = n_steps - 1
+    digest = {"bundle": (args.warmup * M + last) % ring,
+              "sha256": output_digest(*(t.cpu().numpy() for t in outs[last % M]))}
     total_ms = max_over_ranks(ev0.elapsed_time(ev1))
     maps_per_s = job_bundles * 1000.0 / total_ms
 
@@ -456,6 +471,7 @@ def run_b200(args, rank, world, device):
         "mde_per_s": round(maps_per_s * entries / 1e6, 1),
         "entries_per_bundle": entries, "levels": stats,
         "latency_ms": round(statistics.median(lat), 3),
+        "output_digest": digest,
         "gpu_launches": int(launches_per_step * args.steps),
         "e2e": {"value": round(e2e_maps, 3), "unit": "maps/s", "h2d_bytes_per_step": px * views,
                 "d2h_bytes_per_step": px * 20, "host_threads": M},

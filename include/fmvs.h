@@ -127,7 +127,11 @@ const char* fmvs_last_error(void);
 void fmvs_config_default(fmvs_config* cfg, double d_min, double d_max);
 
 /* ------------------------------------------------------------- context -- */
+/* A context owns one CUDA stream and the device arenas of one GPU; device
+ * < 0 selects the calling thread's current CUDA device. */
 int fmvs_ctx_create(int32_t device, fmvs_ctx** out);
+/* The calling thread's current CUDA device (cudaGetDevice), -1 on failure. */
+int32_t fmvs_current_device(void);
 void fmvs_ctx_destroy(fmvs_ctx* ctx);
 int fmvs_ctx_synchronize(fmvs_ctx* ctx);
 /* Per-level statistics of the last estimate_bundle on this context; returns
@@ -149,6 +153,18 @@ void fmvs_ctx_stage_reset(fmvs_ctx* ctx);
  * undecided bit, undecided bits, exact-path views, tile-plane iterations run,
  * tile-plane iterations skipped, exact samples taken, 0}; read-and-clear. */
 int fmvs_ctx_sweep_stats(fmvs_ctx* ctx, uint64_t out[8]);
+/* Stage capture (parity debugging, tests/test_fullsize_gpu.py): when a level
+ * >= 0 is set, the next estimate_bundle on this context keeps that level's
+ * ragged layout (the reference's CostVolume first/count/offset), u16 costs,
+ * u32 SGM aggregate, WTA winners and pre-median depth in host memory (one
+ * extra stream synchronisation). -1 disables. Sizes first, then copy into
+ * caller buffers of width*height (first, count, offset, winners, depth_raw)
+ * and `entries` (costs, aggregate) elements. */
+int fmvs_ctx_set_capture(fmvs_ctx* ctx, int32_t level);
+int fmvs_ctx_capture_sizes(fmvs_ctx* ctx, int32_t* width, int32_t* height, uint64_t* entries);
+int fmvs_ctx_capture_copy(fmvs_ctx* ctx, int32_t* first, int32_t* count, uint64_t* offset,
+                          uint16_t* costs, uint32_t* aggregate, int32_t* winners,
+                          float* depth_raw);
 /* Pinned host memory for zero-staging H2D/D2H of bundles and maps. */
 void* fmvs_host_alloc(uint64_t bytes);
 void fmvs_host_free(void* ptr);
@@ -237,6 +253,15 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t width, int32_t height, const fmvs_plan
                    const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
                    const float* prior_normals_xyz, const float* prior_depth, int32_t dir_x,
                    int32_t dir_y, uint32_t* out_values);
+/* aggregate_single_path (sgm.hpp:91-95, sgm.cpp:301-315) for any integer step
+ * (dir_x, dir_y), including non-unit steps and (0, 0) (no lines: zeros). */
+int fmvs_aggregate_single_path(fmvs_ctx* ctx, int32_t width, int32_t height,
+                               const fmvs_plane_stack* planes, const int32_t* first,
+                               const int32_t* count, const uint64_t* offset, const uint16_t* costs,
+                               uint64_t total, const uint8_t* image, const fmvs_sgm_config* cfg,
+                               const fmvs_intrinsics* intr, const float* prior_normals_xyz,
+                               const float* prior_depth, int32_t dir_x, int32_t dir_y,
+                               uint32_t* out_values);
 
 /* wta (sgm.hpp:93, sgm.cpp:333-349). */
 int fmvs_wta(fmvs_ctx* ctx, int32_t width, int32_t height, const int32_t* first,

@@ -1,6 +1,6 @@
 // Drop-in translation unit (TEST INFRASTRUCTURE for the drop-in proof):
-// defines fassmvs::estimate_bundle, dog_mask and geometric_consistency_mask on
-// top of the B200 library through the
+// defines fassmvs::estimate_bundle, dog_mask, geometric_consistency_mask and
+// every stage-level function of the reference API on top of the B200 library through the
 // public adapter include/fassmvs_b200.hpp. oracle/Makefile links it with the
 // unmodified reference sources -- pipeline.cpp compiled with
 // -Destimate_bundle=estimate_bundle_cpu so its CPU definition steps aside --
@@ -8,4 +8,5 @@
 // exercise the B200 path through the reference's API.
 #define FASSMVS_B200_DEFINE_ESTIMATE_BUNDLE
 #define FASSMVS_B200_DEFINE_POSTFILTER
+#define FASSMVS_B200_DEFINE_STAGES
 #include "fassmvs_b200.hpp"

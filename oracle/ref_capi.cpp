@@ -9,6 +9,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <exception>
+#include <limits>
 #include <span>
 #include <string>
 #include <vector>
@@ -188,11 +189,156 @@ CostVolume to_volume(int w, int h, const fmvs_plane_stack* planes, const int32_t
     return v;
 }
 
+// ---- stage capture (tests/test_fullsize_gpu.py) ---------------------------
+// A staged restatement of estimate_bundle (pipeline.cpp:200-309) through the
+// reference's public stage functions, keeping one level's ragged layout,
+// costs, aggregate, winners and pre-median depth. Its final maps are checked
+// against the reference's own estimate_bundle before anything is reported.
+struct Capture {
+    int level = -1;
+    int w = 0, h = 0;
+    std::vector<int32_t> first, count, winners;
+    std::vector<uint64_t> offset;
+    std::vector<uint16_t> costs;
+    std::vector<uint32_t> agg;
+    std::vector<float> depth_raw;
+};
+thread_local Capture g_cap;
+
+BundleResult estimate_bundle_staged(const std::vector<CalibratedView>& bundle,
+                                    const PipelineConfig& config, Capture* cap) {
+    config.validate();
+    if (bundle.size() < 3 || bundle.size() % 2 == 0)
+        throw InvalidInputError("estimate: bundle must hold an odd number (>= 3) of views");
+    const int ref_index = static_cast<int>(bundle.size()) / 2;
+    const int n = config.pyramid_levels;
+    const PyramidLevelSet pyr = build_pyramids(bundle, n);
+    DepthMap prior_depth;
+    NormalMap prior_normals;
+    PlaneStack coarser;
+    BundleResult out;
+    for (int l = n - 1; l >= 0; --l) {
+        const auto& views = pyr.levels[l];
+        const Intrinsics& intr = views[ref_index].intrinsics;
+        const int w = intr.width, h = intr.height;
+        const auto [dlo, dhi] = bounding_distances(config.depth_bounds, config.sweep_normal, intr);
+        int far = ref_index == 0 ? 1 : 0;
+        double best = -1.0;
+        for (int k = 0; k < static_cast<int>(views.size()); ++k) {
+            const double d = k == ref_index ? -1.0 : (views[k].pose.center - views[ref_index].pose.center).norm();
+            if (k != ref_index && d > best) {
+                best = d;
+                far = k;
+            }
+        }
+        PlaneStack stack;
+        stack.normal = config.sweep_normal;
+        stack.distances = plane_distances(intr, views[ref_index].pose, views[far].intrinsics,
+                                          views[far].pose, dlo, dhi, config.sweep_normal,
+                                          l == n - 1 ? config.max_planes : std::numeric_limits<int>::max());
+        const bool prior = l < n - 1;
+        const SamplingRange ranges =
+            prior ? refine_range(prior_depth, config.range_policy, config.depth_bounds, &coarser, &intr)
+                  : SamplingRange::uniform(config.depth_bounds, w, h);
+        const CostVolume vol = sweep_cost_volume(views, ref_index, stack, ranges, config.cost);
+        SgmConfig sc = config.sgm;
+        sc.penalty_scale = static_cast<int>(bundle.size()) / 2;
+        if (sc.variant == SgmVariant::SurfaceNormal && !prior)
+            sc.variant = SgmVariant::Plane;
+        const AggregatedVolume agg = aggregate(vol, views[ref_index].image, sc, intr,
+                                               prior ? &prior_normals : nullptr,
+                                               prior ? &prior_depth : nullptr);
+        const PlaneIndexMap win = wta(agg);
+        DepthMap depth(w, h, 0.0f);
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                const int32_t i = win.at(x, y);
+                if (i < 0)
+                    continue;
+                const Eigen::Vector2d px(x, y);
+                const double dw = depth_from_plane(px, stack.plane(i), intr);
+                if (dw <= 0.0)
+                    continue;
+                const std::size_t p = agg.pixel(x, y);
+                const int32_t f = agg.first[p];
+                double d = dw;
+                if (i - 1 >= f && i + 1 < f + agg.count[p]) {
+                    const uint32_t* v = agg.values.data() + agg.offset[p];
+                    const double a = depth_from_plane(px, stack.plane(i + 1), intr);
+                    const double c = depth_from_plane(px, stack.plane(i - 1), intr);
+                    if (a > 0.0 && c > 0.0 && a < dw && dw < c)
+                        d = parabola_refine(a, dw, c, v[i + 1 - f], v[i - f], v[i - 1 - f]);
+                }
+                depth.at(x, y) = static_cast<float>(d);
+            }
+        if (cap && cap->level == l) {
+            cap->w = w;
+            cap->h = h;
+            cap->first.assign(vol.first.begin(), vol.first.end());
+            cap->count.assign(vol.count.begin(), vol.count.end());
+            cap->offset.assign(vol.offset.begin(), vol.offset.end());
+            cap->costs.assign(vol.costs.begin(), vol.costs.end());
+            cap->agg.assign(agg.values.begin(), agg.values.end());
+            cap->winners.assign(win.data(), win.data() + win.size());
+            cap->depth_raw.assign(depth.data(), depth.data() + depth.size());
+        }
+        depth = median_filter_5x5(depth);
+        NormalMap normals = smooth_normals(normals_from_depth(depth, intr), views[ref_index].image,
+                                           config.normal_smoothing_radius);
+        ConfidenceMap conf = confidence_map(normals, config.sweep_normal);
+        if (l > 0) {
+            const Intrinsics& next = pyr.levels[l - 1][ref_index].intrinsics;
+            prior_depth = upscale_nearest(depth, next.width, next.height);
+            prior_normals = upscale_nearest(normals, next.width, next.height);
+            coarser = stack;
+        } else {
+            out.depth = std::move(depth);
+            out.normals = std::move(normals);
+            out.confidence = std::move(conf);
+        }
+    }
+    return out;
+}
+
 }  // namespace
 
 extern "C" {
 
 int32_t ref_abi_version(void) { return FMVS_ABI_VERSION; }
+
+// Same contract as fmvs_ctx_set_capture / fmvs_ctx_capture_* (include/fmvs.h).
+int ref_ctx_set_capture(void*, int32_t level) {
+    g_cap = Capture{};
+    g_cap.level = level;
+    return FMVS_OK;
+}
+
+int ref_ctx_capture_sizes(void*, int32_t* w, int32_t* h, uint64_t* entries) {
+    if (g_cap.w == 0) {
+        g_err = "capture: nothing captured";
+        return FMVS_ERR_INVALID_INPUT;
+    }
+    *w = g_cap.w;
+    *h = g_cap.h;
+    *entries = g_cap.costs.size();
+    return FMVS_OK;
+}
+
+int ref_ctx_capture_copy(void*, int32_t* first, int32_t* count, uint64_t* offset, uint16_t* costs,
+                         uint32_t* agg, int32_t* winners, float* depth_raw) {
+    if (g_cap.w == 0) {
+        g_err = "capture: nothing captured";
+        return FMVS_ERR_INVALID_INPUT;
+    }
+    std::copy(g_cap.first.begin(), g_cap.first.end(), first);
+    std::copy(g_cap.count.begin(), g_cap.count.end(), count);
+    std::copy(g_cap.offset.begin(), g_cap.offset.end(), offset);
+    std::copy(g_cap.costs.begin(), g_cap.costs.end(), costs);
+    std::copy(g_cap.agg.begin(), g_cap.agg.end(), agg);
+    std::copy(g_cap.winners.begin(), g_cap.winners.end(), winners);
+    std::copy(g_cap.depth_raw.begin(), g_cap.depth_raw.end(), depth_raw);
+    return FMVS_OK;
+}
 const char* ref_last_error(void) { return g_err.c_str(); }
 
 int ref_worker_count(void) { return worker_count(); }
@@ -218,7 +364,21 @@ void ref_config_default(fmvs_config* cfg, double d_min, double d_max) {
 int ref_estimate_bundle(void*, const fmvs_view* views, int32_t n_views, const fmvs_config* cfg,
                         float* depth, float* normals_xyz, float* confidence) {
     return guard([&] {
-        const BundleResult r = estimate_bundle(to_bundle(views, n_views), to_config(*cfg));
+        const std::vector<CalibratedView> bundle = to_bundle(views, n_views);
+        const PipelineConfig config = to_config(*cfg);
+        const BundleResult r = estimate_bundle(bundle, config);
+        if (g_cap.level >= 0) {
+            const BundleResult s = estimate_bundle_staged(bundle, config, &g_cap);
+            auto same = [](const auto& a, const auto& b, std::size_t bytes) {
+                return std::memcmp(a.data(), b.data(), bytes) == 0;
+            };
+            const std::size_t px = r.depth.size();
+            if (s.depth.size() != px || !same(s.depth, r.depth, 4 * px) ||
+                !same(s.confidence, r.confidence, 4 * px) ||
+                !same(s.normals, r.normals, sizeof(Eigen::Vector3f) * px))
+                throw std::runtime_error("capture: staged restatement differs from estimate_bundle");
+            g_cap.level = -1;
+        }
         std::memcpy(depth, r.depth.data(), sizeof(float) * r.depth.size());
         write_normals(r.normals, normals_xyz);
         std::memcpy(confidence, r.confidence.data(), sizeof(float) * r.confidence.size());
@@ -391,6 +551,27 @@ int ref_aggregate(void*, int32_t w, int32_t h, const fmvs_plane_stack* planes,
                 : aggregate_single_path(v, img, to_sgm(*cfg), in, dir_x, dir_y,
                                         prior_normals_xyz ? &pn : nullptr,
                                         prior_depth ? &pd : nullptr);
+        std::memcpy(out_values, a.values.data(), 4 * a.values.size());
+    });
+}
+
+int ref_aggregate_single_path(void*, int32_t w, int32_t h, const fmvs_plane_stack* planes,
+                              const int32_t* first, const int32_t* count, const uint64_t* offset,
+                              const uint16_t* costs, uint64_t total, const uint8_t* image,
+                              const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
+                              const float* prior_normals_xyz, const float* prior_depth, int32_t dir_x,
+                              int32_t dir_y, uint32_t* out_values) {
+    return guard([&] {
+        const CostVolume v = to_volume(w, h, planes, first, count, offset, costs, total);
+        NormalMap pn;
+        DepthMap pd;
+        if (prior_normals_xyz)
+            pn = to_normals(prior_normals_xyz, w, h);
+        if (prior_depth)
+            pd = to_depth(prior_depth, w, h);
+        const AggregatedVolume a =
+            aggregate_single_path(v, to_image(image, w, h), to_sgm(*cfg), to_intr(*intr), dir_x, dir_y,
+                                  prior_normals_xyz ? &pn : nullptr, prior_depth ? &pd : nullptr);
         std::memcpy(out_values, a.values.data(), 4 * a.values.size());
     });
 }

@@ -96,6 +96,9 @@ SIGNATURES = {
     "ctx_stage_time": (C.c_int, [P, I32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "ctx_stage_reset": (None, [P]),
     "ctx_sweep_stats": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+    "ctx_set_capture": (C.c_int, [P, I32]),
+    "ctx_capture_sizes": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32), C.POINTER(U64)]),
+    "ctx_capture_copy": (C.c_int, [P, P, P, P, P, P, P, P]),
     "host_alloc": (P, [U64]),
     "host_free": (None, [P]),
     "estimate_bundle": (C.c_int, [P, C.POINTER(View_c), I32, C.POINTER(Config_c), P, P, P]),
@@ -118,6 +121,9 @@ SIGNATURES = {
                                          C.POINTER(Intrinsics_c), P]),
     "aggregate": (C.c_int, [P, I32, I32, C.POINTER(PlaneStack_c), P, P, P, P, U64, P,
                             C.POINTER(SgmConfig_c), C.POINTER(Intrinsics_c), P, P, I32, I32, P]),
+    "aggregate_single_path": (C.c_int, [P, I32, I32, C.POINTER(PlaneStack_c), P, P, P, P, U64, P,
+                                        C.POINTER(SgmConfig_c), C.POINTER(Intrinsics_c), P, P, I32, I32,
+                                        P]),
     "wta": (C.c_int, [P, I32, I32, P, P, P, P, U64, P]),
     "median_filter_5x5": (C.c_int, [P, P, I32, I32, P]),
     "normals_from_depth": (C.c_int, [P, P, I32, I32, C.POINTER(Intrinsics_c), P]),

@@ -249,6 +249,17 @@ struct fmvs_ctx {
     bool timing = false;
     int sweep_exact = 0;  // FMVS_SWEEP_EXACT=1: force the exact per-hypothesis sweep
     int sweep_stats = 0;  // FMVS_SWEEP_STATS=1: count certified-census fallbacks
+    // stage capture of one level (fmvs_ctx_set_capture)
+    struct Capture {
+        int level = -1;
+        int w = 0, h = 0;
+        std::vector<fmvs::dev::VolMeta> meta;
+        std::vector<uint64_t> row_base;
+        std::vector<uint16_t> costs;
+        std::vector<uint32_t> agg;
+        std::vector<int32_t> winners;
+        std::vector<float> depth_raw;
+    } cap;
     struct Span {
         int stage;
         cudaEvent_t a, b;
@@ -644,7 +655,34 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         wa.nz = nz;
         wa.planes = d_planes;
         wa.nplanes = np;
+        const bool capture = ctx->cap.level == l;
+        if (capture)
+            wa.winners = ctx->buf("cap_winners").as<int32_t>(static_cast<size_t>(P.w) * P.h);
         ctx->timed("wta", [&] { k::wta_depth(wa, s); });
+        if (capture) {
+            // debug path: synchronous copies of the level's intermediates
+            auto& c = ctx->cap;
+            const size_t px = static_cast<size_t>(P.w) * P.h;
+            c.w = P.w;
+            c.h = P.h;
+            c.meta.resize(px);
+            c.row_base.resize(P.h + 1);
+            c.winners.resize(px);
+            c.depth_raw.resize(px);
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(c.meta.data(), meta, px * sizeof(fmvs::dev::VolMeta),
+                                            cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(c.row_base.data(), rb, (P.h + 1) * 8, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(c.winners.data(), wa.winners, px * 4, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(c.depth_raw.data(), depth_raw, px * 4, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+            const size_t entries = c.row_base[P.h];
+            c.costs.resize(entries);
+            c.agg.resize(entries);
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(c.costs.data(), costs, entries * 2, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(c.agg.data(), agg, entries * 4, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+            c.level = -1;
+        }
         ctx->timed("median", [&] { k::median5(depth_raw, P.w, P.h, depth_l[l], s); });
         launches += 2;
 
@@ -751,6 +789,8 @@ int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
     return guarded([&] {
         if (!out)
             fmvs::fail_input("ctx: null output");
+        if (device < 0)
+            FMVS_CUDA_CHECK(cudaGetDevice(&device));
         auto ctx = std::make_unique<fmvs_ctx>();
         ctx->device = device;
         if (const char* e = std::getenv("FMVS_SWEEP_EXACT"))
@@ -765,6 +805,11 @@ int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
             FMVS_CUDA_CHECK(cudaMemset(ctx->buf("sweep_stats").as<unsigned long long>(8), 0, 64));
         *out = ctx.release();
     });
+}
+
+int32_t fmvs_current_device(void) {
+    int d = -1;
+    return cudaGetDevice(&d) == cudaSuccess ? d : -1;
 }
 
 void fmvs_ctx_destroy(fmvs_ctx* ctx) {
@@ -810,6 +855,42 @@ int fmvs_ctx_sweep_stats(fmvs_ctx* ctx, uint64_t out[8]) {
         FMVS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         FMVS_CUDA_CHECK(cudaMemcpy(out, d, 64, cudaMemcpyDeviceToHost));
         FMVS_CUDA_CHECK(cudaMemset(d, 0, 64));
+    });
+}
+
+int fmvs_ctx_set_capture(fmvs_ctx* ctx, int32_t level) {
+    ctx->cap = fmvs_ctx::Capture{};
+    ctx->cap.level = level;
+    return FMVS_OK;
+}
+
+int fmvs_ctx_capture_sizes(fmvs_ctx* ctx, int32_t* w, int32_t* h, uint64_t* entries) {
+    return guarded([&] {
+        if (ctx->cap.w == 0)
+            fmvs::fail_input("capture: nothing captured");
+        *w = ctx->cap.w;
+        *h = ctx->cap.h;
+        *entries = ctx->cap.costs.size();
+    });
+}
+
+int fmvs_ctx_capture_copy(fmvs_ctx* ctx, int32_t* first, int32_t* count, uint64_t* offset,
+                          uint16_t* costs, uint32_t* agg, int32_t* winners, float* depth_raw) {
+    return guarded([&] {
+        const auto& c = ctx->cap;
+        if (c.w == 0)
+            fmvs::fail_input("capture: nothing captured");
+        for (int y = 0; y < c.h; ++y)
+            for (int x = 0; x < c.w; ++x) {
+                const size_t p = static_cast<size_t>(y) * c.w + x;
+                first[p] = static_cast<int32_t>(c.meta[p].fc & 0xffffu);
+                count[p] = static_cast<int32_t>(c.meta[p].fc >> 16);
+                offset[p] = c.row_base[y] + c.meta[p].rel;
+            }
+        std::copy(c.costs.begin(), c.costs.end(), costs);
+        std::copy(c.agg.begin(), c.agg.end(), agg);
+        std::copy(c.winners.begin(), c.winners.end(), winners);
+        std::copy(c.depth_raw.begin(), c.depth_raw.end(), depth_raw);
     });
 }
 
@@ -1186,12 +1267,18 @@ int fmvs_compute_normal_offsets(fmvs_ctx* ctx, const float* prior_normals_xyz,
     });
 }
 
-int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* planes,
+}  // extern "C"
+
+namespace {
+
+// aggregate (all cfg->paths directions) or aggregate_single_path (one step
+// (dir_x, dir_y), any integers; sgm.cpp:301-331) on a host-given volume.
+int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* planes,
                    const int32_t* first, const int32_t* count, const uint64_t* offset,
                    const uint16_t* costs, uint64_t total, const uint8_t* image,
                    const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
-                   const float* prior_normals_xyz, const float* prior_depth, int32_t dir_x,
-                   int32_t dir_y, uint32_t* out_values) {
+                   const float* prior_normals_xyz, const float* prior_depth, bool all_paths,
+                   int32_t dir_x, int32_t dir_y, uint32_t* out_values) {
     return guarded([&] {
         ctx->use();
         fmvs::validate_sgm(*cfg);  // check_aggregate_inputs, sgm.cpp:241-248
@@ -1200,15 +1287,13 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         static const int kDirs[8][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1},
                                         {1, 1}, {-1, -1}, {1, -1}, {-1, 1}};
         k::SgmArgs ga{};
-        if (dir_x == 0 && dir_y == 0) {
+        if (all_paths) {
             ga.ndirs = cfg->paths == 8 ? 8 : 4;
             for (int d = 0; d < 8; ++d) {
                 ga.dirs[d][0] = kDirs[d][0];
                 ga.dirs[d][1] = kDirs[d][1];
             }
         } else {
-            if (dir_x < -1 || dir_x > 1 || dir_y < -1 || dir_y > 1)
-                fmvs::fail_config("sgm: unsupported path direction");
             ga.ndirs = 1;
             ga.dirs[0][0] = dir_x;
             ga.dirs[0][1] = dir_y;
@@ -1216,6 +1301,22 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         std::vector<fmvs::dev::VolMeta> meta;
         std::vector<uint64_t> rb;
         host_layout(w, h, first, count, offset, total, &meta, &rb);
+        if (!all_paths && cfg->variant == FMVS_SGM_SURFACE_NORMAL) {
+            // The SN shift exists only along the canonical directions and
+            // their opposites; the reference throws when a line takes a step
+            // between two non-empty pixels along another one (sgm.cpp:72-80,
+            // 129-130).
+            const int ax = std::abs(dir_x), ay = std::abs(dir_y);
+            const bool canonical = ax <= 1 && ay <= 1 && (ax | ay) != 0;
+            if (!canonical)
+                for (int y = 0; y < h; ++y)
+                    for (int x = 0; x < w; ++x) {
+                        const int px2 = x - dir_x, py2 = y - dir_y;
+                        if (count[static_cast<size_t>(y) * w + x] > 0 && px2 >= 0 && py2 >= 0 && px2 < w &&
+                            py2 < h && count[static_cast<size_t>(py2) * w + px2] > 0)
+                            fmvs::fail_config("sgm: unsupported path direction");
+                    }
+        }
         cudaStream_t s = ctx->stream;
         Tmp t;
         const size_t px = static_cast<size_t>(w) * h;
@@ -1264,7 +1365,7 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         ga.group_caps = 32;
         const int limit = (200 * 1024) / (4 * 2 * 4);
         if (pmax > limit || ga.group > 0) {
-            const size_t lines = static_cast<size_t>(k::sgm_total_lines(w, h, 8));
+            const size_t lines = static_cast<size_t>(k::sgm_lines(w, h, ga.dirs, ga.ndirs));
             ga.scratch = t.alloc<uint32_t>(lines * 2 * (pmax + 8));
         }
         if (total > 0)
@@ -1273,6 +1374,31 @@ int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
             FMVS_CUDA_CHECK(cudaMemcpyAsync(out_values, ga.agg, total * 4, cudaMemcpyDeviceToHost, s));
         FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
     });
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmvs_aggregate(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* planes,
+                   const int32_t* first, const int32_t* count, const uint64_t* offset,
+                   const uint16_t* costs, uint64_t total, const uint8_t* image,
+                   const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
+                   const float* prior_normals_xyz, const float* prior_depth, int32_t dir_x,
+                   int32_t dir_y, uint32_t* out_values) {
+    return aggregate_impl(ctx, w, h, planes, first, count, offset, costs, total, image, cfg, intr,
+                          prior_normals_xyz, prior_depth, dir_x == 0 && dir_y == 0, dir_x, dir_y,
+                          out_values);
+}
+
+int fmvs_aggregate_single_path(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* planes,
+                               const int32_t* first, const int32_t* count, const uint64_t* offset,
+                               const uint16_t* costs, uint64_t total, const uint8_t* image,
+                               const fmvs_sgm_config* cfg, const fmvs_intrinsics* intr,
+                               const float* prior_normals_xyz, const float* prior_depth,
+                               int32_t dir_x, int32_t dir_y, uint32_t* out_values) {
+    return aggregate_impl(ctx, w, h, planes, first, count, offset, costs, total, image, cfg, intr,
+                          prior_normals_xyz, prior_depth, false, dir_x, dir_y, out_values);
 }
 
 int fmvs_wta(fmvs_ctx* ctx, int32_t w, int32_t h, const int32_t* first, const int32_t* count,

@@ -27,6 +27,45 @@ namespace {
 
 constexpr int kWarps = 4;
 
+// Lines of one path direction: pixels whose predecessor (x - dx, y - dy) lies
+// outside the image (sgm.cpp:213-219), for any step (dx, dy). They form |dx|
+// full columns plus |dy| rows of the remaining columns; `rem` enumerates them
+// column-major in the first region and row-major in the second, which for
+// unit steps is the order of the reference's start scan.
+__host__ __device__ __forceinline__ int lines_of_dir(int w, int h, int dx, int dy) {
+    const int ax = min(dx < 0 ? -dx : dx, w), ay = min(dy < 0 ? -dy : dy, h);
+    return ax * h + (w - ax) * ay;
+}
+
+__device__ __forceinline__ void line_start(int w, int h, int dx, int dy, int rem, int* x, int* y) {
+    const int ax = min(dx < 0 ? -dx : dx, w), ay = min(dy < 0 ? -dy : dy, h);
+    if (rem < ax * h) {
+        const int c = rem / h;
+        *x = dx > 0 ? c : w - 1 - c;
+        *y = rem - c * h;
+    } else {
+        const int k = rem - ax * h, cols = w - ax;
+        const int r = k / cols, c = k - r * cols;
+        *x = dx > 0 ? ax + c : c;
+        *y = dy > 0 ? r : h - 1 - r;
+    }
+}
+
+// Direction owning global line index `line` (directions own consecutive
+// blocks of lines, in a.dirs order) and the line's first pixel.
+__device__ __forceinline__ void locate_line(const SgmArgs& a, int line, int* dx, int* dy, int* x, int* y) {
+    int rem = line, d = 0;
+    for (; d < a.ndirs - 1; ++d) {
+        const int n = lines_of_dir(a.w, a.h, a.dirs[d][0], a.dirs[d][1]);
+        if (rem < n)
+            break;
+        rem -= n;
+    }
+    *dx = a.dirs[d][0];
+    *dy = a.dirs[d][1];
+    line_start(a.w, a.h, *dx, *dy, rem, x, y);
+}
+
 __device__ __forceinline__ bool scene_point(const dev::Intr& k, double nx, double ny, double nz,
                                             double dist, int x, int y, dev::D3* out) {
     using namespace dev;  // sgm.cpp:46-58
@@ -52,31 +91,8 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
     if (gw >= total_lines)
         return;
     // Direction d owns the next lines(d) warps (sgm.cpp:231-239 order).
-    int rem = gw;
-    int d = 0;
-    for (; d < a.ndirs; ++d) {
-        const int ddx = a.dirs[d][0], ddy = a.dirs[d][1];
-        const int n = (ddx != 0 && ddy != 0) ? a.h + a.w - 1 : (ddy == 0 ? a.h : a.w);
-        if (rem < n)
-            break;
-        rem -= n;
-    }
-    const int dx = a.dirs[d][0], dy = a.dirs[d][1];
-    int x, y;
-    if (dy == 0) {
-        x = dx > 0 ? 0 : a.w - 1;
-        y = rem;
-    } else if (dx == 0) {
-        x = rem;
-        y = dy > 0 ? 0 : a.h - 1;
-    } else if (rem < a.h) {
-        x = dx > 0 ? 0 : a.w - 1;
-        y = rem;
-    } else {
-        const int k = rem - a.h;  // 0 .. w-2
-        x = dx > 0 ? k + 1 : k;
-        y = dy > 0 ? 0 : a.h - 1;
-    }
+    int dx, dy, x, y;
+    locate_line(a, gw, &dx, &dy, &x, &y);
 
     uint32_t* buf_prev = (a.scratch ? a.scratch + static_cast<size_t>(gw) * 2 * a.pmax
                                     : smem + static_cast<size_t>(warp) * 2 * a.pmax);
@@ -362,32 +378,8 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_lanes_kernel(SgmArgs a, int t
     const int w = a.w, h = a.h;
 
     int dx = 1, dy = 0, x = -1, y = -1;
-    if (line < total_lines) {
-        int rem = line, d = 0;
-        for (; d < a.ndirs; ++d) {
-            const int ddx = a.dirs[d][0], ddy = a.dirs[d][1];
-            const int n = (ddx != 0 && ddy != 0) ? h + w - 1 : (ddy == 0 ? h : w);
-            if (rem < n)
-                break;
-            rem -= n;
-        }
-        dx = a.dirs[d][0];
-        dy = a.dirs[d][1];
-        if (dy == 0) {
-            x = dx > 0 ? 0 : w - 1;
-            y = rem;
-        } else if (dx == 0) {
-            x = rem;
-            y = dy > 0 ? 0 : h - 1;
-        } else if (rem < h) {
-            x = dx > 0 ? 0 : w - 1;
-            y = rem;
-        } else {
-            const int k = rem - h;
-            x = dx > 0 ? k + 1 : k;
-            y = dy > 0 ? 0 : h - 1;
-        }
-    }
+    if (line < total_lines)
+        locate_line(a, line, &dx, &dy, &x, &y);
     // buffer layout (both smem and global): [kSent sentinels][caps or pmax][kSent]
     uint32_t* sA = smem + static_cast<size_t>(warp * LPW + grp) * stride + kSent;
     uint32_t* sB = sA + caps + 2 * kSent;
@@ -739,11 +731,7 @@ void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
 }
 
 void sgm(const SgmArgs& a, cudaStream_t s) {
-    int total = 0;
-    for (int d = 0; d < a.ndirs; ++d) {
-        const int dx = a.dirs[d][0], dy = a.dirs[d][1];
-        total += (dx != 0 && dy != 0) ? a.h + a.w - 1 : (dy == 0 ? a.h : a.w);
-    }
+    const int total = sgm_lines(a.w, a.h, a.dirs, a.ndirs);
     if (total == 0)
         return;
     // int32 recurrence is exact when every intermediate stays below 2^31:
@@ -789,6 +777,13 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
 
 int sgm_total_lines(int w, int h, int ndirs) {
     return ndirs == 8 ? 2 * h + 2 * w + 4 * (w + h - 1) : 2 * h + 2 * w;
+}
+
+int sgm_lines(int w, int h, const int (*dirs)[2], int ndirs) {
+    int total = 0;
+    for (int d = 0; d < ndirs; ++d)
+        total += lines_of_dir(w, h, dirs[d][0], dirs[d][1]);
+    return total;
 }
 
 // Largest per-warp path buffer that keeps kWarps warps in shared memory.

@@ -133,6 +133,8 @@ struct SgmArgs {
 };
 void sgm(const SgmArgs& a, cudaStream_t s);
 int sgm_total_lines(int w, int h, int ndirs);
+// Lines of the given path directions (any step, sgm.cpp:213-219).
+int sgm_lines(int w, int h, const int (*dirs)[2], int ndirs);
 
 // ---- K7: WTA + depth + parabola (sgm.cpp:333-363, pipeline.cpp:263-288) ---
 struct WtaArgs {

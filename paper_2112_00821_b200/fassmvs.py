@@ -372,6 +372,28 @@ class Backend:
         del keep
         return BundleResult(depth, normals, conf)
 
+    def estimate_bundle_captured(self, bundle: Sequence[CalibratedView], config: PipelineConfig,
+                                 level: int = 0) -> dict:
+        """estimate_bundle keeping one level's intermediates (parity debugging):
+        the ragged layout first/count/offset of the reference's CostVolume
+        (matching.hpp:36-53), u16 costs, u32 aggregate, WTA winners and the
+        depth before the median filter (pipeline.cpp:263-288)."""
+        self._check(self.fn["ctx_set_capture"](self.ctx, level))
+        res = self.estimate_bundle(bundle, config)
+        w, h, n = C.c_int32(), C.c_int32(), C.c_uint64()
+        self._check(self.fn["ctx_capture_sizes"](self.ctx, C.byref(w), C.byref(h), C.byref(n)))
+        px = w.value * h.value
+        out = dict(first=np.zeros(px, np.int32), count=np.zeros(px, np.int32),
+                   offset=np.zeros(px, np.uint64), costs=np.zeros(n.value, np.uint16),
+                   aggregate=np.zeros(n.value, np.uint32), winners=np.zeros(px, np.int32),
+                   depth_raw=np.zeros((h.value, w.value), np.float32))
+        self._check(self.fn["ctx_capture_copy"](
+            self.ctx, *(_ptr(out[k]) for k in ("first", "count", "offset", "costs", "aggregate",
+                                               "winners", "depth_raw"))))
+        self.fn["ctx_set_capture"](self.ctx, -1)
+        out["result"] = res
+        return out
+
     def level_stats(self):
         out = (_abi.LevelStats_c * 16)()
         n = self.fn["ctx_level_stats"](self.ctx, out, 16)
@@ -500,7 +522,8 @@ class Backend:
         return out
 
     def _aggregate(self, vol: CostVolume, image: np.ndarray, config: SgmConfig,
-                   intrinsics: Intrinsics, dx: int, dy: int, prior_normals=None, prior_depth=None):
+                   intrinsics: Intrinsics, dx: int, dy: int, prior_normals=None, prior_depth=None,
+                   entry="aggregate"):
         st, keep = _stack_c(vol.planes)
         img = np.ascontiguousarray(image, np.uint8)
         first = np.ascontiguousarray(vol.first, np.int32)
@@ -511,10 +534,10 @@ class Backend:
         pn = _f32(prior_normals) if prior_normals is not None else None
         pd = _f32(prior_depth) if prior_depth is not None else None
         cfg = config.to_c()
-        self._check(self.fn["aggregate"](self.ctx, vol.width, vol.height, C.byref(st), _ptr(first),
-                                         _ptr(count), _ptr(offset), _ptr(costs), len(costs), _ptr(img),
-                                         C.byref(cfg), C.byref(intrinsics.to_c()), _ptr(pn), _ptr(pd),
-                                         dx, dy, _ptr(out)))
+        self._check(self.fn[entry](self.ctx, vol.width, vol.height, C.byref(st), _ptr(first),
+                                   _ptr(count), _ptr(offset), _ptr(costs), len(costs), _ptr(img),
+                                   C.byref(cfg), C.byref(intrinsics.to_c()), _ptr(pn), _ptr(pd),
+                                   dx, dy, _ptr(out)))
         return AggregatedVolume(vol.width, vol.height, vol.planes, first, count, offset,
                                 out[:len(costs)].copy())
 
@@ -526,8 +549,9 @@ class Backend:
     def aggregate_single_path(self, vol: CostVolume, image, config: SgmConfig, intrinsics: Intrinsics,
                               dir_x: int, dir_y: int, prior_normals=None,
                               prior_depth=None) -> AggregatedVolume:
-        """aggregate_single_path (sgm.hpp:91-96)."""
-        return self._aggregate(vol, image, config, intrinsics, dir_x, dir_y, prior_normals, prior_depth)
+        """aggregate_single_path (sgm.hpp:91-96): any integer step (dir_x, dir_y)."""
+        return self._aggregate(vol, image, config, intrinsics, dir_x, dir_y, prior_normals, prior_depth,
+                               entry="aggregate_single_path")
 
     def wta(self, agg: AggregatedVolume) -> np.ndarray:
         px = agg.width * agg.height

@@ -271,6 +271,40 @@ def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive, group, mon
             assert_same(a.values, b.values, f"path {dx},{dy}")
 
 
+STEPS = [(2, 1), (-1, 3), (3, 0), (0, -2), (-2, -2), (4, -3), (20, 0), (0, 0), (1, 0), (-1, 1)]
+
+
+@pytest.mark.parametrize("group", ["0", "4x4", "32x4"])
+@pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.PathGradient])
+def test_aggregate_single_path_any_step(b200, oracle, rng, variant, group, monkeypatch):
+    """aggregate_single_path walks any integer step (sgm.cpp:210-229): lines
+    start at the pixels whose predecessor (x - dx, y - dy) is outside."""
+    _blocking(monkeypatch, group)
+    w, h = 17, 11
+    img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    intr = Intrinsics(30.0, 30.0, 8.0, 5.0, w, h)
+    cfg = SgmConfig(variant, 8, 60.0, True, 0.0, 8.0, 10.0, 2)
+    vol = _volume(14, w, h, rng)
+    for dx, dy in STEPS:
+        a = b200.aggregate_single_path(vol, img, cfg, intr, dx, dy)
+        b = oracle.aggregate_single_path(vol, img, cfg, intr, dx, dy)
+        assert_same(a.values, b.values, f"step {dx},{dy}")
+
+
+def test_aggregate_single_path_sn_noncanonical(b200, rng):
+    """The surface-normal shift exists only for the canonical directions: a
+    non-unit step that links two non-empty pixels is a ConfigError
+    (sgm.cpp:72-80; the reference throws it from a worker thread)."""
+    w, h = 9, 7
+    vol = _volume(6, w, h, rng, ragged=False)
+    img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    intr = Intrinsics(20.0, 20.0, 4.0, 3.0, w, h)
+    pn = np.tile(np.array([0, 0, -1], np.float32), (h, w, 1))
+    pd = np.full((h, w), 10.0, np.float32)
+    with pytest.raises(ConfigError):
+        b200.aggregate_single_path(vol, img, SgmConfig(SgmVariant.SurfaceNormal), intr, 2, 1, pn, pd)
+
+
 @pytest.mark.parametrize("group", ["0", "4x4", "8x2", "32x4"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.SurfaceNormal, SgmVariant.PathGradient])
 @pytest.mark.parametrize("paths", [8, 4])
