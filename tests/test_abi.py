@@ -35,7 +35,7 @@ def test_oracle_exports_the_same_entry_points(oracle):
             "fmvs_ctx_last_launch_count", "fmvs_ctx_stream", "fmvs_host_alloc", "fmvs_host_free",
             "fmvs_estimate_bundle_device", "fmvs_ctx_set_timing", "fmvs_ctx_stage_count",
             "fmvs_ctx_stage_name", "fmvs_ctx_stage_time", "fmvs_ctx_stage_reset",
-            "fmvs_ctx_sweep_stats",
+            "fmvs_ctx_sweep_stats", "fmvs_current_device",
             # the reference writer runs as oracle/_ref/pfm_tool (a subprocess)
             "fmvs_write_pfm"}
     missing = [n for n in declared() if n not in skip and not hasattr(oracle.lib, "ref_" + n[5:])]
