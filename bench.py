@@ -164,43 +164,72 @@ def render_frames(b200, scene, frames):
     return bundle
 
 
-def alg_bytes(stage, stats, n_views, paths):
-    """Algorithmic HBM bytes of one stage summed over levels."""
-    tot = 0
-    for lv in stats:
-        px = lv["width"] * lv["height"]
-        e = lv["entries"]
-        if stage.startswith("sgm"):
-            if (stage == "sgm_l0") != (lv is stats[0]):
-                continue
-            tot += e * (2 * paths + 4) + px * paths * 9
-        elif stage.startswith("sweep"):
-            if (stage == "sweep_l0") != (lv is stats[0]):
-                continue
-            tot += e * (2 + 4) + px * (8 + n_views)  # u16 cost + zeroed u32 aggregate
-    return tot
+def alg_bytes(stage, stats, n_views, paths, sn=False):
+    """Algorithmic HBM bytes of one stage per bundle, summed over the levels
+    it runs on: every map read or written once, cost
+    volumes at the reference's widths (u16 cost, u32 aggregate), 8 B of
+    ragged-layout metadata per pixel. stats[0] is level 0 (finest)."""
+    L = len(stats)
+    px = [lv["width"] * lv["height"] for lv in stats]
+    ent = [lv["entries"] for lv in stats]
+    tail = range(L) if sn else [0]   # levels that compute normals (SN needs them as priors)
+    if stage == "sweep_l0":
+        return ent[0] * (2 + 4) + px[0] * (8 + n_views)   # u16 cost + zeroed u32 aggregate
+    if stage == "sweep":
+        return sum(ent[l] * 6 + px[l] * (8 + n_views) for l in range(1, L))
+    if stage == "sgm_l0":
+        return ent[0] * (2 * paths + 4) + px[0] * paths * 9
+    if stage == "sgm":
+        return sum(ent[l] * (2 * paths + 4) + px[l] * paths * 9 for l in range(1, L))
+    if stage == "pyramid":      # blur + ceil-halve: read level l-1, write level l, every view
+        return sum(n_views * (px[l - 1] + px[l]) for l in range(1, L))
+    if stage == "quads":        # matching views: 1 B in, 4 B packed bilinear taps out
+        return sum((n_views - 1) * px[l] * 5 for l in range(L))
+    if stage == "range":        # prior depth (coarser level) in; meta + row totals out
+        return sum(px[l] * 8 + (4 * px[l + 1] if l + 1 < L else 0) for l in range(L))
+    if stage == "offsets":      # SN: prior depth + normals (coarser) in, 4 x int16 out
+        return sum(16 * px[l + 1] + 8 * px[l] for l in range(L - 1)) if sn else 0
+    if stage == "wta":          # aggregate + meta in, depth out
+        return sum(ent[l] * 4 + px[l] * (8 + 4) for l in range(L))
+    if stage == "median":
+        return sum(px[l] * 8 for l in range(L))
+    if stage == "normals":      # depth in, raw normals out
+        return sum(px[l] * 16 for l in tail)
+    if stage == "smooth_conf":  # raw normals + image in, normals out (+ confidence at level 0)
+        return sum(px[l] * (12 + 1 + 12) + (4 * px[l] if l == 0 else 0) for l in tail)
+    return 0
 
 
-# ncu --set full captures of the bench command (scripts/ncu_capture.sh ->
-# scripts/ncu_summary.py), per stage: DRAM bytes of one launch and SM
-# throughput. Read from the committed summary; never measured under ncu here.
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r1", "ncu_c2_full.json")
-NCU_KEYS = {"sweep_l0": "full_sweep_census_tiled", "sgm_l0": "full_sgm_lanes_kernel"}
+# ncu --set full captures of the bench command, one per (workload, stage)
+# (scripts/ncu_capture.sh -> scripts/ncu_summary.py): DRAM bytes of one launch
+# of the stage's kernel and its SM-side utilisation. Read from the committed
+# summary of THIS workload only; never measured under ncu here, never
+# borrowed from another workload or kernel (null when no capture exists).
+NCU_DIR = os.path.join(ROOT, "profiles", "r2")
 
 
-def roofline_entry(stage, st, peak, peak_src):
+def ncu_capture(workload, stage):
+    path = os.path.join(NCU_DIR, f"ncu_{workload}_full.json")
+    try:
+        with open(path) as f:
+            m = json.load(f)[stage]
+    except (OSError, KeyError, ValueError):
+        return None, None
+    return m, os.path.relpath(path, ROOT)
+
+
+def roofline_entry(stage, st, peak, peak_src, workload):
     ach = st["gbs"] or 0.0
     e = {"kernel": stage, "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
          "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
          "alg_bytes_per_launch": st["alg_bytes"], "avg_launch_ms": st["ms_per_step"]}
-    try:
-        with open(NCU_SUMMARY) as f:
-            m = json.load(f)[NCU_KEYS[stage]]
+    m, src = ncu_capture(workload, stage)
+    if m is not None:
         e["traffic"] = int(m["dram_bytes_per_launch"])
-        e["traffic_source"] = (f"{os.path.relpath(NCU_SUMMARY, ROOT)}: dram__bytes_read.sum + "
-                               f"dram__bytes_write.sum of one ncu --set full launch")
+        e["traffic_source"] = (f"{src}: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                               f"ncu --set full launch of {m['kernel'].split('(')[0]} ({workload})")
         e["sm_throughput_pct"] = m.get("sm__throughput.avg.pct_of_peak_sustained_elapsed")
-        # the binding resource of these kernels is instruction issue, not HBM
+        # the binding resource of the sweeps is instruction issue, not HBM
         # (SURVEY §8d / BASELINE.md §3): its fraction from the same capture
         e["compute_roofline"] = {
             "resource": "SM issue slots (warp-instructions / cycle / SMSP)",
@@ -209,15 +238,14 @@ def roofline_entry(stage, st, peak, peak_src):
                 "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", 0.0)) / 100, 4),
             "alu_pipe_frac": round(float(m.get(
                 "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", 0.0)) / 100, 4),
-            "source": "ncu --set full capture (profiles/r1/ncu_c2_full.json)"}
-    except (OSError, KeyError, ValueError):
-        pass
+            "warps_active_frac": round(float(m.get(
+                "sm__warps_active.avg.pct_of_peak_sustained_active", 0.0)) / 100, 4),
+            "source": f"ncu --set full capture ({src})"}
     if stage.startswith("sweep"):
         e["note"] = ("achieved = algorithmic bytes (2 B cost + 4 B zeroed aggregate per hypothesis "
                      "+ 8 B meta + 1 B per view per pixel) / CUDA-event launch time; the sweep is "
-                     "ALU-issue-bound "
-                     "(FP32 certified census + FP64 tie fallback), not HBM-bound: see "
-                     "DESIGN.md section 5")
+                     "ALU-issue-bound (certified FP32/integer matching + FP64 tie fallback), not "
+                     "HBM-bound: see DESIGN.md section 5")
     else:
         e["note"] = ("achieved = algorithmic bytes (per hypothesis and path 2 B cost + 4 B "
                      "aggregate, per pixel and path 9 B) / CUDA-event launch time")
@@ -400,7 +428,7 @@ def run_b200(args, rank, world, device):
         stages[name] = {"ms_per_step": ms.value / nprof, "launches_per_step": calls.value / nprof}
     peak, peak_src = peaks()
     for name, st in stages.items():
-        b = alg_bytes(name, stats, views, cfg.sgm.paths)
+        b = alg_bytes(name, stats, views, cfg.sgm.paths, sn=cfg.sgm.variant == pkg.SgmVariant.SurfaceNormal)
         st["alg_bytes"] = b
         st["gbs"] = b / (st["ms_per_step"] * 1e6) if b and st["ms_per_step"] > 0 else None
     dominant = max(stages, key=lambda n: stages[n]["ms_per_step"]) if stages else None
@@ -480,17 +508,24 @@ def run_b200(args, rank, world, device):
                    for k, v in stages.items()},
     }
     if dominant is not None:
-        result["roofline"] = roofline_entry(dominant, stages[dominant], peak, peak_src)
+        result["roofline"] = roofline_entry(dominant, stages[dominant], peak, peak_src, args.workload)
         if "sgm_l0" in stages and dominant != "sgm_l0":
             # the north star names both the sweep and SGM; SGM is the HBM/L2-facing one
-            result["roofline_sgm"] = roofline_entry("sgm_l0", stages["sgm_l0"], peak, peak_src)
+            result["roofline_sgm"] = roofline_entry("sgm_l0", stages["sgm_l0"], peak, peak_src,
+                                                    args.workload)
     for c in ctxs:
         c.close()
     return result
 
 
-def cpu_reference(args, scene, cfgkw, steps, warmup):
-    """The reference CPU implementation (oracle/_ref, the unmodified sources)."""
+def cpu_reference(args, scene, cfgkw, steps, warmup, threads=None):
+    """The reference CPU implementation (oracle/_ref, the unmodified sources),
+    on `threads` workers (FASSMVS_THREADS, parallel.cpp:10-18; default: every
+    host thread)."""
+    if threads:
+        os.environ["FASSMVS_THREADS"] = str(threads)
+    else:
+        os.environ.pop("FASSMVS_THREADS", None)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ref
     import paper_2112_00821_b200 as pkg
@@ -511,6 +546,26 @@ def cpu_reference(args, scene, cfgkw, steps, warmup):
     return steps / sum(times), cores, times
 
 
+def self_spawn(n: int) -> int:
+    """Re-launches this command under torch.distributed.run with one rank per
+    GPU (the driver's own launch form); fails loudly when fewer than n GPUs
+    are visible (never a silent 1-GPU run)."""
+    import socket
+    if not SHARE_DEVICE:
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} requested but {have} GPU(s) visible", file=sys.stderr)
+            return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -522,17 +577,27 @@ def main():
     ap.add_argument("--inflight", type=int, default=5, help="bundles in flight (contexts/streams; also the e2e host threads)")
     ap.add_argument("--cpu-baseline-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline-1t", action="store_true",
+                    help="also time one bundle of the reference on ONE host thread (~1 min at C2)")
+    ap.add_argument("--cpu-threads", type=int, default=0,
+                    help="reference arm: host threads (default: all)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: one process per GPU, launched here
+        sys.exit(self_spawn(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     scene, cfgkw, desc = WORKLOADS[args.workload]
 
     if args.impl == "reference":
         if rank != 0:
             return
-        value, cores, times = cpu_reference(args, scene, cfgkw, args.steps, args.warmup)
+        value, cores, times = cpu_reference(args, scene, cfgkw, args.steps, args.warmup,
+                                            args.cpu_threads or None)
         sample = f"{args.steps} full {args.workload.upper()} bundles, estimate_bundle only"
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "maps/s",
@@ -560,9 +625,14 @@ def main():
         try:
             v, cores, times = cpu_reference(args, scene, cfgkw, args.cpu_baseline_steps, 0)
             result["cpu_baseline"] = {"value": round(v, 5), "unit": "maps/s", "cores": cores,
-                                      "kind": "reference",
+                                      "kind": "reference", "host_threads": os.cpu_count(),
                                       "sample": f"{args.cpu_baseline_steps} {args.workload.upper()} "
                                                 f"bundle(s) on {cores} host threads (oracle/_ref)"}
+            if args.cpu_baseline_1t:
+                v1, c1, _ = cpu_reference(args, scene, cfgkw, 1, 0, threads=1)
+                result["cpu_baseline"]["single_thread"] = {
+                    "value": round(v1, 5), "unit": "maps/s", "cores": c1,
+                    "sample": f"1 {args.workload.upper()} bundle on 1 host thread (FASSMVS_THREADS=1)"}
         except Exception as e:  # reported, never silently replaced
             result["cpu_baseline"] = {"value": None, "error": str(e)}
     if world > 1:

@@ -348,6 +348,33 @@ int fmvs_estimate_sequence(fmvs_ctx* ctx, const fmvs_view* frames, int32_t n_fra
                            float* depth, float* normals_xyz, float* confidence,
                            int32_t* ref_frames, int32_t capacity, int32_t* n_results);
 
+/* The same loop sharded over GPUs: devices[0..n_devices) own
+ * contiguous shards of the result list (a device id may repeat: several
+ * shards on one GPU), each run by one host thread with `inflight` bundles in
+ * flight (one stream each) and a post stream for the filters. Results stream
+ * back as soon as they are final (direct async D2H when the three output
+ * buffers are pinned, e.g. fmvs_host_alloc; else through pinned staging),
+ * device memory is a bounded pool of result slots, and the geometric filter's
+ * window crosses shard boundaries through a halo of DoG-filtered depth maps
+ * copied peer to peer (cudaMemcpyPeerAsync over NVLink, after the producer's
+ * event). Arguments, outputs and errors as fmvs_estimate_sequence, whose
+ * results it reproduces bit for bit for any device list. */
+int fmvs_estimate_sequence_multi(const int32_t* devices, int32_t n_devices, int32_t inflight,
+                                 const fmvs_view* frames, int32_t n_frames, int32_t stride,
+                                 const fmvs_config* cfg, int32_t filter, float* depth,
+                                 float* normals_xyz, float* confidence, int32_t* ref_frames,
+                                 int32_t capacity, int32_t* n_results);
+
+/* Shard and halo plan of fmvs_estimate_sequence_multi (host only, no GPU):
+ * for m results over n_shards contiguous shards and a geometric window of
+ * `window` results (min(5, m) with the geometric filter, else 0), shard
+ * `shard`'s result range [*begin, *end), the results it imports from other
+ * shards and the results it exports to them (ascending; arrays of m entries
+ * or NULL). */
+int fmvs_sequence_plan(int32_t m, int32_t n_shards, int32_t shard, int32_t window, int32_t* begin,
+                       int32_t* end, int32_t* imports, int32_t* n_imports, int32_t* exports,
+                       int32_t* n_exports);
+
 /* ------------------------------------- output stage -- */
 /* colorize_depth / colorize_normals / colorize_confidence (colorize.hpp:9-15,
  * colorize.cpp:32-70): rgb = 3*width*height bytes. */

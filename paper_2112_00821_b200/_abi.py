@@ -139,6 +139,10 @@ SIGNATURES = {
                                              C.POINTER(GeomFilterConfig_c), P]),
     "estimate_sequence": (C.c_int, [P, C.POINTER(View_c), I32, I32, C.POINTER(Config_c), I32, P, P,
                                     P, P, I32, C.POINTER(I32)]),
+    "estimate_sequence_multi": (C.c_int, [C.POINTER(I32), I32, I32, C.POINTER(View_c), I32, I32,
+                                          C.POINTER(Config_c), I32, P, P, P, P, I32, C.POINTER(I32)]),
+    "sequence_plan": (C.c_int, [I32, I32, I32, I32, C.POINTER(I32), C.POINTER(I32), P, C.POINTER(I32), P,
+                                C.POINTER(I32)]),
     "colorize_depth": (C.c_int, [P, P, I32, I32, D, D, P]),
     "colorize_normals": (C.c_int, [P, P, I32, I32, P]),
     "colorize_confidence": (C.c_int, [P, P, I32, I32, P]),

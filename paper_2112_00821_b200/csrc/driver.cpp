@@ -15,11 +15,14 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -732,31 +735,58 @@ void copy_views_to_device(fmvs_ctx* ctx, const fmvs_view* views, int n,
     }
 }
 
-// Converts the reference ragged layout (first, count, offset) to meta +
-// row bases; offsets must be the exclusive prefix sum of counts.
+// Converts the reference ragged layout (first, count, offset) to meta + row
+// bases. The reference allows any per-pixel offsets (matching.hpp:36-53: a
+// pixel's entries are costs[offset[p], offset[p] + count[p]); test_sgm.cpp:262
+// zeroes a count in place); the device layout is the compact prefix sum, so a
+// non-compact input is gathered: *src receives each compact entry's source
+// index (empty when the input is already compact). *compact_total = sum of
+// counts.
 void host_layout(int w, int h, const int32_t* first, const int32_t* count, const uint64_t* offset,
-                 uint64_t total, std::vector<fmvs::dev::VolMeta>* meta, std::vector<uint64_t>* rb) {
-    meta->resize(static_cast<size_t>(w) * h);
+                 uint64_t total, std::vector<fmvs::dev::VolMeta>* meta, std::vector<uint64_t>* rb,
+                 std::vector<uint64_t>* src, uint64_t* compact_total) {
+    const size_t px = static_cast<size_t>(w) * h;
+    meta->resize(px);
     rb->resize(h + 1);
+    src->clear();
+    bool compact = true;
     uint64_t run = 0;
+    for (size_t p = 0; p < px; ++p) {
+        if (first[p] < 0 || first[p] > 65535 || count[p] < 0 || count[p] > 65535)
+            fmvs::fail_input("b200 layout: first/count out of the supported range");
+        if (offset[p] + static_cast<uint64_t>(count[p]) > total)
+            fmvs::fail_input("b200 layout: a pixel's entries lie outside the cost array");
+        if (count[p] > 0 && offset[p] != run)
+            compact = false;
+        run += static_cast<uint64_t>(count[p]);
+    }
+    *compact_total = run;
+    if (!compact)
+        src->reserve(run);
+    run = 0;
     for (int y = 0; y < h; ++y) {
         const size_t row = static_cast<size_t>(y) * w;
-        (*rb)[y] = w > 0 ? offset[row] : run;
+        (*rb)[y] = run;
         for (int x = 0; x < w; ++x) {
             const size_t p = row + x;
-            if (offset[p] != run)
-                fmvs::fail_input("b200 layout: offsets must be the prefix sum of counts");
-            if (first[p] < 0 || first[p] > 65535 || count[p] < 0 || count[p] > 65535)
-                fmvs::fail_input("b200 layout: first/count out of the supported range");
-            (*meta)[p] = fmvs::dev::VolMeta{static_cast<uint32_t>(offset[p] - (*rb)[y]),
+            (*meta)[p] = fmvs::dev::VolMeta{static_cast<uint32_t>(run - (*rb)[y]),
                                             static_cast<uint32_t>(first[p]) |
                                                 (static_cast<uint32_t>(count[p]) << 16)};
+            if (!compact)
+                for (int32_t i = 0; i < count[p]; ++i)
+                    src->push_back(offset[p] + i);
             run += static_cast<uint64_t>(count[p]);
         }
     }
     (*rb)[h] = run;
-    if (run != total)
-        fmvs::fail_input("b200 layout: counts do not sum to the cost count");
+}
+
+template <typename T>
+std::vector<T> gather(const T* in, const std::vector<uint64_t>& src) {
+    std::vector<T> out(src.size());
+    for (size_t i = 0; i < src.size(); ++i)
+        out[i] = in[src[i]];
+    return out;
 }
 
 }  // namespace
@@ -1299,8 +1329,16 @@ int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
             ga.dirs[0][1] = dir_y;
         }
         std::vector<fmvs::dev::VolMeta> meta;
-        std::vector<uint64_t> rb;
-        host_layout(w, h, first, count, offset, total, &meta, &rb);
+        std::vector<uint64_t> rb, src;
+        uint64_t n_entries = 0;
+        host_layout(w, h, first, count, offset, total, &meta, &rb, &src, &n_entries);
+        std::vector<uint16_t> gathered;
+        if (!src.empty()) {
+            gathered = gather(costs, src);
+            costs = gathered.data();
+        }
+        const uint64_t stored = total;  // the caller's value array (zeros outside pixel ranges)
+        total = n_entries;
         if (!all_paths && cfg->variant == FMVS_SGM_SURFACE_NORMAL) {
             // The SN shift exists only along the canonical directions and
             // their opposites; the reference throws when a line takes a step
@@ -1370,9 +1408,21 @@ int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         }
         if (total > 0)
             k::sgm(ga, s);
+        std::vector<uint32_t> compact_out;
+        const bool remap = !src.empty() || total != stored;
+        uint32_t* dst = out_values;
+        if (remap) {
+            compact_out.resize(total);
+            dst = compact_out.data();
+        }
         if (total > 0)
-            FMVS_CUDA_CHECK(cudaMemcpyAsync(out_values, ga.agg, total * 4, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(dst, ga.agg, total * 4, cudaMemcpyDeviceToHost, s));
         FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (remap) {  // make_accumulator zeroes the whole array (sgm.cpp:198-208)
+            std::fill(out_values, out_values + stored, 0u);
+            for (size_t i = 0; i < compact_out.size(); ++i)
+                out_values[src.empty() ? i : src[i]] = compact_out[i];
+        }
     });
 }
 
@@ -1406,8 +1456,15 @@ int fmvs_wta(fmvs_ctx* ctx, int32_t w, int32_t h, const int32_t* first, const in
     return guarded([&] {
         ctx->use();
         std::vector<fmvs::dev::VolMeta> meta;
-        std::vector<uint64_t> rb;
-        host_layout(w, h, first, count, offset, total, &meta, &rb);
+        std::vector<uint64_t> rb, src;
+        uint64_t n_entries = 0;
+        host_layout(w, h, first, count, offset, total, &meta, &rb, &src, &n_entries);
+        std::vector<uint32_t> gathered;
+        if (!src.empty()) {
+            gathered = gather(values, src);
+            values = gathered.data();
+        }
+        total = n_entries;
         cudaStream_t s = ctx->stream;
         Tmp t;
         const size_t px = static_cast<size_t>(w) * h;
@@ -1820,6 +1877,565 @@ int fmvs_estimate_sequence(fmvs_ctx* ctx, const fmvs_view* frames, int32_t n_fra
     });
 }
 
+}  // extern "C"
+
+// ======================================================= multi-GPU sequence
+// fmvs_estimate_sequence_multi: the `fassmvs estimate` loop (tools/fassmvs.cpp:
+// 139-176) sharded over GPUs. Results (bundles) are independent
+// (SPEC.md:408), so each device owns a contiguous shard and runs it with
+// `inflight` bundles in flight (one context = one stream each). Post-filters
+// run on a per-device post stream as soon as their inputs exist; results
+// stream back to the caller's buffers one by one (D2H right after the result
+// is final), and device memory is a bounded pool of result slots. The only
+// cross-device data is the geometric filter's window (postfilter.cpp:95-160):
+// the DoG-filtered depth maps of the few results at shard boundaries, copied
+// peer to peer (cudaMemcpyPeerAsync over NVLink) after the producer's event.
+
+namespace {
+
+// Window of the geometric filter for result i of m (ws = min(5, m);
+// tools/fassmvs.cpp:163-172): [start, start + ws).
+int window_start(int i, int m, int ws) { return std::clamp(i - ws / 2, 0, m - ws); }
+
+struct SeqPlan {
+    std::vector<int> begin, end;  // shard bounds over results
+    // per shard: results imported from other shards / exported to them
+    std::vector<std::vector<int>> imports, exports;
+};
+
+SeqPlan plan_sequence(int m, int shards, int ws) {
+    SeqPlan p;
+    p.begin.resize(shards);
+    p.end.resize(shards);
+    const int base = m / shards, extra = m % shards;
+    int at = 0;
+    for (int s = 0; s < shards; ++s) {
+        p.begin[s] = at;
+        at += base + (s < extra ? 1 : 0);
+        p.end[s] = at;
+    }
+    p.imports.assign(shards, {});
+    p.exports.assign(shards, {});
+    if (ws <= 1)
+        return p;
+    std::vector<int> owner(m);
+    for (int s = 0; s < shards; ++s)
+        for (int k = p.begin[s]; k < p.end[s]; ++k)
+            owner[k] = s;
+    std::vector<std::vector<char>> need(shards, std::vector<char>(m, 0));
+    for (int s = 0; s < shards; ++s)
+        for (int i = p.begin[s]; i < p.end[s]; ++i) {
+            const int st = window_start(i, m, ws);
+            for (int k = st; k < st + ws; ++k)
+                if (owner[k] != s)
+                    need[s][k] = 1;
+        }
+    std::vector<char> exported(m, 0);
+    for (int s = 0; s < shards; ++s)
+        for (int k = 0; k < m; ++k)
+            if (need[s][k]) {
+                p.imports[s].push_back(k);
+                exported[k] = 1;
+            }
+    for (int k = 0; k < m; ++k)
+        if (exported[k])
+            p.exports[owner[k]].push_back(k);
+    return p;
+}
+
+// Host-side publication of exported (DoG-filtered) depth maps.
+struct HaloBoard {
+    std::mutex mu;
+    std::condition_variable cv;
+    struct Entry {
+        const float* depth = nullptr;
+        int device = 0;
+        cudaEvent_t ready = nullptr;
+    };
+    std::unordered_map<int, Entry> posted;
+    bool failed = false;
+
+    void post(int k, const Entry& e) {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            posted[k] = e;
+        }
+        cv.notify_all();
+    }
+    // false when another shard failed (the caller then stops)
+    bool wait(int k, Entry* out) {
+        std::unique_lock<std::mutex> g(mu);
+        cv.wait(g, [&] { return failed || posted.count(k) > 0; });
+        if (failed)
+            return false;
+        *out = posted[k];
+        return true;
+    }
+    void fail() {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            failed = true;
+        }
+        cv.notify_all();
+    }
+};
+
+struct SeqJob {
+    const fmvs_view* frames;
+    int n_frames;
+    const fmvs_config* cfg;
+    int filter;
+    int m, ws, half, w, h;
+    std::vector<int> refs;
+    float* depth;
+    float* normals;
+    float* conf;
+    fmvs_geom_filter_config gc;
+};
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// One shard on one device: everything its host thread owns.
+struct Shard {
+    int device = 0, begin = 0, end = 0, inflight = 1;
+    std::vector<int> imports, exports;
+    std::vector<fmvs_ctx*> ctxs;
+    fmvs_ctx* post = nullptr;  // its stream is the post stream; its buffers hold masks
+    std::vector<void*> allocs;
+    std::vector<cudaEvent_t> events;
+    std::string error;
+    int code = FMVS_OK;
+
+    float* alloc_maps(size_t px) {
+        void* p = nullptr;
+        FMVS_CUDA_CHECK(cudaMalloc(&p, 5 * px * sizeof(float)));
+        allocs.push_back(p);
+        return static_cast<float*>(p);
+    }
+    cudaEvent_t event() {
+        cudaEvent_t e;
+        FMVS_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        events.push_back(e);
+        return e;
+    }
+    void release() {
+        FMVS_CUDA_CHECK(cudaSetDevice(device));
+        for (void* p : allocs)
+            cudaFree(p);
+        for (cudaEvent_t e : events)
+            cudaEventDestroy(e);
+        for (fmvs_ctx* c : ctxs)
+            fmvs_ctx_destroy(c);
+        if (post)
+            fmvs_ctx_destroy(post);
+        allocs.clear();
+        events.clear();
+        ctxs.clear();
+        post = nullptr;
+    }
+};
+
+void run_shard(Shard& sh, const SeqJob& job, HaloBoard& board) {
+    FMVS_CUDA_CHECK(cudaSetDevice(sh.device));
+    const size_t px = static_cast<size_t>(job.w) * job.h;
+    const int nb = job.cfg->bundle_size;
+    for (int i = 0; i < sh.inflight; ++i) {
+        fmvs_ctx* c = nullptr;
+        const int rc = fmvs_ctx_create(sh.device, &c);
+        if (rc != FMVS_OK)
+            throw Error(rc, g_last_error);
+        sh.ctxs.push_back(c);
+    }
+    {
+        fmvs_ctx* c = nullptr;
+        const int rc = fmvs_ctx_create(sh.device, &c);
+        if (rc != FMVS_OK)
+            throw Error(rc, g_last_error);
+        sh.post = c;
+    }
+    cudaStream_t ps = sh.post->stream;
+    if (sh.begin >= sh.end)
+        return;
+
+    // frames of this shard, resident once; bundles reference them in place
+    const int f0 = job.refs[sh.begin] - job.half;
+    const int f1 = job.refs[sh.end - 1] + job.half + 1;
+    uint8_t* d_frames = sh.post->buf("seq_frames").as<uint8_t>(px * (f1 - f0));
+    for (int f = f0; f < f1; ++f)
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(d_frames + (f - f0) * px, job.frames[f].image, px,
+                                        cudaMemcpyHostToDevice, ps));
+    cudaEvent_t frames_ready = sh.event();
+    FMVS_CUDA_CHECK(cudaEventRecord(frames_ready, ps));
+    for (fmvs_ctx* c : sh.ctxs)
+        FMVS_CUDA_CHECK(cudaStreamWaitEvent(c->stream, frames_ready, 0));
+
+    const bool dog = job.filter == FMVS_FILTER_DOG || job.filter == FMVS_FILTER_BOTH;
+    const bool geom = job.ws > 1;
+    const int m = job.m;
+    // last post step (result index) that reads result k
+    auto last_user = [&](int k) {
+        int last = k;
+        if (geom)
+            for (int i = std::max(0, k - job.ws + 1); i < std::min(m, k + job.ws); ++i) {
+                const int st = window_start(i, m, job.ws);
+                if (k >= st && k < st + job.ws)
+                    last = std::max(last, i);
+            }
+        return last;
+    };
+
+    // result slots: depth | normals | conf (5 px floats). Exported results
+    // keep theirs to the end; the others cycle through a pool, a slot going
+    // back to the pool after the post step of its last reader (recorded on
+    // the post stream; the next bundle in it waits for that event).
+    struct PoolSlot {
+        float* maps;
+        cudaEvent_t after;
+    };
+    std::vector<PoolSlot> pool;  // FIFO: the longest-released slot is reused first
+    size_t pool_head = 0;
+    int pooled_slots = 0;
+    // enough slots that `inflight` bundles never wait for each other's D2H
+    const int min_slots = sh.inflight + job.ws + 2;
+    std::unordered_map<int, float*> slot_of;  // result -> maps (local and imported)
+    std::vector<std::pair<int, int>> held;    // (last reader, result) of pooled slots in use
+    const std::vector<int>& ex = sh.exports;
+    auto is_export = [&](int k) { return std::binary_search(ex.begin(), ex.end(), k); };
+
+    uint8_t* dog_mask = sh.post->buf("seq_dog").as<uint8_t>(px);
+    uint8_t* keep = sh.post->buf("seq_keep").as<uint8_t>(px);
+    float* out_depth = sh.post->buf("seq_out_depth").as<float>(px);
+    const int nlocal = sh.end - sh.begin;
+    k::GeomView* gv_host = nullptr;
+    k::GeomView* gv_dev = nullptr;
+    HostBuf gv_pinned;
+    if (geom) {
+        gv_host = static_cast<k::GeomView*>(gv_pinned.get(sizeof(k::GeomView) * nlocal * job.ws));
+        gv_dev = sh.post->buf("seq_geom_views").as<k::GeomView>(static_cast<size_t>(nlocal) * job.ws);
+    }
+    // D2H: straight into the caller's buffers when they are pinned, else
+    // through pinned staging slots drained by this thread
+    const bool direct = host_pinned(job.depth) && host_pinned(job.normals) && host_pinned(job.conf);
+    struct Staged {
+        int k;
+        float* host;
+        cudaEvent_t done;
+    };
+    std::vector<Staged> staged;  // in flight
+    std::vector<std::pair<float*, cudaEvent_t>> stage_free;
+    auto drain = [&](bool all) {
+        while (!staged.empty()) {
+            Staged& st = staged.front();
+            if (!all && cudaEventQuery(st.done) == cudaErrorNotReady) {
+                cudaGetLastError();
+                break;
+            }
+            FMVS_CUDA_CHECK(cudaEventSynchronize(st.done));
+            std::memcpy(job.depth + st.k * px, st.host, 4 * px);
+            std::memcpy(job.normals + 3 * st.k * px, st.host + px, 12 * px);
+            std::memcpy(job.conf + st.k * px, st.host + 4 * px, 4 * px);
+            stage_free.push_back({st.host, st.done});
+            staged.erase(staged.begin());
+        }
+    };
+    HostBuf stage_mem;  // pinned staging ring (grown to 2 * inflight + 2 slots)
+    std::vector<float*> stage_slots;
+
+    // bundle order: exported results first (so every shard publishes its
+    // halo before it could wait for another's), then the rest ascending
+    std::vector<int> order(ex.begin(), ex.end());
+    for (int k = sh.begin; k < sh.end; ++k)
+        if (!is_export(k))
+            order.push_back(k);
+    std::vector<char> enqueued(m, 0);
+    int next_post = sh.begin;
+    int rr = 0;
+
+    auto post_step = [&](int i) {
+        float* mi = slot_of.at(i);
+        float* dep = mi;
+        float* nrm = mi + px;
+        float* cf = mi + 4 * px;
+        const float* final_depth = dep;
+        if (geom) {
+            const int st = window_start(i, m, job.ws);
+            for (int j = 0; j < job.ws; ++j) {
+                const int kk = st + j;
+                if (!slot_of.count(kk)) {  // import from the owning shard
+                    HaloBoard::Entry e;
+                    if (!board.wait(kk, &e))
+                        throw Error(FMVS_ERR_CUDA, "sequence: another shard failed");
+                    float* dst = sh.alloc_maps(px);  // depth only is used
+                    FMVS_CUDA_CHECK(cudaStreamWaitEvent(ps, e.ready, 0));
+                    FMVS_CUDA_CHECK(cudaMemcpyPeerAsync(dst, sh.device, e.depth, e.device, 4 * px, ps));
+                    slot_of[kk] = dst;
+                }
+                const int fr = job.refs[kk];
+                gv_host[(i - sh.begin) * job.ws + j] =
+                    geom_view(slot_of[kk], job.w, job.h, job.frames[fr].intrinsics, job.frames[fr].pose);
+            }
+            k::GeomView* g = gv_dev + static_cast<size_t>(i - sh.begin) * job.ws;
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(g, gv_host + (i - sh.begin) * job.ws, sizeof(k::GeomView) * job.ws,
+                                            cudaMemcpyHostToDevice, ps));
+            k::GeomArgs ga{};
+            ga.views = g;
+            ga.n = job.ws;
+            ga.ref = i - st;
+            ga.eta_r = job.gc.eta_r;
+            ga.eta_h = job.gc.eta_h;
+            ga.bilinear = job.gc.lookup == FMVS_LOOKUP_BILINEAR;
+            ga.keep = keep;
+            k::geometric_mask(ga, job.w, job.h, ps);
+            // the slot keeps the DoG-filtered depth for later windows; the
+            // final depth is a masked copy
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(out_depth, dep, 4 * px, cudaMemcpyDeviceToDevice, ps));
+            k::apply_mask(out_depth, nrm, cf, keep, static_cast<int>(px), ps);
+            final_depth = out_depth;
+        }
+        if (direct) {
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(job.depth + i * px, final_depth, 4 * px, cudaMemcpyDeviceToHost, ps));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(job.normals + 3 * i * px, nrm, 12 * px, cudaMemcpyDeviceToHost, ps));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(job.conf + i * px, cf, 4 * px, cudaMemcpyDeviceToHost, ps));
+        } else {
+            drain(false);
+            float* hs = nullptr;
+            cudaEvent_t done = nullptr;
+            if (!stage_free.empty()) {
+                hs = stage_free.back().first;
+                done = stage_free.back().second;
+                stage_free.pop_back();
+            } else if (stage_slots.size() < static_cast<size_t>(2 * sh.inflight + 2)) {
+                if (stage_slots.empty())
+                    stage_mem.get(sizeof(float) * 5 * px * (2 * sh.inflight + 2));
+                hs = static_cast<float*>(stage_mem.ptr) + 5 * px * stage_slots.size();
+                stage_slots.push_back(hs);
+                done = sh.event();
+            } else {
+                drain(true);
+                hs = stage_free.back().first;
+                done = stage_free.back().second;
+                stage_free.pop_back();
+            }
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(hs, final_depth, 4 * px, cudaMemcpyDeviceToHost, ps));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(hs + px, nrm, 12 * px, cudaMemcpyDeviceToHost, ps));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(hs + 4 * px, cf, 4 * px, cudaMemcpyDeviceToHost, ps));
+            FMVS_CUDA_CHECK(cudaEventRecord(done, ps));
+            staged.push_back({i, hs, done});
+        }
+        // release pooled slots whose last reader was this step
+        cudaEvent_t after = nullptr;
+        for (auto it = held.begin(); it != held.end();) {
+            if (it->first <= i) {
+                if (!after) {
+                    after = sh.event();
+                    FMVS_CUDA_CHECK(cudaEventRecord(after, ps));
+                }
+                pool.push_back({slot_of[it->second], after});
+                it = held.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    };
+
+    for (size_t pos = 0; pos < order.size(); ++pos) {
+        const int k = order[pos];
+        fmvs_ctx* c = sh.ctxs[rr++ % sh.inflight];
+        float* maps = nullptr;
+        if (is_export(k)) {
+            maps = sh.alloc_maps(px);
+        } else {
+            if (pool_head < pool.size() && pooled_slots >= min_slots) {
+                maps = pool[pool_head].maps;
+                FMVS_CUDA_CHECK(cudaStreamWaitEvent(c->stream, pool[pool_head].after, 0));
+                ++pool_head;
+            } else {
+                maps = sh.alloc_maps(px);
+                ++pooled_slots;
+            }
+            held.push_back({last_user(k), k});
+        }
+        slot_of[k] = maps;
+        const int first = job.refs[k] - job.half;
+        std::vector<const uint8_t*> d_images(nb);
+        for (int v = 0; v < nb; ++v)
+            d_images[v] = d_frames + (first + v - f0) * px;
+        run_bundle(c, job.frames + first, nb, *job.cfg, d_images.data(), maps, maps + px, maps + 4 * px);
+        cudaEvent_t done = sh.event();
+        FMVS_CUDA_CHECK(cudaEventRecord(done, c->stream));
+        FMVS_CUDA_CHECK(cudaStreamWaitEvent(ps, done, 0));
+        if (dog) {  // tools/fassmvs.cpp:151-158
+            dog_mask_device(sh.post, d_frames + (job.refs[k] - f0) * px, job.w, job.h, dog_mask);
+            k::apply_mask(maps, maps + px, maps + 4 * px, dog_mask, static_cast<int>(px), ps);
+        }
+        if (is_export(k)) {
+            cudaEvent_t ready = sh.event();
+            FMVS_CUDA_CHECK(cudaEventRecord(ready, ps));
+            board.post(k, HaloBoard::Entry{maps, sh.device, ready});
+        }
+        enqueued[k] = 1;
+        // every result whose window is now enqueued locally (imports are
+        // awaited inside the step). Not before all exports are posted: a
+        // shard never waits for another while holding back its own halo.
+        if (pos + 1 < ex.size())
+            continue;
+        while (next_post < sh.end) {
+            bool ready = true;
+            if (geom) {
+                const int st = window_start(next_post, m, job.ws);
+                for (int kk = st; kk < st + job.ws; ++kk)
+                    if (kk >= sh.begin && kk < sh.end && !enqueued[kk])
+                        ready = false;
+            } else {
+                ready = enqueued[next_post] != 0;
+            }
+            if (!ready)
+                break;
+            post_step(next_post++);
+        }
+    }
+    FMVS_CUDA_CHECK(cudaStreamSynchronize(ps));
+    for (fmvs_ctx* c : sh.ctxs)
+        FMVS_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    drain(true);
+}
+
+}  // namespace
+
+extern "C" {
+
+int fmvs_sequence_plan(int32_t m, int32_t n_shards, int32_t shard, int32_t window, int32_t* begin,
+                       int32_t* end, int32_t* imports, int32_t* n_imports, int32_t* exports,
+                       int32_t* n_exports) {
+    return guarded([&] {
+        if (m < 0 || n_shards < 1 || shard < 0 || shard >= n_shards || window < 0 || window > std::max(m, 0))
+            fmvs::fail_input("sequence plan: invalid arguments");
+        const SeqPlan p = plan_sequence(m, n_shards, window);
+        *begin = p.begin[shard];
+        *end = p.end[shard];
+        *n_imports = static_cast<int32_t>(p.imports[shard].size());
+        *n_exports = static_cast<int32_t>(p.exports[shard].size());
+        if (imports)
+            std::copy(p.imports[shard].begin(), p.imports[shard].end(), imports);
+        if (exports)
+            std::copy(p.exports[shard].begin(), p.exports[shard].end(), exports);
+    });
+}
+
+int fmvs_estimate_sequence_multi(const int32_t* devices, int32_t n_devices, int32_t inflight,
+                                 const fmvs_view* frames, int32_t n_frames, int32_t stride,
+                                 const fmvs_config* cfg, int32_t filter, float* depth, float* normals_xyz,
+                                 float* confidence, int32_t* ref_frames, int32_t capacity,
+                                 int32_t* n_results) {
+    if (n_results)
+        *n_results = 0;
+    std::vector<Shard> shards;
+    int rc = guarded([&] {
+        if (!devices || n_devices < 1)
+            fmvs::fail_input("sequence: no devices");
+        if (inflight < 1)
+            fmvs::fail_config("sequence: inflight must be at least 1");
+        if (!cfg)
+            fmvs::fail_config("estimate: null config");
+        // the CLI's checks, in its order (tools/fassmvs.cpp:93-135)
+        if (cfg->bundle_size < 3 || cfg->bundle_size % 2 == 0)
+            fmvs::fail_config("--bundle-size must be odd and at least 3");
+        if (stride < 1)
+            fmvs::fail_config("--stride must be at least 1");
+        if (filter < FMVS_FILTER_NONE || filter > FMVS_FILTER_BOTH)
+            fmvs::fail_config("--filter must be none, dog, geom or both");
+        fmvs::validate_config(*cfg);
+        for (int i = 0; i < n_frames; ++i)
+            fmvs::validate_view(frames[i]);
+        if (n_frames < cfg->bundle_size)
+            fmvs::fail_input("sequence shorter than one bundle");
+        SeqJob job{};
+        job.frames = frames;
+        job.n_frames = n_frames;
+        job.cfg = cfg;
+        job.filter = filter;
+        job.half = cfg->bundle_size / 2;
+        for (int r = job.half; r + job.half < n_frames; r += stride)
+            job.refs.push_back(r);
+        job.m = static_cast<int>(job.refs.size());
+        if (n_results)
+            *n_results = job.m;
+        if (job.m > capacity)
+            throw Error(FMVS_ERR_CAPACITY, "estimate_sequence: result capacity too small");
+        job.w = frames[0].intrinsics.width;
+        job.h = frames[0].intrinsics.height;
+        for (int i = 0; i < n_frames; ++i)
+            if (frames[i].intrinsics.width != job.w || frames[i].intrinsics.height != job.h)
+                fmvs::fail_input("estimate_sequence: frames must share one size");
+        fmvs_geom_filter_config_default(&job.gc);
+        job.ws = 0;
+        if (filter == FMVS_FILTER_GEOM || filter == FMVS_FILTER_BOTH) {
+            job.ws = std::min(5, job.m);
+            check_geom_window(job.ws, 0, job.gc);
+        }
+        job.depth = depth;
+        job.normals = normals_xyz;
+        job.conf = confidence;
+        const SeqPlan plan = plan_sequence(job.m, n_devices, job.ws);
+        shards.resize(n_devices);
+        for (int d = 0; d < n_devices; ++d) {
+            shards[d].device = devices[d];
+            shards[d].begin = plan.begin[d];
+            shards[d].end = plan.end[d];
+            shards[d].inflight = inflight;
+            shards[d].imports = plan.imports[d];
+            shards[d].exports = plan.exports[d];
+        }
+        // NVLink peer access between devices that exchange halos
+        for (int d = 0; d < n_devices; ++d)
+            for (int e = 0; e < n_devices; ++e) {
+                if (devices[d] == devices[e] || shards[d].imports.empty())
+                    continue;
+                int can = 0;
+                if (cudaDeviceCanAccessPeer(&can, devices[d], devices[e]) == cudaSuccess && can) {
+                    FMVS_CUDA_CHECK(cudaSetDevice(devices[d]));
+                    const cudaError_t pe = cudaDeviceEnablePeerAccess(devices[e], 0);
+                    if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+                        FMVS_CUDA_CHECK(pe);
+                    cudaGetLastError();
+                }
+            }
+        HaloBoard board;
+        std::vector<std::thread> threads;
+        for (int d = 0; d < n_devices; ++d)
+            threads.emplace_back([&, d] {
+                Shard& sh = shards[d];
+                sh.code = guarded([&] { run_shard(sh, job, board); });
+                if (sh.code != FMVS_OK) {
+                    sh.error = g_last_error;
+                    board.fail();
+                }
+            });
+        for (auto& t : threads)
+            t.join();
+        for (const Shard& sh : shards)
+            if (sh.code != FMVS_OK)
+                throw Error(sh.code, sh.error);
+        for (int r = 0; r < job.m; ++r)
+            ref_frames[r] = job.refs[r];
+    });
+    // every shard's streams are idle here (joined; on failure, synchronise
+    // before freeing: peers may still read exported buffers)
+    for (Shard& sh : shards) {
+        cudaSetDevice(sh.device);
+        cudaDeviceSynchronize();
+    }
+    for (Shard& sh : shards)
+        sh.release();
+    return rc;
+}
 }  // extern "C"
 
 // ------------------------------------------------ output stage (§8f) --

@@ -666,6 +666,54 @@ class Backend:
         return [FrameResult(int(refs[r]), BundleResult(depth[r], normals[r], conf[r]))
                 for r in range(nres.value)]
 
+    def estimate_sequence_multi(self, frames: Sequence[CalibratedView], config: PipelineConfig,
+                                devices: Sequence[int], stride: int = 1, filter: Filter = Filter.none,
+                                inflight: int = 3, pinned: bool = False) -> list:
+        """estimate_sequence sharded over `devices` (contiguous shards, halo
+        exchange for the geometric filter; fmvs_estimate_sequence_multi).
+        pinned=True hands the library pinned output buffers (direct D2H)."""
+        views, keep = _views_c(frames)
+        cfg = config.to_c()
+        n = len(frames)
+        h, w = (frames[0].image.shape if n else (1, 1))
+        half = max(config.bundle_size, 1) // 2
+        cap = max(1, (n - 2 * half + max(stride, 1) - 1) // max(stride, 1)) if n else 1
+        px = h * w
+        hbuf = None
+        if pinned:
+            hbuf = self.fn["host_alloc"](cap * px * 20)
+            base = np.ctypeslib.as_array(C.cast(hbuf, C.POINTER(C.c_float)), shape=(cap * px * 5,))
+            depth = base[:cap * px].reshape(cap, h, w)
+            normals = base[cap * px:4 * cap * px].reshape(cap, h, w, 3)
+            conf = base[4 * cap * px:].reshape(cap, h, w)
+        else:
+            depth = np.zeros((cap, h, w), np.float32)
+            normals = np.zeros((cap, h, w, 3), np.float32)
+            conf = np.zeros((cap, h, w), np.float32)
+        refs = np.zeros(cap, np.int32)
+        nres = C.c_int32(0)
+        devs = (C.c_int32 * len(devices))(*devices)
+        try:
+            self._check(self.fn["estimate_sequence_multi"](devs, len(devices), inflight, views, n, stride,
+                                                           C.byref(cfg), int(filter), _ptr(depth), _ptr(normals),
+                                                           _ptr(conf), _ptr(refs), cap, C.byref(nres)))
+            out = [FrameResult(int(refs[r]), BundleResult(depth[r].copy(), normals[r].copy(), conf[r].copy()))
+                   for r in range(nres.value)]
+        finally:
+            if hbuf:
+                self.fn["host_free"](hbuf)
+        del keep
+        return out
+
+    def sequence_plan(self, m: int, shards: int, shard: int, window: int) -> dict:
+        """Shard / halo plan of estimate_sequence_multi (host only)."""
+        b, e, ni, ne = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        imp = np.zeros(max(m, 1), np.int32)
+        exp = np.zeros(max(m, 1), np.int32)
+        self._check(self.fn["sequence_plan"](m, shards, shard, window, C.byref(b), C.byref(e), _ptr(imp),
+                                             C.byref(ni), _ptr(exp), C.byref(ne)))
+        return dict(begin=b.value, end=e.value, imports=imp[:ni.value].tolist(), exports=exp[:ne.value].tolist())
+
     # ------------------------------------------- output stage (§8f)
     def colorize_depth(self, depth: np.ndarray, lo: float, hi: float) -> np.ndarray:
         """colorize_depth (colorize.hpp:9): uint8 (h, w, 3) viridis."""

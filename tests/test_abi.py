@@ -36,6 +36,8 @@ def test_oracle_exports_the_same_entry_points(oracle):
             "fmvs_estimate_bundle_device", "fmvs_ctx_set_timing", "fmvs_ctx_stage_count",
             "fmvs_ctx_stage_name", "fmvs_ctx_stage_time", "fmvs_ctx_stage_reset",
             "fmvs_ctx_sweep_stats", "fmvs_current_device",
+            # the multi-GPU sequence engine is checked against ref_estimate_sequence
+            "fmvs_estimate_sequence_multi", "fmvs_sequence_plan",
             # the reference writer runs as oracle/_ref/pfm_tool (a subprocess)
             "fmvs_write_pfm"}
     missing = [n for n in declared() if n not in skip and not hasattr(oracle.lib, "ref_" + n[5:])]

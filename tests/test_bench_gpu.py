@@ -47,6 +47,19 @@ def test_bench_single_gpu_contract():
     assert d["roofline"]["peak"] > 0 and 0 <= d["roofline"]["frac"] < 1
 
 
+def test_bench_self_spawns_ranks():
+    """`python bench.py --gpus 2` with no launcher starts one rank per GPU
+    itself (here: two ranks sharing cuda:0 through the test hook)."""
+    env = dict(os.environ, FMVS_BENCH_SHARE_DEVICE="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--workload", "c1", "--steps", "3",
+                        "--warmup", "3", "--ring", "4"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["value"] > 0
+
+
 def test_bench_two_ranks_shared_device():
     env = dict(os.environ, FMVS_BENCH_SHARE_DEVICE="1")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
@@ -56,3 +69,4 @@ def test_bench_two_ranks_shared_device():
     assert r.returncode == 0, r.stderr[-3000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+

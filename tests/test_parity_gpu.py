@@ -345,6 +345,33 @@ def test_aggregate_dense_wide(b200, oracle, rng, group, variant, monkeypatch):
     assert_same(a.values, b.values, "aggregate")
 
 
+def test_aggregate_noncompact_layouts(b200, oracle, rng):
+    """The reference layout allows any per-pixel offsets (test_sgm.cpp:262-274
+    zeroes a count in place): holes, reversed pixel order and shared trailing
+    space are gathered into the compact device layout and scattered back."""
+    w, h, planes = 11, 7, 9
+    img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    intr = Intrinsics(20.0, 20.0, 5.0, 3.0, w, h)
+    cfg = SgmConfig(SgmVariant.Plane, 8, 50.0, True, 0.0, 8.0, 10.0, 2)
+    vol = _volume(planes, w, h, rng)
+    holes = vol.count.copy()
+    holes[rng.random(w * h) < 0.2] = 0
+    rev = np.zeros(w * h, np.uint64)
+    rev[::-1] = np.cumsum(vol.count[::-1], dtype=np.uint64) - vol.count[::-1].astype(np.uint64)
+    pad = np.concatenate([vol.costs, rng.integers(0, 300, 17).astype(np.uint16)])
+    cases = [(holes, vol.offset, vol.costs), (vol.count, rev, vol.costs[::-1].copy()),
+             (vol.count, vol.offset, pad)]
+    for count, offset, costs in cases:
+        v = CostVolume(w, h, vol.planes, 2, vol.first, count, offset, costs)
+        a = b200.aggregate(v, img, cfg, intr)
+        b = oracle.aggregate(v, img, cfg, intr)
+        assert_same(a.values, b.values, "aggregate")
+        assert_same(b200.wta(b), oracle.wta(b), "wta")
+        for dx, dy in ((1, 0), (2, -1)):
+            assert_same(b200.aggregate_single_path(v, img, cfg, intr, dx, dy).values,
+                        oracle.aggregate_single_path(v, img, cfg, intr, dx, dy).values, "single path")
+
+
 def test_aggregate_errors(b200, oracle, rng):
     vol = _volume(5, 6, 4, rng)
     img = np.zeros((4, 6), np.uint8)

@@ -140,6 +140,41 @@ def test_estimate_sequence_bitexact(b200, oracle, filt, stride, name, cfg):
         assert_same(ra.maps.confidence, rb.maps.confidence, f"confidence[{ra.frame}]")
 
 
+SHARDINGS = [([0, 0], 3, False), ([0, 0, 0], 1, True), ([0, 0, 0, 0, 0], 2, False)]
+
+
+@pytest.mark.parametrize("filt", [Filter.none, Filter.dog, Filter.geom, Filter.both])
+@pytest.mark.parametrize("devices,inflight,pinned", SHARDINGS, ids=["2x3", "3x1-pinned", "5x2"])
+def test_estimate_sequence_multi_bitexact(b200, oracle, filt, devices, inflight, pinned):
+    """fmvs_estimate_sequence_multi with several shards on one GPU (the
+    cross-shard halo goes through the same cudaMemcpyPeerAsync path as on
+    NVLink) reproduces the reference CLI loop bit for bit, including the
+    geometric filter's windows that straddle shard boundaries; 5 shards of
+    1-2 results make every result a halo export."""
+    frames, _, _ = render(oracle, "slanted", 96, 64, tilt=30.0, views=13, step=0.35, texture=0.3)
+    c = config(**SEQ_CFGS[0][1])
+    a = b200.estimate_sequence_multi(frames, c, devices, 1, filt, inflight=inflight, pinned=pinned)
+    b = oracle.estimate_sequence(frames, c, 1, filt)
+    assert [r.frame for r in a] == [r.frame for r in b]
+    for ra, rb in zip(a, b):
+        assert_same(ra.maps.depth, rb.maps.depth, f"depth[{ra.frame}]")
+        assert_same(ra.maps.normals, rb.maps.normals, f"normals[{ra.frame}]")
+        assert_same(ra.maps.confidence, rb.maps.confidence, f"confidence[{ra.frame}]")
+
+
+def test_estimate_sequence_multi_errors(b200):
+    frames, _, _ = render(b200, "fronto", 48, 40, views=6, step=0.3)
+    c = config(8.0, 12.0, levels=1, cost="census5", max_planes=32)
+    with pytest.raises(ConfigError):
+        b200.estimate_sequence_multi(frames, c, [0, 0], 0)
+    with pytest.raises(InvalidInputError):
+        b200.estimate_sequence_multi(frames[:4], c, [0], 1)
+    with pytest.raises(ConfigError):
+        b200.estimate_sequence_multi(frames, c, [0, 0], 1, Filter.geom)
+    with pytest.raises(ConfigError):
+        b200.estimate_sequence_multi(frames, c, [0], 1, inflight=0)
+
+
 def test_estimate_sequence_errors(b200, oracle):
     frames, _, _ = render(oracle, "fronto", 48, 40, views=6, step=0.3)
     c = config(8.0, 12.0, levels=1, cost="census5", max_planes=32)
