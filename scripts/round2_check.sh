@@ -1,0 +1,7 @@
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+nproc
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -3 gpurun_out/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=25 > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+tail -60 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+cat gpurun_out/bench.json; tail -20 gpurun_out/bench.err
