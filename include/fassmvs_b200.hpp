@@ -28,7 +28,9 @@
 #include <string>
 #include <vector>
 
+#include "fassmvs/colorize.hpp"
 #include "fassmvs/errors.hpp"
+#include "fassmvs/map_io.hpp"
 #include "fassmvs/matching.hpp"
 #include "fassmvs/pipeline.hpp"
 #include "fassmvs/postfilter.hpp"
@@ -595,6 +597,46 @@ inline fassmvs::TextureMask geometric_consistency_mask(
     return keep;
 }
 
+// Output stage of the CLI (colorize.hpp:9-15, map_io.hpp:25-27).
+inline fassmvs::RgbImage rgb_image(const std::vector<std::uint8_t>& rgb, int w, int h) {
+    fassmvs::RgbImage img(w, h);
+    for (size_t i = 0; i < img.size(); ++i)
+        img.data()[i] = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+    return img;
+}
+inline fassmvs::RgbImage colorize_depth(const fassmvs::DepthMap& map, double lo, double hi,
+                                        Context& ctx = Context::thread_default()) {
+    std::vector<std::uint8_t> rgb(3 * map.size());
+    check(fmvs_colorize_depth(ctx.get(), map.data(), map.width(), map.height(), lo, hi, rgb.data()));
+    return rgb_image(rgb, map.width(), map.height());
+}
+inline fassmvs::RgbImage colorize_normals(const fassmvs::NormalMap& map, Context& ctx = Context::thread_default()) {
+    const std::vector<float> xyz = normals_xyz(map);
+    std::vector<std::uint8_t> rgb(3 * map.size());
+    check(fmvs_colorize_normals(ctx.get(), xyz.data(), map.width(), map.height(), rgb.data()));
+    return rgb_image(rgb, map.width(), map.height());
+}
+inline fassmvs::RgbImage colorize_confidence(const fassmvs::ConfidenceMap& map,
+                                             Context& ctx = Context::thread_default()) {
+    std::vector<std::uint8_t> rgb(3 * map.size());
+    check(fmvs_colorize_confidence(ctx.get(), map.data(), map.width(), map.height(), rgb.data()));
+    return rgb_image(rgb, map.width(), map.height());
+}
+inline void write_pfm(const std::string& path, const fassmvs::DepthMap& map) {
+    check(fmvs_write_pfm(path.c_str(), map.data(), map.width(), map.height(), 1));
+}
+inline void write_pfm(const std::string& path, const fassmvs::NormalMap& map) {
+    const std::vector<float> xyz = normals_xyz(map);
+    check(fmvs_write_pfm(path.c_str(), xyz.data(), map.width(), map.height(), 3));
+}
+inline void write_png(const std::string& path, const fassmvs::RgbImage& image) {
+    std::vector<std::uint8_t> rgb(3 * image.size());
+    for (size_t i = 0; i < image.size(); ++i)
+        for (int c = 0; c < 3; ++c)
+            rgb[3 * i + c] = image.data()[i][c];
+    check(fmvs_write_png(path.c_str(), rgb.data(), image.width(), image.height()));
+}
+
 }  // namespace fassmvs_b200
 
 #ifdef FASSMVS_B200_DEFINE_ESTIMATE_BUNDLE
@@ -720,5 +762,21 @@ std::vector<double> plane_distances(const Intrinsics& ref_intr, const Pose& ref_
 double depth_from_plane(const Eigen::Vector2d& pixel, const SweepPlane& plane, const Intrinsics& intr) {
     return fassmvs_b200::depth_from_plane(pixel, plane, intr);
 }
+}  // namespace fassmvs
+#endif
+
+#ifdef FASSMVS_B200_DEFINE_OUTPUT
+namespace fassmvs {
+// The CLI's output stage (colorize.hpp:9-15, map_io.hpp:25-27) served by the
+// B200 library (colorize.cpp / map_io.cpp compiled with each name renamed
+// <name>_cpu, oracle/Makefile).
+RgbImage colorize_depth(const DepthMap& map, double lo, double hi) {
+    return fassmvs_b200::colorize_depth(map, lo, hi);
+}
+RgbImage colorize_normals(const NormalMap& map) { return fassmvs_b200::colorize_normals(map); }
+RgbImage colorize_confidence(const ConfidenceMap& map) { return fassmvs_b200::colorize_confidence(map); }
+void write_pfm(const std::string& path, const DepthMap& map) { fassmvs_b200::write_pfm(path, map); }
+void write_pfm(const std::string& path, const NormalMap& map) { fassmvs_b200::write_pfm(path, map); }
+void write_png(const std::string& path, const RgbImage& image) { fassmvs_b200::write_png(path, image); }
 }  // namespace fassmvs
 #endif

@@ -297,6 +297,24 @@ int fmvs_render_plane_scene(fmvs_ctx* ctx, int32_t kind, int32_t width, int32_t 
                             uint8_t* images, float* gt_depth, float* gt_normals_xyz,
                             fmvs_intrinsics* intr, fmvs_pose* poses);
 
+/* render_scene (render.hpp:12-48, render.cpp:52-141) on the device for any
+ * SyntheticScene: planes (ScenePlane: point, normal, u_axis, half extents;
+ * +inf = unbounded), one view per pose, texture 0 = checkerboard, 1 = value
+ * noise. Each pixel's ray takes the nearest plane hit inside its extents;
+ * outputs as fmvs_render_plane_scene (images n_poses*width*height bytes;
+ * gt_depth / gt_normals_xyz may be NULL). Errors as the reference:
+ * intrinsics, empty planes/poses, texture scale, then each pose in order. */
+typedef struct fmvs_scene_plane {
+    double point[3], normal[3], u_axis[3];
+    double extent_u, extent_v;
+} fmvs_scene_plane;
+#define FMVS_TEXTURE_CHECKERBOARD 0
+#define FMVS_TEXTURE_VALUE_NOISE 1
+int fmvs_render_scene(fmvs_ctx* ctx, const fmvs_scene_plane* planes, int32_t n_planes,
+                      const fmvs_pose* poses, int32_t n_poses, const fmvs_intrinsics* intrinsics,
+                      int32_t texture, double texture_scale, uint64_t seed, uint8_t* images,
+                      float* gt_depth, float* gt_normals_xyz);
+
 /* ------------------------------------------ post-filters -- */
 /* dog_mask (postfilter.hpp:13-18, postfilter.cpp:67-79): out = width*height
  * bytes, 1 = textured (keep). */
@@ -390,6 +408,12 @@ int fmvs_colorize_confidence(fmvs_ctx* ctx, const float* confidence, int32_t wid
  * file cannot be written. */
 int fmvs_write_pfm(const char* path, const float* data, int32_t width, int32_t height,
                    int32_t channels);
+/* write_png (map_io.hpp:27, map_io.cpp:203-260): 8-bit RGB, one IDAT chunk of
+ * the filter-0 scanlines deflated by zlib at level 6 (compress2), CRC-32 per
+ * chunk -- byte-identical to the reference with the same zlib.
+ * rgb = 3*width*height bytes, row-major (the output of fmvs_colorize_*).
+ * InvalidInputError if the file cannot be written or compression fails. */
+int fmvs_write_png(const char* path, const uint8_t* rgb, int32_t width, int32_t height);
 
 /* --------------------------------------- accuracy scoring -- */
 /* L1Result + AccCplF (evaluation.hpp:11-30). */

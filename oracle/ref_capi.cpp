@@ -658,6 +658,39 @@ int ref_render_plane_scene(void*, int32_t kind, int32_t w, int32_t h, double foc
     });
 }
 
+// render_scene (render.hpp:41-48) for an arbitrary SyntheticScene.
+int ref_render_scene(void*, const fmvs_scene_plane* planes, int32_t n_planes, const fmvs_pose* poses,
+                     int32_t n_poses, const fmvs_intrinsics* intr, int32_t texture, double texture_scale,
+                     uint64_t seed, uint8_t* images, float* gt_depth, float* gt_normals_xyz) {
+    return guard([&] {
+        SyntheticScene s;
+        for (int i = 0; i < n_planes; ++i) {
+            ScenePlane sp;
+            sp.point = Eigen::Vector3d(planes[i].point[0], planes[i].point[1], planes[i].point[2]);
+            sp.normal = Eigen::Vector3d(planes[i].normal[0], planes[i].normal[1], planes[i].normal[2]);
+            sp.u_axis = Eigen::Vector3d(planes[i].u_axis[0], planes[i].u_axis[1], planes[i].u_axis[2]);
+            sp.extent_u = planes[i].extent_u;
+            sp.extent_v = planes[i].extent_v;
+            s.planes.push_back(sp);
+        }
+        for (int i = 0; i < n_poses; ++i)
+            s.poses.push_back(to_pose(poses[i]));
+        s.intrinsics = to_intr(*intr);
+        s.texture = texture == FMVS_TEXTURE_CHECKERBOARD ? TextureKind::Checkerboard : TextureKind::ValueNoise;
+        s.texture_scale = texture_scale;
+        s.seed = seed;
+        const std::vector<RenderedView> r = render_scene(s);
+        const std::size_t npx = static_cast<std::size_t>(intr->width) * intr->height;
+        for (int k = 0; k < n_poses; ++k) {
+            std::memcpy(images + k * npx, r[k].view.image.data(), npx);
+            if (gt_depth)
+                std::memcpy(gt_depth + k * npx, r[k].gt_depth.data(), 4 * npx);
+            if (gt_normals_xyz)
+                write_normals(r[k].gt_normals, gt_normals_xyz + 3 * k * npx);
+        }
+    });
+}
+
 // --- post-filters (postfilter.hpp) and the CLI estimate loop ------------
 
 

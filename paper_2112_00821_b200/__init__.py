@@ -10,12 +10,14 @@ from .fassmvs import (  # noqa: F401
     AggregatedVolume, Backend, BundleResult, CalibratedView, ConfigError, ConsistencyView,
     CostFunctionSpec, CostKind, CostVolume, CudaError, DepthLookup, Filter, FrameResult,
     GeomFilterConfig, GeometryError, Intrinsics, InvalidInputError, PipelineConfig, PlaneStack,
-    Pose, RangeKind, RangePolicy, SgmConfig, SgmVariant, default_backend, estimate_bundle)
+    Pose, RangeKind, RangePolicy, ScenePlane, SgmConfig, SgmVariant, SyntheticScene, TextureKind,
+    default_backend, estimate_bundle, lateral_trajectory)
 
 __all__ = [
     "AggregatedVolume", "Backend", "BundleResult", "CalibratedView", "ConfigError",
     "ConsistencyView", "CostFunctionSpec", "CostKind", "CostVolume", "CudaError", "DepthLookup",
     "Filter", "FrameResult", "GeomFilterConfig", "GeometryError", "Intrinsics",
     "InvalidInputError", "PipelineConfig", "PlaneStack", "Pose", "RangeKind", "RangePolicy",
-    "SgmConfig", "SgmVariant", "default_backend", "estimate_bundle",
+    "ScenePlane", "SgmConfig", "SgmVariant", "SyntheticScene", "TextureKind", "default_backend",
+    "estimate_bundle", "lateral_trajectory",
 ]

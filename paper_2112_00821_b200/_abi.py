@@ -25,6 +25,11 @@ class Pose_c(C.Structure):
     _fields_ = [("rotation", C.c_double * 9), ("center", C.c_double * 3)]
 
 
+class ScenePlane_c(C.Structure):
+    _fields_ = [("point", C.c_double * 3), ("normal", C.c_double * 3), ("u_axis", C.c_double * 3),
+                ("extent_u", C.c_double), ("extent_v", C.c_double)]
+
+
 class View_c(C.Structure):
     _fields_ = [("image", C.c_void_p), ("intrinsics", Intrinsics_c), ("pose", Pose_c)]
 
@@ -132,6 +137,8 @@ SIGNATURES = {
     "upscale_nearest": (C.c_int, [P, P, I32, I32, I32, I32, I32, P]),
     "render_plane_scene": (C.c_int, [P, I32, I32, I32, D, D, D, I32, D, U64, D, P, P, P,
                                      C.POINTER(Intrinsics_c), C.POINTER(Pose_c)]),
+    "render_scene": (C.c_int, [P, C.POINTER(ScenePlane_c), I32, C.POINTER(Pose_c), I32,
+                               C.POINTER(Intrinsics_c), I32, D, U64, P, P, P]),
     "dog_mask": (C.c_int, [P, P, I32, I32, P]),
     "apply_mask": (C.c_int, [P, P, P, P, I32, I32, P]),
     "geom_filter_config_default": (None, [C.POINTER(GeomFilterConfig_c)]),
@@ -147,6 +154,7 @@ SIGNATURES = {
     "colorize_normals": (C.c_int, [P, P, I32, I32, P]),
     "colorize_confidence": (C.c_int, [P, P, I32, I32, P]),
     "write_pfm": (C.c_int, [C.c_char_p, P, I32, I32, I32]),
+    "write_png": (C.c_int, [C.c_char_p, P, I32, I32]),
     "evaluate": (C.c_int, [P, P, P, I32, I32, PD, I32, C.POINTER(L1Result_c), C.POINTER(AccCplF_c)]),
     "roc_curve": (C.c_int, [P, P, P, P, I32, I32, D, PD, PD]),
     "gaussian_blur": (C.c_int, [P, P, I32, I32, I32, D, P]),

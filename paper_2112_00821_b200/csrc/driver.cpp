@@ -26,6 +26,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <zlib.h>
 
 #include "host.hpp"
 #include "kernels.hpp"
@@ -1574,81 +1575,103 @@ int fmvs_upscale_nearest(fmvs_ctx* ctx, const float* in, int32_t iw, int32_t ih,
     });
 }
 
-int fmvs_render_plane_scene(fmvs_ctx* ctx, int32_t kind, int32_t w, int32_t h, double focal,
-                            double depth, double tilt_deg, int32_t n_views, double step,
-                            uint64_t seed, double texture_scale, uint8_t* images, float* gt_depth,
-                            float* gt_normals_xyz, fmvs_intrinsics* intr, fmvs_pose* poses) {
+int fmvs_render_scene(fmvs_ctx* ctx, const fmvs_scene_plane* planes, int32_t n_planes,
+                      const fmvs_pose* poses, int32_t n_poses, const fmvs_intrinsics* intrinsics,
+                      int32_t texture, double texture_scale, uint64_t seed, uint8_t* images,
+                      float* gt_depth, float* gt_normals_xyz) {
     return guarded([&] {
         ctx->use();
-        // base_scene / fronto_scene / slanted_scene (render.cpp:143-183)
-        const fmvs_intrinsics k0{focal, focal, (w - 1) / 2.0, (h - 1) / 2.0, w, h};
+        // render_scene (render.cpp:52-141): validation in the reference's order
+        const fmvs_intrinsics k0 = *intrinsics;
         fmvs::validate_intrinsics(k0);
-        if (n_views < 1)
+        if (n_planes < 1 || n_poses < 1)
             fmvs::fail_input("render: scene needs at least one plane and one pose");
         if (!(texture_scale > 0.0))
             fmvs::fail_input("render: texture scale must be positive");
-        fmvs::V3 pn{0, 0, -1};
-        if (kind == 1) {
-            const double rad = tilt_deg * M_PI / 180.0;
-            pn = {0.0, -std::sin(rad), -std::cos(rad)};
+        if (texture != FMVS_TEXTURE_CHECKERBOARD && texture != FMVS_TEXTURE_VALUE_NOISE)
+            fmvs::fail_input("render: unknown texture kind");
+        // PlaneFrame (render.cpp:64-72): Eigen normalized() leaves a zero vector as is
+        auto normalized = [](fmvs::V3 v) {
+            const double n2 = fmvs::dot(v, v);
+            return n2 > 0.0 ? fmvs::divs(v, std::sqrt(n2)) : v;
+        };
+        std::vector<k::RenderPlane> frames(n_planes);
+        for (int i = 0; i < n_planes; ++i) {
+            const fmvs_scene_plane& sp = planes[i];
+            const fmvs::V3 fn = normalized(fmvs::V3{sp.normal[0], sp.normal[1], sp.normal[2]});
+            const fmvs::V3 u0{sp.u_axis[0], sp.u_axis[1], sp.u_axis[2]};
+            const fmvs::V3 fu = normalized(fmvs::sub(u0, fmvs::scale(fmvs::dot(u0, fn), fn)));
+            const fmvs::V3 fv = fmvs::cross(fn, fu);
+            k::RenderPlane& f = frames[i];
+            for (int c = 0; c < 3; ++c)
+                f.pt[c] = sp.point[c];
+            f.n[0] = fn.x, f.n[1] = fn.y, f.n[2] = fn.z;
+            f.u[0] = fu.x, f.u[1] = fu.y, f.u[2] = fu.z;
+            f.v[0] = fv.x, f.v[1] = fv.y, f.v[2] = fv.z;
+            f.ext_u = sp.extent_u;
+            f.ext_v = sp.extent_v;
         }
-        // PlaneFrame (render.cpp:64-72)
-        const double len = fmvs::norm(pn);
-        fmvs::V3 fn = pn;
-        if (fmvs::dot(pn, pn) > 0.0)
-            fn = fmvs::divs(pn, len);
-        const fmvs::V3 u0{1, 0, 0};
-        const fmvs::V3 ur = fmvs::sub(u0, fmvs::scale(fmvs::dot(u0, fn), fn));
-        fmvs::V3 fu = ur;
-        if (fmvs::dot(ur, ur) > 0.0)
-            fu = fmvs::divs(ur, fmvs::norm(ur));
-        const fmvs::V3 fv = fmvs::cross(fn, fu);
         cudaStream_t s = ctx->stream;
         Tmp t;
-        const size_t px = static_cast<size_t>(w) * h;
-        uint8_t* dimg = t.alloc<uint8_t>(px * n_views);
-        float* dd = gt_depth ? t.alloc<float>(px * n_views) : nullptr;
-        float* dn = gt_normals_xyz ? t.alloc<float>(3 * px * n_views) : nullptr;
-        for (int v = 0; v < n_views; ++v) {
-            fmvs_pose pose{};
-            pose.rotation[0] = pose.rotation[4] = pose.rotation[8] = 1.0;
-            pose.center[0] = (v - (n_views - 1) / 2.0) * step;  // lateral_trajectory
+        const size_t px = static_cast<size_t>(k0.width) * k0.height;
+        k::RenderPlane* dplanes = t.upload(frames.data(), frames.size(), s);
+        uint8_t* dimg = t.alloc<uint8_t>(px * n_poses);
+        float* dd = gt_depth ? t.alloc<float>(px * n_poses) : nullptr;
+        float* dn = gt_normals_xyz ? t.alloc<float>(3 * px * n_poses) : nullptr;
+        for (int v = 0; v < n_poses; ++v) {
+            fmvs::validate_pose(fmvs::camera_of(k0, poses[v]).rot);  // pose.validate() per view
             k::RenderArgs ra{};
-            ra.w = w;
-            ra.h = h;
+            ra.w = k0.width;
+            ra.h = k0.height;
             ra.intr = intr_of(k0);
-            std::memcpy(ra.rot, pose.rotation, sizeof(ra.rot));
-            std::memcpy(ra.center, pose.center, sizeof(ra.center));
-            ra.pn[0] = fn.x;
-            ra.pn[1] = fn.y;
-            ra.pn[2] = fn.z;
-            ra.pp[0] = 0;
-            ra.pp[1] = 0;
-            ra.pp[2] = depth;
-            ra.pu[0] = fu.x;
-            ra.pu[1] = fu.y;
-            ra.pu[2] = fu.z;
-            ra.pv[0] = fv.x;
-            ra.pv[1] = fv.y;
-            ra.pv[2] = fv.z;
+            std::memcpy(ra.rot, poses[v].rotation, sizeof(ra.rot));
+            std::memcpy(ra.center, poses[v].center, sizeof(ra.center));
+            ra.planes = dplanes;
+            ra.nplanes = n_planes;
+            ra.texture = texture;
             ra.texture_scale = texture_scale;
             ra.seed = seed;
             ra.image = dimg + v * px;
             ra.gt_depth = dd ? dd + v * px : nullptr;
             ra.gt_normals = dn ? dn + 3 * v * px : nullptr;
-            k::render_plane(ra, s);
-            if (intr)
-                intr[v] = k0;
-            if (poses)
-                poses[v] = pose;
+            k::render_view(ra, s);
         }
-        FMVS_CUDA_CHECK(cudaMemcpyAsync(images, dimg, px * n_views, cudaMemcpyDeviceToHost, s));
+        FMVS_CUDA_CHECK(cudaMemcpyAsync(images, dimg, px * n_poses, cudaMemcpyDeviceToHost, s));
         if (dd)
-            FMVS_CUDA_CHECK(cudaMemcpyAsync(gt_depth, dd, 4 * px * n_views, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(gt_depth, dd, 4 * px * n_poses, cudaMemcpyDeviceToHost, s));
         if (dn)
-            FMVS_CUDA_CHECK(cudaMemcpyAsync(gt_normals_xyz, dn, 12 * px * n_views, cudaMemcpyDeviceToHost, s));
+            FMVS_CUDA_CHECK(cudaMemcpyAsync(gt_normals_xyz, dn, 12 * px * n_poses, cudaMemcpyDeviceToHost, s));
         FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
     });
+}
+
+int fmvs_render_plane_scene(fmvs_ctx* ctx, int32_t kind, int32_t w, int32_t h, double focal,
+                            double depth, double tilt_deg, int32_t n_views, double step,
+                            uint64_t seed, double texture_scale, uint8_t* images, float* gt_depth,
+                            float* gt_normals_xyz, fmvs_intrinsics* intr, fmvs_pose* poses) {
+    // base_scene / fronto_scene / slanted_scene (render.cpp:143-183)
+    const fmvs_intrinsics k0{focal, focal, (w - 1) / 2.0, (h - 1) / 2.0, w, h};
+    const double inf = std::numeric_limits<double>::infinity();
+    fmvs_scene_plane plane{{0, 0, depth}, {0, 0, -1}, {1, 0, 0}, inf, inf};
+    if (kind == 1) {
+        const double rad = tilt_deg * M_PI / 180.0;
+        plane.normal[1] = -std::sin(rad);
+        plane.normal[2] = -std::cos(rad);
+        plane.normal[0] = 0.0;
+    }
+    std::vector<fmvs_pose> ps(n_views > 0 ? n_views : 0);
+    for (int v = 0; v < n_views; ++v) {
+        fmvs_pose pose{};
+        pose.rotation[0] = pose.rotation[4] = pose.rotation[8] = 1.0;
+        pose.center[0] = (v - (n_views - 1) / 2.0) * step;  // lateral_trajectory
+        ps[v] = pose;
+        if (intr)
+            intr[v] = k0;
+        if (poses)
+            poses[v] = pose;
+    }
+    return fmvs_render_scene(ctx, &plane, 1, ps.data(), n_views, &k0, FMVS_TEXTURE_VALUE_NOISE,
+                             texture_scale, seed, images, gt_depth, gt_normals_xyz);
 }
 
 }  // extern "C"
@@ -2489,6 +2512,62 @@ int fmvs_write_pfm(const char* path, const float* data, int32_t w, int32_t h, in
         ok = (std::fclose(f) == 0) && ok;
         if (!ok)
             fmvs::fail_input("short write on float map file");
+    });
+}
+
+// write_png (map_io.cpp:203-260): signature, IHDR (8-bit RGB), one IDAT of
+// the filter-0 scanlines deflated by compress2 at level 6, IEND; every chunk
+// is length (big endian), type, data, CRC-32 over type + data.
+int fmvs_write_png(const char* path, const uint8_t* rgb, int32_t w, int32_t h) {
+    return guarded([&] {
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f)
+            fmvs::fail_input(std::string("cannot open for writing: ") + path);  // map_io.cpp:20-25
+        std::vector<uint8_t> out;
+        auto be32 = [&](uint32_t v) {
+            const uint8_t b[4] = {uint8_t(v >> 24), uint8_t(v >> 16), uint8_t(v >> 8), uint8_t(v)};
+            out.insert(out.end(), b, b + 4);
+        };
+        auto chunk = [&](const char* type, const uint8_t* data, size_t n) {
+            be32(static_cast<uint32_t>(n));
+            out.insert(out.end(), type, type + 4);
+            if (n)
+                out.insert(out.end(), data, data + n);
+            uLong crc = crc32(0L, reinterpret_cast<const Bytef*>(type), 4);
+            if (n)
+                crc = crc32(crc, data, static_cast<uInt>(n));
+            be32(static_cast<uint32_t>(crc));
+        };
+        static const uint8_t sig[8] = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1a, '\n'};
+        out.insert(out.end(), sig, sig + 8);
+        uint8_t ihdr[13] = {0};
+        const uint32_t uw = static_cast<uint32_t>(w), uh = static_cast<uint32_t>(h);
+        for (int i = 0; i < 4; ++i) {
+            ihdr[i] = static_cast<uint8_t>(uw >> (24 - 8 * i));
+            ihdr[4 + i] = static_cast<uint8_t>(uh >> (24 - 8 * i));
+        }
+        ihdr[8] = 8;  // bit depth
+        ihdr[9] = 2;  // RGB
+        chunk("IHDR", ihdr, 13);
+        const size_t row = 3 * static_cast<size_t>(w > 0 ? w : 0);
+        std::vector<uint8_t> raw;
+        raw.reserve(static_cast<size_t>(h > 0 ? h : 0) * (1 + row));
+        for (int y = 0; y < h; ++y) {
+            raw.push_back(0);  // filter type 0 per scanline
+            raw.insert(raw.end(), rgb + static_cast<size_t>(y) * row, rgb + static_cast<size_t>(y + 1) * row);
+        }
+        uLongf bound = compressBound(static_cast<uLong>(raw.size()));
+        std::vector<uint8_t> z(bound);
+        if (compress2(z.data(), &bound, raw.data(), static_cast<uLong>(raw.size()), 6) != Z_OK) {
+            std::fclose(f);
+            fmvs::fail_input(std::string("png compression failed: ") + path);
+        }
+        chunk("IDAT", z.data(), bound);
+        chunk("IEND", nullptr, 0);
+        bool ok = std::fwrite(out.data(), 1, out.size(), f) == out.size();
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok)
+            fmvs::fail_input(std::string("short write: ") + path);
     });
 }
 

@@ -1,8 +1,9 @@
-// Synthetic input generator on the device: render_scene for a single
-// textured plane (render.cpp:52-141) with the fractal value-noise texture
-// (render.cpp:12-50). Used by bench.py to produce the BASELINE configs'
-// bundles at full resolution without a CPU bottleneck; parity with the
-// reference renderer is checked in tests/test_render.py.
+// Synthetic input generator on the device: render_scene (render.cpp:52-141)
+// for any set of textured planes with extents, checkerboard or fractal
+// value-noise texture (render.cpp:12-50). Used by bench.py to produce the
+// BASELINE configs' bundles at full resolution without a CPU bottleneck;
+// parity with the reference renderer: tests/test_fullsize_gpu.py
+// (test_render_fullsize) and tests/test_parity_gpu.py (test_render_*).
 #include "host.hpp"
 #include "kernels.hpp"
 
@@ -62,31 +63,54 @@ __global__ void render_kernel(RenderArgs a) {
     const D3 dir{add(add(mul(a.rot[0], ray.x), mul(a.rot[3], ray.y)), mul(a.rot[6], ray.z)),
                  add(add(mul(a.rot[1], ray.x), mul(a.rot[4], ray.y)), mul(a.rot[7], ray.z)),
                  add(add(mul(a.rot[2], ray.x), mul(a.rot[5], ray.y)), mul(a.rot[8], ray.z))};
-    const D3 n{a.pn[0], a.pn[1], a.pn[2]};
-    const D3 pt{a.pp[0], a.pp[1], a.pp[2]};
     const D3 c{a.center[0], a.center[1], a.center[2]};
+    // nearest plane hit inside its extents (render.cpp:85-110)
+    double best_t = __longlong_as_double(0x7FF0000000000000LL);  // +inf
+    int best = -1;
+    double best_u = 0.0, best_v = 0.0;
+    for (int pi = 0; pi < a.nplanes; ++pi) {
+        const RenderPlane& f = a.planes[pi];
+        const D3 n{f.n[0], f.n[1], f.n[2]};
+        const double denom = dot3(n, dir);
+        if (fabs(denom) < 1e-12)
+            continue;
+        const double t = div(dot3(n, sub3(D3{f.pt[0], f.pt[1], f.pt[2]}, c)), denom);
+        if (t <= 0.0 || t >= best_t)
+            continue;
+        const D3 hit = add3(c, scale3(t, dir));
+        const D3 rel = sub3(hit, D3{f.pt[0], f.pt[1], f.pt[2]});
+        const double pu = dot3(rel, D3{f.u[0], f.u[1], f.u[2]});
+        const double pv = dot3(rel, D3{f.v[0], f.v[1], f.v[2]});
+        if (fabs(pu) > f.ext_u || fabs(pv) > f.ext_v)
+            continue;
+        best_t = t;
+        best = pi;
+        best_u = pu;
+        best_v = pv;
+    }
     uint8_t pix = 0;
     float gd = 0.0f;
     float3 gn = make_float3(0.0f, 0.0f, 0.0f);
-    const double denom = dot3(n, dir);
-    if (!(fabs(denom) < 1e-12)) {
-        const double t = div(dot3(n, sub3(pt, c)), denom);
-        if (t > 0.0) {
-            const D3 hit = add3(c, scale3(t, dir));
-            const D3 rel = sub3(hit, pt);
-            const double pu = dot3(rel, D3{a.pu[0], a.pu[1], a.pu[2]});
-            const double pv = dot3(rel, D3{a.pv[0], a.pv[1], a.pv[2]});
-            const double val = value_noise(div(pu, a.texture_scale), div(pv, a.texture_scale), a.seed);
-            pix = static_cast<uint8_t>(lround(mul(255.0, val)));
-            gd = __double2float_rn(t);
-            // n_cam = R * n, camera-facing
-            D3 nc{add(add(mul(a.rot[0], n.x), mul(a.rot[1], n.y)), mul(a.rot[2], n.z)),
-                  add(add(mul(a.rot[3], n.x), mul(a.rot[4], n.y)), mul(a.rot[5], n.z)),
-                  add(add(mul(a.rot[6], n.x), mul(a.rot[7], n.y)), mul(a.rot[8], n.z))};
-            if (nc.z > 0.0)
-                nc = {-nc.x, -nc.y, -nc.z};
-            gn = make_float3(__double2float_rn(nc.x), __double2float_rn(nc.y), __double2float_rn(nc.z));
+    if (best >= 0) {
+        const double tu = div(best_u, a.texture_scale), tv = div(best_v, a.texture_scale);
+        double val;
+        if (a.texture == FMVS_TEXTURE_CHECKERBOARD) {  // render.cpp:118-121
+            const long long parity = static_cast<long long>(floor(tu)) + static_cast<long long>(floor(tv));
+            val = (parity & 1) ? 224.0 / 255.0 : 32.0 / 255.0;
+        } else {
+            val = value_noise(tu, tv, a.seed + 7919ull * static_cast<uint64_t>(best));
         }
+        pix = static_cast<uint8_t>(lround(mul(255.0, val)));
+        gd = __double2float_rn(best_t);
+        // n_cam = R * n, camera-facing
+        const RenderPlane& f = a.planes[best];
+        const D3 n{f.n[0], f.n[1], f.n[2]};
+        D3 nc{add(add(mul(a.rot[0], n.x), mul(a.rot[1], n.y)), mul(a.rot[2], n.z)),
+              add(add(mul(a.rot[3], n.x), mul(a.rot[4], n.y)), mul(a.rot[5], n.z)),
+              add(add(mul(a.rot[6], n.x), mul(a.rot[7], n.y)), mul(a.rot[8], n.z))};
+        if (nc.z > 0.0)
+            nc = {-nc.x, -nc.y, -nc.z};
+        gn = make_float3(__double2float_rn(nc.x), __double2float_rn(nc.y), __double2float_rn(nc.z));
     }
     a.image[p] = pix;
     if (a.gt_depth)
@@ -100,7 +124,7 @@ __global__ void render_kernel(RenderArgs a) {
 
 }  // namespace
 
-void render_plane(const RenderArgs& a, cudaStream_t s) {
+void render_view(const RenderArgs& a, cudaStream_t s) {
     render_kernel<<<dim3((a.w + 31) / 32, (a.h + 7) / 8), dim3(32, 8), 0, s>>>(a);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }

@@ -227,20 +227,26 @@ void roc_sort_prefix(const float* keys, float* keys_sorted, const uint8_t* pass,
                      int n, void* temp, size_t temp_bytes, const RocSteps& steps,
                      unsigned long long* prefix, cudaStream_t s);
 
-// ---- synthetic input: render_scene for one textured plane ------------------
+// ---- synthetic input: render_scene (any planes, both textures) -------------
+struct RenderPlane {
+    double pt[3], n[3], u[3], v[3];  // PlaneFrame (normalised on the host)
+    double ext_u, ext_v;
+};
 struct RenderArgs {
     int w, h;
     dev::Intr intr;
     double rot[9];                   // world -> camera rotation (row-major)
     double center[3];
-    double pn[3], pp[3], pu[3], pv[3];  // plane frame (normalised on the host)
+    const RenderPlane* planes;       // device array
+    int nplanes;
+    int texture;                     // FMVS_TEXTURE_*
     double texture_scale;
     uint64_t seed;
     uint8_t* image;
     float* gt_depth;
     float* gt_normals;
 };
-void render_plane(const RenderArgs& a, cudaStream_t s);
+void render_view(const RenderArgs& a, cudaStream_t s);
 
 }  // namespace k
 }  // namespace fmvs

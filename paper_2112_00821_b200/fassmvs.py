@@ -745,6 +745,13 @@ class Backend:
         ch = 1 if a.ndim == 2 else a.shape[2]
         self._check(self.fn["write_pfm"](path.encode(), _ptr(a), a.shape[1], a.shape[0], ch))
 
+    def write_png(self, path: str, rgb: np.ndarray) -> None:
+        """write_png (map_io.hpp:27): uint8 (h, w, 3) RGB, byte-identical to the reference."""
+        a = np.ascontiguousarray(rgb, np.uint8)
+        if a.ndim != 3 or a.shape[2] != 3:
+            raise ValueError("write_png: expected an (h, w, 3) uint8 image")
+        self._check(self.fn["write_png"](path.encode(), _ptr(a), a.shape[1], a.shape[0]))
+
     # -------------------------------------- remaining reference helpers
     def gaussian_blur(self, image: np.ndarray, radius: int, sigma: float) -> np.ndarray:
         """gaussian_blur (pipeline.hpp:54): float32 (h, w)."""
@@ -848,6 +855,62 @@ class Backend:
                   for i in range(views)]
         del px
         return bundle, gd, gn
+
+    def render_scene(self, scene: "SyntheticScene"):
+        """render_scene (render.hpp:41-48) of any SyntheticScene (planes with
+        extents, checkerboard or value-noise texture).
+
+        Returns (bundle, gt_depth[views,h,w], gt_normals[views,h,w,3])."""
+        n = len(scene.planes)
+        planes = (_abi.ScenePlane_c * max(n, 1))()
+        for i, sp in enumerate(scene.planes):
+            planes[i].point[:] = [float(v) for v in sp.point]
+            planes[i].normal[:] = [float(v) for v in sp.normal]
+            planes[i].u_axis[:] = [float(v) for v in sp.u_axis]
+            planes[i].extent_u = float(sp.extent_u)
+            planes[i].extent_v = float(sp.extent_v)
+        views = len(scene.poses)
+        poses = (_abi.Pose_c * max(views, 1))(*[p.to_c() for p in scene.poses])
+        k = scene.intrinsics
+        h, w = max(k.height, 0), max(k.width, 0)
+        imgs = np.zeros((views, h, w), np.uint8)
+        gd = np.zeros((views, h, w), np.float32)
+        gn = np.zeros((views, h, w, 3), np.float32)
+        intr = k.to_c()
+        self._check(self.fn["render_scene"](self.ctx, planes, n, poses, views, C.byref(intr),
+                                            int(scene.texture), float(scene.texture_scale),
+                                            int(scene.seed), _ptr(imgs), _ptr(gd), _ptr(gn)))
+        bundle = [CalibratedView(imgs[i].copy(), k, scene.poses[i]) for i in range(views)]
+        return bundle, gd, gn
+
+
+class TextureKind(enum.IntEnum):  # render.hpp:12
+    Checkerboard = 0
+    ValueNoise = 1
+
+
+@dataclass
+class ScenePlane:  # render.hpp:16-22
+    point: Sequence[float] = (0.0, 0.0, 0.0)
+    normal: Sequence[float] = (0.0, 0.0, -1.0)
+    u_axis: Sequence[float] = (1.0, 0.0, 0.0)
+    extent_u: float = float("inf")
+    extent_v: float = float("inf")
+
+
+@dataclass
+class SyntheticScene:  # render.hpp:24-31
+    planes: list
+    poses: list
+    intrinsics: "Intrinsics"
+    texture: TextureKind = TextureKind.ValueNoise
+    texture_scale: float = 0.5
+    seed: int = 1
+
+
+def lateral_trajectory(views: int, step: float) -> list:
+    """lateral_trajectory (render.cpp:143-148)."""
+    return [Pose(np.eye(3), np.array([(i - (views - 1) / 2.0) * step, 0.0, 0.0])) for i in range(views)]
 
 
 def default_backend() -> Backend:

@@ -38,8 +38,8 @@ def test_oracle_exports_the_same_entry_points(oracle):
             "fmvs_ctx_sweep_stats", "fmvs_current_device",
             # the multi-GPU sequence engine is checked against ref_estimate_sequence
             "fmvs_estimate_sequence_multi", "fmvs_sequence_plan",
-            # the reference writer runs as oracle/_ref/pfm_tool (a subprocess)
-            "fmvs_write_pfm"}
+            # the reference writers run as oracle/_ref/{pfm,png}_tool (subprocesses)
+            "fmvs_write_pfm", "fmvs_write_png"}
     missing = [n for n in declared() if n not in skip and not hasattr(oracle.lib, "ref_" + n[5:])]
     assert not missing, missing
 

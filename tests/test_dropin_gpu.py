@@ -3,7 +3,9 @@ linked so that fassmvs::estimate_bundle, every stage-level function of the
 reference API (build_pyramids, gaussian_blur, upscale_nearest, refine_range,
 median_filter_5x5, census_transform, sweep_cost_volume, aggregate,
 aggregate_single_path, wta, compute_normal_offsets, normals_from_depth,
-smooth_normals, confidence_map, the host geometry) and the post-filters are
+smooth_normals, confidence_map, the host geometry), the post-filters and the
+CLI's output stage (colorize_*, write_pfm, write_png; test_io.cpp:32-66,168-181,
+240-270) are
 served by the B200 library through include/fassmvs_b200.hpp (oracle/Makefile
 target `dropin`), pass on the GPU, and the acceptance run prints exactly the
 golden numbers of proj/test_output.txt:13-22 (the B200 path is bit-exact with
@@ -35,11 +37,14 @@ DROPIN_SYMBOLS = ["estimate_bundle", "build_pyramids", "gaussian_blur", "upscale
                   "median_filter_5x5", "census_transform", "sweep_cost_volume", "aggregate",
                   "aggregate_single_path", "wta", "compute_normal_offsets", "normals_from_depth",
                   "smooth_normals", "confidence_map", "plane_distances", "plane_homography", "dog_mask",
-                  "geometric_consistency_mask"]
+                  "geometric_consistency_mask", "colorize_depth", "colorize_normals", "colorize_confidence",
+                  "write_pfm", "write_png"]
 C_ABI = ["fmvs_estimate_bundle", "fmvs_build_pyramids", "fmvs_sweep_cost_volume", "fmvs_aggregate",
          "fmvs_aggregate_single_path", "fmvs_wta", "fmvs_compute_normal_offsets", "fmvs_median_filter_5x5",
          "fmvs_normals_from_depth", "fmvs_smooth_normals", "fmvs_confidence_map", "fmvs_refine_range",
-         "fmvs_upscale_nearest", "fmvs_gaussian_blur", "fmvs_census_transform", "fmvs_plane_distances"]
+         "fmvs_upscale_nearest", "fmvs_gaussian_blur", "fmvs_census_transform", "fmvs_plane_distances",
+         "fmvs_colorize_depth", "fmvs_colorize_normals", "fmvs_colorize_confidence", "fmvs_write_pfm",
+         "fmvs_write_png"]
 
 
 @pytest.mark.parametrize("name", ["unit_tests_b200", "acceptance_b200"])

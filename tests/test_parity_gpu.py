@@ -38,6 +38,69 @@ def test_render_matches_reference(b200, oracle):
         assert_same(na, nb, "gt normals")
 
 
+def _scenes():
+    """SyntheticScenes beyond a single unbounded plane (render.cpp:52-141):
+    several planes with extents (nearest hit, misses), checkerboard texture,
+    rotated cameras, oblique u axes, a plane seen edge-on, zero-size extents."""
+    from paper_2112_00821_b200 import Intrinsics, Pose, ScenePlane, SyntheticScene, TextureKind
+    from paper_2112_00821_b200 import lateral_trajectory
+
+    def rot(ax, deg):
+        c, s_ = np.cos(np.radians(deg)), np.sin(np.radians(deg))
+        if ax == "y":
+            return np.array([[c, 0, s_], [0, 1, 0], [-s_, 0, c]])
+        return np.array([[1, 0, 0], [0, c, -s_], [0, s_, c]])
+
+    k = Intrinsics(110.0, 104.0, 63.5, 41.0, 128, 83)
+    boxes = [ScenePlane((0, 0, 9.0), (0, 0, -1), (1, 0, 0), 4.0, 2.5),
+             ScenePlane((0.5, -0.3, 6.0), (0.2, 0.1, -1.0), (1, 1, 0), 1.5, 0.8),
+             ScenePlane((-1.2, 0.6, 5.0), (0, -0.5, -1.0), (1, 0, 0.3), 0.7, 1.1),
+             ScenePlane((0.0, 1.5, 7.0), (0, 1, 0), (1, 0, 0), 3.0, 3.0),  # seen edge-on / from below
+             ScenePlane((2.0, 0.0, 4.0), (0, 0, -1), (0, 1, 0), 0.0, 0.5)]  # zero-width strip
+    poses = lateral_trajectory(3, 0.4) + [Pose(rot("y", 7.0), np.array([0.3, -0.2, 0.5])),
+                                          Pose(rot("x", -5.0) @ rot("y", -4.0), np.array([-0.6, 0.1, -1.0]))]
+    yield "boxes_noise", SyntheticScene(boxes, poses, k, TextureKind.ValueNoise, 0.23, 5)
+    yield "boxes_checker", SyntheticScene(boxes, poses, k, TextureKind.Checkerboard, 0.31, 1)
+    yield "plane_checker", SyntheticScene([ScenePlane((0, 0, 10.0), (0, -0.5, -0.866))],
+                                          lateral_trajectory(5, 0.59), Intrinsics(96.0, 96.0, 47.5, 31.5, 96, 64),
+                                          TextureKind.Checkerboard, 0.1, 1)
+    yield "behind", SyntheticScene([ScenePlane((0, 0, -3.0), (0, 0, 1))], lateral_trajectory(2, 1.0), k,
+                                   TextureKind.ValueNoise, 0.5, 2)
+
+
+@pytest.mark.parametrize("name", ["boxes_noise", "boxes_checker", "plane_checker", "behind"])
+def test_render_scene_matches_reference(b200, oracle, name):
+    scene = dict(_scenes())[name]
+    a, ga, na = b200.render_scene(scene)
+    b, gb, nb = oracle.render_scene(scene)
+    for va, vb in zip(a, b):
+        assert_same(va.image, vb.image, "image")
+    assert_same(ga, gb, "gt depth")
+    assert_same(na, nb, "gt normals")
+    if name.startswith("boxes"):
+        assert len(np.unique(a[0].image)) > 1 and (ga[0] == 0).any() and (ga[0] > 0).any()
+
+
+def test_render_scene_errors_match(b200, oracle):
+    from paper_2112_00821_b200 import Intrinsics, Pose, ScenePlane, SyntheticScene
+    from paper_2112_00821_b200 import lateral_trajectory
+    k = Intrinsics(50.0, 50.0, 15.5, 11.5, 32, 24)
+    cases = [SyntheticScene([], lateral_trajectory(2, 0.5), k),
+             SyntheticScene([ScenePlane()], [], k),
+             SyntheticScene([ScenePlane()], lateral_trajectory(2, 0.5), Intrinsics(0.0, 50.0, 1, 1, 32, 24)),
+             SyntheticScene([ScenePlane()], lateral_trajectory(2, 0.5), k, texture_scale=0.0),
+             SyntheticScene([ScenePlane()], [Pose(), Pose(np.diag([1.0, 1.0, -1.0]))], k)]
+    for scene in cases:
+        errs = []
+        for backend in (b200, oracle):
+            try:
+                backend.render_scene(scene)
+                errs.append(None)
+            except Exception as e:  # noqa: BLE001
+                errs.append(type(e))
+        assert errs[0] is not None and errs[0] == errs[1], errs
+
+
 # ------------------------------------------------------------- stages ----
 def test_build_pyramids(b200, oracle):
     bundle, _, _ = render(oracle, "slanted", 97, 61, tilt=20.0)
