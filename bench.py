@@ -174,9 +174,11 @@ def alg_bytes(stage, stats, n_views, paths, sn=False):
     ent = [lv["entries"] for lv in stats]
     tail = range(L) if sn else [0]   # levels that compute normals (SN needs them as priors)
     if stage == "sweep_l0":
-        return ent[0] * (2 + 4) + px[0] * (8 + n_views)   # u16 cost + zeroed u32 aggregate
+        return ent[0] * 2 + px[0] * (8 + n_views)   # u16 cost per hypothesis
     if stage == "sweep":
-        return sum(ent[l] * 6 + px[l] * (8 + n_views) for l in range(1, L))
+        return sum(ent[l] * 2 + px[l] * (8 + n_views) for l in range(1, L))
+    if stage == "zero":         # the u32 SGM accumulator of every level, zeroed
+        return sum(ent[l] * 4 for l in range(L))
     if stage == "sgm_l0":
         return ent[0] * (2 * paths + 4) + px[0] * paths * 9
     if stage == "sgm":
@@ -242,8 +244,8 @@ def roofline_entry(stage, st, peak, peak_src, workload):
                 "sm__warps_active.avg.pct_of_peak_sustained_active", 0.0)) / 100, 4),
             "source": f"ncu --set full capture ({src})"}
     if stage.startswith("sweep"):
-        e["note"] = ("achieved = algorithmic bytes (2 B cost + 4 B zeroed aggregate per hypothesis "
-                     "+ 8 B meta + 1 B per view per pixel) / CUDA-event launch time; the sweep is "
+        e["note"] = ("achieved = algorithmic bytes (2 B cost per hypothesis + 8 B meta + 1 B per view "
+                     "per pixel) / CUDA-event launch time; the sweep is "
                      "ALU-issue-bound (certified FP32/integer matching + FP64 tie fallback), not "
                      "HBM-bound: see DESIGN.md section 5")
     else:

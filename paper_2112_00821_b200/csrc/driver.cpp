@@ -573,7 +573,6 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         sa.meta = meta;
         sa.row_base = rb;
         sa.costs = costs;
-        sa.agg_zero = agg;
         sa.kind = cfg.cost.kind;
         sa.ww = cfg.cost.window_w;
         sa.wh = cfg.cost.window_h;
@@ -584,6 +583,9 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         if (ctx->sweep_stats)
             sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(8);
         ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { launches += k::sweep(sa, s); });
+        // the SGM accumulator of the level (make_accumulator, sgm.cpp:198-208)
+        ctx->timed("zero", [&] { k::zero_entries(agg, rb + P.h, s); });
+        ++launches;
 
         int variant = cfg.sgm.variant;
         if (variant == FMVS_SGM_SURFACE_NORMAL && !have_prior)

@@ -172,6 +172,25 @@ void range_rows(const RangeArgs& a, cudaStream_t s) {
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 
+// agg[0 .. *count) = 0 with contiguous 16-byte stores; the entry count is read
+// on the device (row_base[h] of the level), so no host synchronisation.
+__global__ void zero_entries_kernel(uint32_t* __restrict__ agg, const uint64_t* __restrict__ count) {
+    const uint64_t n = *count;
+    const uint64_t n4 = n / 4;
+    uint4* a4 = reinterpret_cast<uint4*>(agg);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride)
+        a4[i] = make_uint4(0u, 0u, 0u, 0u);
+    const uint64_t r = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n)
+        agg[r] = 0u;
+}
+
+void zero_entries(uint32_t* agg, const uint64_t* count, cudaStream_t s) {
+    zero_entries_kernel<<<148 * 4, 512, 0, s>>>(agg, count);
+    FMVS_CUDA_CHECK(cudaGetLastError());
+}
+
 void scan_rows(const uint32_t* row_total, int h, uint64_t* row_base, cudaStream_t s) {
     scan_rows_kernel<<<1, 1024, 0, s>>>(row_total, h, row_base);
     FMVS_CUDA_CHECK(cudaGetLastError());

@@ -271,8 +271,6 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
         }
         const uint64_t o = base + s_rel[j] + (e - s_prefix[j]);
         a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
-        if (a.agg_zero)
-            a.agg_zero[o] = 0u;
     }
     __syncthreads();  // the segment's shared state is rewritten next iteration
     }
@@ -530,6 +528,39 @@ __device__ __forceinline__ int bit_to_pos(int bi) {
 constexpr int kItemCap = 1024;
 constexpr int kPlaneChunk = 16;  // tile parameters computed for this many planes at once
 
+// Dense levels (plane slicing): a CTA sweeps the same planes for all its
+// pixels, one plane at a time, so direct u16 stores hit each pixel's run in a
+// different sector per plane (C3: 3.3x the algorithmic DRAM bytes from
+// partially written sectors evicted before completion). Each thread instead
+// stages its pixel's costs of kRun consecutive planes in shared memory (its
+// own row, stride chosen for conflict-free u16 stores) and writes them as one
+// 32-byte run -- two 16-byte stores when the run is full and aligned.
+// Census kernels stage 16 planes (32-byte runs); the NCC kernel 8 (16-byte
+// runs: its shared memory would otherwise drop it from 4 to 3 CTAs per SM).
+// Row stride kRun + 2 u16: an odd number of words, so the u16 stores of a
+// warp's 32 threads hit distinct banks.
+constexpr int kRun = 16, kRunNcc = 8;
+
+// Writes the staged costs of planes [c0, p] that lie in the pixel's range.
+template <int RUN>
+__device__ __forceinline__ void flush_run(uint16_t* __restrict__ costs, const uint16_t* run, int c0, int p,
+                                          int first, int count, uint64_t base) {
+    const int lo = max(c0, first), hi = min(p, first + count - 1);
+    if (lo > hi)
+        return;
+    const uint64_t o = base + static_cast<uint64_t>(lo - first);
+    if (hi - lo + 1 == RUN && (o & 7) == 0) {
+        const uint32_t* r = reinterpret_cast<const uint32_t*>(run);  // lo == c0: the whole row
+        uint4* dst = reinterpret_cast<uint4*>(costs + o);
+#pragma unroll
+        for (int q = 0; q < RUN / 8; ++q)
+            dst[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    } else {
+        for (int q = lo; q <= hi; ++q)
+            costs[base + static_cast<uint64_t>(q - first)] = run[q - c0];
+    }
+}
+
 struct ViewConst {
     const uint32_t* quad;
     const double* homs;  // homs of this view, plane 0
@@ -737,6 +768,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
     __shared__ uint32_t s_items[kItemCap];  // (thread, view, window position)
     __shared__ double s_vals[kItemCap];     // their exact FP64 samples
     __shared__ uint16_t s_lut[WW * WH];     // census cost LUT (popcount -> cost)
+    __shared__ __align__(16) uint16_t s_run[kTiledThreads * (kRun + 2)];  // dense levels: staged runs
 
     const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
@@ -1070,11 +1102,15 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                 else
                     sum_r += cost;
             }
-            const uint64_t o = base + static_cast<uint64_t>(p - first);
-            a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
-            if (a.agg_zero)
-                a.agg_zero[o] = 0u;
+            const uint16_t v = static_cast<uint16_t>(min(sum_l, sum_r));
+            if (a.plane_slicing)
+                s_run[threadIdx.x * (kRun + 2) + (p - pmin) % kRun] = v;
+            else
+                a.costs[base + static_cast<uint64_t>(p - first)] = v;
         }
+        if (a.plane_slicing && ((p - pmin) % kRun == kRun - 1 || p == pmax))
+            flush_run<kRun>(a.costs, s_run + threadIdx.x * (kRun + 2), p - (p - pmin) % kRun, p, first, count,
+                            base);
     }
 }
 
@@ -1192,6 +1228,9 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
     // of each tile sample as a window centre (general tiles only)
     int16_t* s_cost = reinterpret_cast<int16_t*>(s_F + NM * SN);  // [NM][kTiledThreads]
     uint8_t* s_in = reinterpret_cast<uint8_t*>(s_cost + NM * kTiledThreads);
+    // dense levels: staged runs (after the inside flags, 16-byte aligned)
+    uint16_t* s_run = reinterpret_cast<uint16_t*>(
+        (reinterpret_cast<uintptr_t>(s_in + NM * SN) + 15) & ~static_cast<uintptr_t>(15));
     __shared__ int s_ref[SN];  // edge-clamped reference tile + halo (u8 values)
     __shared__ TileParams64 s_tp[kPlaneChunk][NM];
     __shared__ ViewConst s_vc[NM];
@@ -1532,18 +1571,23 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
                 else
                     sum_r += c;
             }
-            const uint64_t o = base + static_cast<uint64_t>(p - first);
-            a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
-            if (a.agg_zero)
-                a.agg_zero[o] = 0u;
+            const uint16_t v = static_cast<uint16_t>(min(sum_l, sum_r));
+            if (a.plane_slicing)
+                s_run[threadIdx.x * (kRunNcc + 2) + (p - pmin) % kRunNcc] = v;
+            else
+                a.costs[base + static_cast<uint64_t>(p - first)] = v;
         }
+        if (a.plane_slicing && ((p - pmin) % kRunNcc == kRunNcc - 1 || p == pmax))
+            flush_run<kRunNcc>(a.costs, s_run + threadIdx.x * (kRunNcc + 2), p - (p - pmin) % kRunNcc, p, first,
+                               count, base);
     }
 }
 
 template <int WW, int WH, int NM>
 void launch_ncc_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
     const size_t smem = (sizeof(int) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1) +
-                        sizeof(int16_t) * NM * kTiledThreads;
+                        sizeof(int16_t) * NM * kTiledThreads + 16 +
+                        (a.plane_slicing ? sizeof(uint16_t) * kTiledThreads * (kRunNcc + 2) : 0);
     FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_ncc_tiled<WW, WH, NM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));

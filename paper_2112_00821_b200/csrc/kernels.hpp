@@ -62,6 +62,9 @@ struct RangeArgs {
 void range_rows(const RangeArgs& a, cudaStream_t s);
 // row_base[y] = sum of row_total[0..y), row_base[H] = total entries.
 void scan_rows(const uint32_t* row_total, int h, uint64_t* row_base, cudaStream_t s);
+// agg[0 .. *count) = 0 (the SGM accumulator of a level; count on the device,
+// 16-byte aligned agg).
+void zero_entries(uint32_t* agg, const uint64_t* count, cudaStream_t s);
 
 // ---- K4: plane-sweep cost volume (matching.cpp:116-294) ------------------
 struct SweepArgs {
@@ -76,14 +79,15 @@ struct SweepArgs {
     const dev::VolMeta* meta;
     const uint64_t* row_base;
     uint16_t* costs;
-    uint32_t* agg_zero;              // optional: zeroed at the same entries
     int kind, ww, wh;
     const uint16_t* census_lut;      // [bits+1]
     // set by the launcher: pixels with count <= exact_above go to the tiled
     // certified census kernel, the rest to the exact per-hypothesis kernel
     int exact_above;
     int disable_tiled;               // force the exact per-hypothesis kernel
-    int plane_slicing;               // dense ranges: split planes across CTAs (grid z)
+    int plane_slicing;               // dense ranges: split planes across CTAs (grid z); the
+                                     // tiled kernels then stage each pixel's costs of 16
+                                     // planes and write them as one 32-byte run
     int narrow_max;                  // pixels with more hypotheses take the exact kernel (0: default)
     unsigned long long* stats;       // optional diagnostics (fmvs_ctx_sweep_stats)
 };
