@@ -481,7 +481,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
     uint32_t* agg = nullptr;
     if (!compact) {
         costs = ctx->buf("costs").as<uint16_t>(max_entries);
-        agg = ctx->buf("agg").as<uint32_t>(max_entries);
+        agg = ctx->buf("agg").as<uint32_t>(max_entries + k::kAggSlack);
     }
     auto* offs = ctx->buf("offsets").as<int16_t>(4 * max_px);
     auto* depth_raw = ctx->buf("depth_raw").as<float>(max_px);
@@ -510,6 +510,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
             lines = std::max(lines, static_cast<size_t>(k::sgm_total_lines(P.w, P.h, 8)));
         sgm_scratch = ctx->buf("sgm_scratch").as<uint32_t>(lines * 2 * (max_p + 8));
     }
+    uint32_t* sgm_line = ctx->buf("sgm_line").as<uint32_t>(k::sgm_line_scratch_words(lv[0].w, lv[0].h));
 
     const double cos_rho = std::cos(60.0 * M_PI / 180.0);
     const double pdv = (cfg.sweep_normal[0] * 0.0 + cfg.sweep_normal[1] * 0.0) +
@@ -551,13 +552,15 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
             k::scan_rows(row_total, P.h, rb, s);
         });
         launches += 2;
+        uint64_t entries_bound = static_cast<uint64_t>(P.w) * P.h * np;
         if (compact) {
             uint64_t entries = 0;
             FMVS_CUDA_CHECK(cudaMemcpyAsync(&entries, rb + P.h, sizeof(entries), cudaMemcpyDeviceToHost, s));
             FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+            entries_bound = entries;
             const size_t need = std::max<size_t>(entries, 1);
             costs = ctx->buf("costs").as<uint16_t>(need);
-            agg = ctx->buf("agg").as<uint32_t>(need);
+            agg = ctx->buf("agg").as<uint32_t>(need + k::kAggSlack);
         }
 
         k::SweepArgs sa{};
@@ -645,6 +648,8 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         }
         ga.group_caps = l == L - 1 ? std::min(np, 1024) : 32;
         ga.scratch = (ga.group > 0 || np > pmax_smem_limit) ? sgm_scratch : nullptr;
+        ga.line_scratch = sgm_line;
+        ga.entries_bound = entries_bound;
         ctx->timed(l == 0 ? "sgm_l0" : "sgm", [&] { k::sgm(ga, s); });
         ++launches;
 
@@ -1369,7 +1374,7 @@ int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         ga.meta = t.upload(meta.data(), px, s);
         ga.row_base = t.upload(rb.data(), rb.size(), s);
         ga.costs = t.upload(costs, total, s);
-        ga.agg = t.alloc<uint32_t>(total);
+        ga.agg = t.alloc<uint32_t>(total + k::kAggSlack);
         FMVS_CUDA_CHECK(cudaMemsetAsync(ga.agg, 0, std::max<uint64_t>(total, 1) * 4, s));
         ga.image = t.upload(image, px, s);
         ga.variant = cfg->variant;
@@ -1409,6 +1414,8 @@ int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
             const size_t lines = static_cast<size_t>(k::sgm_lines(w, h, ga.dirs, ga.ndirs));
             ga.scratch = t.alloc<uint32_t>(lines * 2 * (pmax + 8));
         }
+        ga.line_scratch = t.alloc<uint32_t>(k::sgm_line_scratch_words(w, h));
+        ga.entries_bound = total;
         if (total > 0)
             k::sgm(ga, s);
         std::vector<uint32_t> compact_out;

@@ -15,7 +15,9 @@
 // reference's determinism contract, README.md:87-88).
 // Roofline: HBM/L2-bound -- per hypothesis and path: 2 B cost read + 4 B
 // atomic add; per pixel and path: 8 B meta + 1 B image.
+#include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 #include "host.hpp"
 #include "kernels.hpp"
@@ -627,6 +629,268 @@ done:
     return;
 }
 
+// ---- line kernel: Plane / SurfaceNormal, unit directions, int32 ------------
+//
+// Same recurrence and mapping as sgm_lanes_kernel (G lanes per scanline, K
+// hypotheses per lane and pass), restructured so that a step costs few
+// instructions:
+//  * every per-pixel operand of a step comes from ONE 16-byte record built
+//    per level by sgm_prep_kernel (32-bit entry index; first | count << 11 |
+//    intensity << 23; the four SN shifts), so a step issues one record load
+//    instead of meta + row base + image + SN loads and their 64-bit address
+//    arithmetic; records past the end of a line read a zero dummy record;
+//  * the line's length is known at its start (no per-step inside tests, the
+//    warp runs max-length steps);
+//  * the path buffers of a line live in ONE address space for the whole line,
+//    chosen at its start: shared memory, or the global scratch when any pixel
+//    of the line is wider than the shared capacity (flagged by the prep
+//    kernel per row / column / diagonal / anti-diagonal); the double buffer
+//    alternates on every step, so with an even pipeline depth its parity is
+//    static in the unrolled step loop;
+//  * a pixel without a predecessor reads only the three left sentinels (its
+//    window offset is pushed far left), so no has_prev selects in the
+//    hypothesis loop; the phi2 LUT lives in shared memory.
+// Records hold 32-bit entry indices and <= kRecPlanes planes (host-checked;
+// other volumes take the general kernel).
+constexpr int kRecPlanes = 2048;
+
+__device__ __forceinline__ int rec_first(uint32_t pk) { return static_cast<int>(pk & 0x7FFu); }
+__device__ __forceinline__ int rec_count(uint32_t pk) { return static_cast<int>((pk >> 11) & 0xFFFu); }
+__device__ __forceinline__ int rec_img(uint32_t pk) { return static_cast<int>(pk >> 23); }
+
+// wide-line flags: one word per row, column, diagonal (x - y) and
+// anti-diagonal (x + y)
+struct LineFlags {
+    uint32_t* row;
+    uint32_t* col;
+    uint32_t* diag;
+    uint32_t* anti;
+};
+__host__ __device__ inline LineFlags line_flags(uint32_t* base, int w, int h) {
+    return {base, base + h, base + h + w, base + h + w + (w + h - 1)};
+}
+__host__ __device__ inline size_t line_flag_words(int w, int h) {
+    return static_cast<size_t>(h) + w + 2 * (static_cast<size_t>(w) + h - 1);
+}
+
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F& f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+// f(integral_constant<int, 0>) ... f(integral_constant<int, N - 1>)
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// Path-buffer store (generic: shared or global scratch) predicated on p, and
+// an UNCONDITIONAL aggregate RED of (p ? v : 0) at a byte offset: straight-line
+// code (a predicated or guarded RED compiles to a branch per hypothesis). An
+// inactive lane adds 0 to an entry of a later pixel, or to the >= 64-entry
+// slack every aggregate allocation carries past the volume's last entry.
+template <int OFF>
+__device__ __forceinline__ void store_red(bool p, uint32_t* buf, uint32_t* agg, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ne.u32 q, %0, 0;\n\t"
+        "@q st.u32 [%1+%3], %4;\n\t"
+        "red.relaxed.gpu.global.add.u32 [%2+%3], %5;\n\t}"
+        :
+        : "r"(static_cast<uint32_t>(p)), "l"(buf), "l"(agg), "n"(OFF), "r"(v), "r"(p ? v : 0u));
+}
+
+__global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps) {
+    const int n = a.w * a.h;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > n)
+        return;
+    if (p == n) {  // the dummy record read past the end of a line
+        rec[p] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
+    const int y = p / a.w, x = p - y * a.w;
+    const dev::VolMeta m = a.meta[p];
+    const int c = dev::meta_count(m.fc);
+    uint4 r;
+    r.x = static_cast<uint32_t>(a.row_base[y] + m.rel);
+    r.y = (c > 0 ? static_cast<uint32_t>(dev::meta_first(m.fc)) : 0u) | static_cast<uint32_t>(c) << 11 |
+          static_cast<uint32_t>(a.image[p]) << 23;
+    if (a.offsets) {
+        const uint2 o = reinterpret_cast<const uint2*>(a.offsets)[p];
+        r.z = o.x;
+        r.w = o.y;
+    } else {
+        r.z = r.w = 0u;
+    }
+    rec[p] = r;
+    if (c > caps) {
+        atomicOr(fl.row + y, 1u);
+        atomicOr(fl.col + x, 1u);
+        atomicOr(fl.diag + (x - y + a.h - 1), 1u);
+        atomicOr(fl.anti + (x + y), 1u);
+    }
+}
+
+template <bool SN, int G, int K, int S, int GAP>
+__global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const uint4* __restrict__ rec,
+                                                               LineFlags fl, int total_lines, int caps,
+                                                               int stride) {
+    constexpr int LPW = 32 / G;
+    constexpr int PASS = G * K;
+    static_assert(S % 2 == 0, "static double-buffer parity needs an even pipeline depth");
+    extern __shared__ uint32_t smem[];
+    int* lut = reinterpret_cast<int*>(smem);
+    for (int i = threadIdx.x; i < 256; i += kWarps * 32)
+        lut[i] = static_cast<int>(a.phi2_lut[i]);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / G, gl = lane % G;
+    const int line = (blockIdx.x * kWarps + warp) * LPW + grp;
+    const int w = a.w, h = a.h;
+
+    int dx = 1, dy = 0, x = 0, y = 0, n = 0;
+    bool wide = false;
+    if (line < total_lines) {
+        locate_line(a, line, &dx, &dy, &x, &y);
+        const int nx = dx > 0 ? w - x : (dx < 0 ? x + 1 : 0x7FFFFFFF);
+        const int ny = dy > 0 ? h - y : (dy < 0 ? y + 1 : 0x7FFFFFFF);
+        n = min(nx, ny);
+        const uint32_t* f = dy == 0 ? fl.row + y
+                                    : (dx == 0 ? fl.col + x : (dx == dy ? fl.diag + (x - y + h - 1) : fl.anti + (x + y)));
+        wide = *f != 0u;
+    }
+    uint32_t* bufA;
+    uint32_t* bufB;
+    if (wide) {
+        const size_t gs = static_cast<size_t>(a.pmax) + 2 * kSent;
+        bufA = a.scratch + static_cast<size_t>(line) * 2 * gs + kSent;
+        bufB = bufA + gs;
+    } else {
+        bufA = smem + 256 + (warp * LPW + grp) * stride + kSent;
+        bufB = bufA + caps + 2 * kSent;
+    }
+    if (gl < kSent) {
+        bufA[-kSent + gl] = kSentinel;
+        bufB[-kSent + gl] = kSentinel;
+    }
+    __syncwarp();
+    const int nmax = static_cast<int>(__reduce_max_sync(0xFFFFFFFFu, static_cast<unsigned>(n)));
+
+    // SN: canonical slot of +-(dx, dy) and the direction's sign (sgm.cpp:72-87)
+    const int slot = dy == 0 ? 0 : (dx == 0 ? 1 : (dx == dy ? 2 : 3));
+    const int sign = (dy == 0 || dx == 0) ? dx + dy : dx;
+    const int off_sh = (slot & 1) * 16;
+    const bool off_hi = (slot >> 1) != 0;
+    const int phi1 = static_cast<int>(a.phi1);
+    const int dp = dy * w + dx;
+    const int dummy = w * h;
+
+    uint4 R[S];
+    uint32_t C[S][K];
+    int PH[S];
+    int q = y * w + x;  // pixel of the next record load
+    int jn = 0;         // its step index along the line
+    auto load_rec = [&](uint4& r) {
+        const int idx = jn < n ? q : dummy;
+        if (SN) {
+            r = __ldg(rec + idx);
+        } else {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(rec + idx));
+            r.x = v.x;
+            r.y = v.y;
+            r.z = r.w = 0u;
+        }
+        q += dp;
+        ++jn;
+    };
+    auto load_costs = [&](int si, int sp) {
+        const uint32_t pk = R[si].y;
+        const int c = rec_count(pk);
+        const uint16_t* cp = a.costs + (R[si].x + gl);
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            C[si][k] = gl + G * k < c ? cp[G * k] : 0u;
+        PH[si] = lut[abs(rec_img(pk) - rec_img(R[sp].y))];
+    };
+
+    // prologue: records of pixels 0..S-2, costs of pixels 0..S-2-GAP
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j)
+        load_rec(R[j]);
+    R[S - 1] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int j = 0; j < S - 1 - GAP; ++j)
+        load_costs(j, (j + S - 1) % S);
+
+    int prev_first = 0, prev_count = 0, prev_min = 0;
+    bool has_prev = false;
+    for (int j0 = 0; j0 < nmax; j0 += S) {
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            if (j0 + u >= nmax)
+                break;
+            // record of pixel j+S-1 (into the slot of pixel j-1), costs of
+            // pixel j+S-1-GAP (its record arrived GAP steps ago)
+            load_rec(R[(u + S - 1) % S]);
+            load_costs((u + S - 1 - GAP) % S, (u + S - 2 - GAP) % S);
+
+            // recurrence of pixel j (walk_line, sgm.cpp:97-195)
+            uint32_t* cur = (u & 1) ? bufA : bufB;
+            const uint32_t* prev = (u & 1) ? bufB : bufA;
+            const uint32_t pk = R[u].y;
+            const int c = rec_count(pk), f = rec_first(pk);
+            uint32_t run_min = 0xFFFFFFFFu;
+            if (c > 0) {
+                int shift = 0;
+                if (SN && has_prev) {
+                    const uint32_t wd = off_hi ? R[u].w : R[u].z;
+                    shift = sign * static_cast<int>(static_cast<int16_t>(wd >> off_sh));
+                }
+                const int toff = has_prev ? f + shift - prev_first : -0x40000000;
+                const int pm = has_prev ? prev_min : 0;
+                const int bp = has_prev ? prev_min + PH[u] : 0;
+                const int tmax = prev_count + 1;
+                const uint32_t ib = R[u].x + gl;
+                // branch-free: every lane evaluates its K slots; the path
+                // buffer store and the aggregate RED are predicated on i < c
+                auto pass = [&](int i0, const uint32_t* sc) {
+                    uint32_t* ap = a.agg + (ib + i0);
+                    uint32_t* cp = cur + (gl + i0);
+                    static_for<K>([&](auto kc) {
+                        constexpr int k = decltype(kc)::value;
+                        const int i = i0 + gl + G * k;
+                        const int t = min(max(toff + i, -2), tmax);
+                        const int b3 = min(static_cast<int>(prev[t - 1]), static_cast<int>(prev[t + 1])) + phi1;
+                        const int best = min(min(bp, static_cast<int>(prev[t])), b3);
+                        const uint32_t v = sc[k] + static_cast<uint32_t>(best - pm);
+                        store_red<4 * G * k>(i < c, cp, ap, v);
+                        run_min = min(run_min, i < c ? v : 0xFFFFFFFFu);
+                    });
+                };
+                pass(0, C[u]);
+                for (int i0 = PASS; i0 < c; i0 += PASS) {  // pixels wider than a pass
+                    const uint16_t* cp = a.costs + (ib + i0);
+                    uint32_t sc[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        sc[k] = i0 + gl + G * k < c ? cp[G * k] : 0u;
+                    pass(i0, sc);
+                }
+                if (gl < kSent)
+                    cur[c + gl] = kSentinel;
+            }
+            const uint32_t nmin = group_min<G>(run_min);
+            __syncwarp();
+            if (c > 0) {
+                prev_min = static_cast<int>(nmin);
+                prev_first = f;
+                prev_count = c;
+            }
+            has_prev = c > 0;
+        }
+    }
+}
+
 // compute_normal_offsets (sgm.cpp:252-299) on the upscaled prior maps.
 __global__ void normal_offsets_kernel(OffsetArgs a) {
     using namespace dev;
@@ -730,6 +994,43 @@ void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
         throw Error(FMVS_ERR_CONFIG, "sgm: unsupported lane blocking");
 }
 
+template <bool SN, int G, int K>
+void launch_line(const SgmArgs& a, int total, cudaStream_t s) {
+    constexpr int LPW = 32 / G;
+    constexpr int S = K >= 8 ? 4 : 6;
+    constexpr int GAP = K >= 8 ? 1 : 2;
+    const int caps = a.group_caps;
+    int stride = 2 * (caps + 2 * kSent);
+    stride += ((G % 32) - stride % 32 + 32) % 32;
+    const int blocks = (total + kWarps * LPW - 1) / (kWarps * LPW);
+    const size_t smem = (256 + static_cast<size_t>(kWarps) * LPW * stride) * sizeof(uint32_t);
+    auto* rec = reinterpret_cast<uint4*>(a.line_scratch);
+    const LineFlags fl = line_flags(a.line_scratch + 4 * (static_cast<size_t>(a.w) * a.h + 1), a.w, a.h);
+    FMVS_CUDA_CHECK(cudaMemsetAsync(fl.row, 0, line_flag_words(a.w, a.h) * sizeof(uint32_t), s));
+    const int npx = a.w * a.h + 1;
+    sgm_prep_kernel<<<(npx + 255) / 256, 256, 0, s>>>(a, rec, fl, caps);
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_line_kernel<SN, G, K, S, GAP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    sgm_line_kernel<SN, G, K, S, GAP><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, caps, stride);
+}
+
+template <bool SN>
+bool launch_line_gk(const SgmArgs& a, int total, cudaStream_t s) {
+    if (a.group == 4 && a.kper == 4)
+        launch_line<SN, 4, 4>(a, total, s);
+    else if (a.group == 32 && a.kper == 4)
+        launch_line<SN, 32, 4>(a, total, s);
+    else if (a.group == 32 && a.kper == 8)
+        launch_line<SN, 32, 8>(a, total, s);
+    else
+        return false;
+    return true;
+}
+
+size_t sgm_line_scratch_words(int w, int h) {
+    return 4 * (static_cast<size_t>(w) * h + 1) + line_flag_words(w, h);
+}
+
 void sgm(const SgmArgs& a, cudaStream_t s) {
     const int total = sgm_lines(a.w, a.h, a.dirs, a.ndirs);
     if (total == 0)
@@ -738,6 +1039,24 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
     // path values <= 65535 + phi2_max, candidates <= value + max(phi1, phi2).
     const bool fast32 = a.phi1 >= 0 && a.phi2_max >= 0 && a.phi1 < (1ll << 28) &&
                         a.phi2_max < (1ll << 28);
+    // line kernel: Plane / SN, int32, unit directions, 32-bit entry indices
+    static const bool line_on = [] {
+        const char* e = std::getenv("FMVS_SGM_LINE");
+        return !(e && e[0] == '0');
+    }();
+    bool unit = true;
+    for (int d = 0; d < a.ndirs; ++d)
+        unit = unit && std::abs(a.dirs[d][0]) <= 1 && std::abs(a.dirs[d][1]) <= 1 &&
+               (a.dirs[d][0] != 0 || a.dirs[d][1] != 0);
+    if (line_on && a.line_scratch && a.scratch && fast32 && unit && a.group > 0 &&
+        a.variant != FMVS_SGM_PATH_GRADIENT && a.nplanes <= kRecPlanes &&
+        a.entries_bound + 1024 < (1ull << 32)) {
+        const bool done = a.offsets ? launch_line_gk<true>(a, total, s) : launch_line_gk<false>(a, total, s);
+        if (done) {
+            FMVS_CUDA_CHECK(cudaGetLastError());
+            return;
+        }
+    }
     if (a.group > 0) {
         // lane-blocked kernel; scratch (global overflow buffers) is mandatory here
         if (a.variant == FMVS_SGM_PATH_GRADIENT) {

@@ -134,8 +134,18 @@ struct SgmArgs {
     int group;                       // lanes per line for Plane/SN (4, 8, 32); 0 = 1 line/warp kernel
     int kper;                        // hypotheses per lane and pass (register blocking)
     int group_caps;                  // shared-memory path buffer length per line (grouped kernel)
+    // Line kernel (unit directions, Plane/SN, int32 recurrence): scratch of
+    // sgm_line_scratch_words(w, h) words for the per-pixel step records and
+    // the wide-line flags, or null for the general kernel; an upper bound of
+    // the level's entry count (the records hold 32-bit entry indices).
+    uint32_t* line_scratch;
+    uint64_t entries_bound;
 };
 void sgm(const SgmArgs& a, cudaStream_t s);
+// entries every aggregate allocation carries past the volume (the line
+// kernel's inactive lanes add 0 there)
+constexpr size_t kAggSlack = 64;
+size_t sgm_line_scratch_words(int w, int h);
 int sgm_total_lines(int w, int h, int ndirs);
 // Lines of the given path directions (any step, sgm.cpp:213-219).
 int sgm_lines(int w, int h, const int (*dirs)[2], int ndirs);
