@@ -108,7 +108,9 @@ struct Tmp {
     template <typename T>
     T* alloc(size_t count) {
         void* p = nullptr;
-        FMVS_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)));
+        // + 256 B: kernels may over-read a volume's tail by up to a 48-byte
+        // aligned chunk (SGM cost staging) or add 0 past it (SGM REDs)
+        FMVS_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T) + 256));
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
@@ -130,9 +132,13 @@ fmvs::V3 v3(const double* n) { return {n[0], n[1], n[2]}; }
 // Lane blocking of the SGM kernel at the refined levels: G lanes per scanline,
 // K hypotheses per lane and pass (FMVS_SGM_G / FMVS_SGM_K; results are
 // identical, only speed differs). G = 0 selects the one-line-per-warp kernel.
-void sgm_blocking(int* g, int* k) {
+// Lanes per scanline and hypotheses per lane of the refined-level SGM.
+// `widest` bounds the pixels' hypothesis counts when known (0: unknown): the
+// default spacing-multiple policy (3 coarser spacings) gives <= 12, one
+// G=4 x K=3 pass; wider pixels take the kernel's multi-pass lines.
+void sgm_blocking(int* g, int* k, int widest = 0) {
     *g = 4;
-    *k = 4;
+    *k = widest > 0 && widest <= 12 ? 3 : 4;
     if (const char* e = std::getenv("FMVS_SGM_G"))
         *g = std::atoi(e);
     if (const char* e = std::getenv("FMVS_SGM_K"))
@@ -480,7 +486,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
     uint16_t* costs = nullptr;
     uint32_t* agg = nullptr;
     if (!compact) {
-        costs = ctx->buf("costs").as<uint16_t>(max_entries);
+        costs = ctx->buf("costs").as<uint16_t>(max_entries + k::kAggSlack);
         agg = ctx->buf("agg").as<uint32_t>(max_entries + k::kAggSlack);
     }
     auto* offs = ctx->buf("offsets").as<int16_t>(4 * max_px);
@@ -559,7 +565,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
             FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
             entries_bound = entries;
             const size_t need = std::max<size_t>(entries, 1);
-            costs = ctx->buf("costs").as<uint16_t>(need);
+            costs = ctx->buf("costs").as<uint16_t>(need + k::kAggSlack);
             agg = ctx->buf("agg").as<uint32_t>(need + k::kAggSlack);
         }
 
@@ -641,7 +647,9 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         ga.pmax = np;
         // coarsest level: dense ranges, one line per warp-wide group; refined
         // levels: ~12 hypotheses per pixel, 32/G lines per warp
-        sgm_blocking(&ga.group, &ga.kper);
+        // spacing multiple m: about 4m + 1 finer planes per pixel
+        const bool narrow_policy = cfg.range_kind == FMVS_RANGE_SPACING_MULTIPLE && cfg.range_value <= 3.0;
+        sgm_blocking(&ga.group, &ga.kper, narrow_policy ? 12 : 0);
         if (l == L - 1) {  // dense coarsest level: one line per warp, one pass up to 256 planes
             ga.group = 32;
             ga.kper = np > 128 ? 8 : 4;
@@ -1407,7 +1415,7 @@ int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
             ga.offsets = oa.out;
         }
         ga.pmax = pmax;
-        sgm_blocking(&ga.group, &ga.kper);
+        sgm_blocking(&ga.group, &ga.kper, pmax);
         ga.group_caps = 32;
         const int limit = (200 * 1024) / (4 * 2 * 4);
         if (pmax > limit || ga.group > 0) {

@@ -683,20 +683,13 @@ __device__ __forceinline__ void static_for(F&& f) {
     static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
-// Path-buffer store (generic: shared or global scratch) predicated on p, and
-// an UNCONDITIONAL aggregate RED of (p ? v : 0) at a byte offset: straight-line
+// Aggregate RED of (p ? v : 0) at a byte offset, UNCONDITIONAL: straight-line
 // code (a predicated or guarded RED compiles to a branch per hypothesis). An
-// inactive lane adds 0 to an entry of a later pixel, or to the >= 64-entry
-// slack every aggregate allocation carries past the volume's last entry.
+// inactive lane adds 0 to an entry of a later pixel, or to the kAggSlack
+// entries every aggregate allocation carries past the volume's last entry.
 template <int OFF>
-__device__ __forceinline__ void store_red(bool p, uint32_t* buf, uint32_t* agg, uint32_t v) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\t"
-        "setp.ne.u32 q, %0, 0;\n\t"
-        "@q st.u32 [%1+%3], %4;\n\t"
-        "red.relaxed.gpu.global.add.u32 [%2+%3], %5;\n\t}"
-        :
-        : "r"(static_cast<uint32_t>(p)), "l"(buf), "l"(agg), "n"(OFF), "r"(v), "r"(p ? v : 0u));
+__device__ __forceinline__ void red_add(uint32_t* agg, bool p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0+%1], %2;" : : "l"(agg), "n"(OFF), "r"(p ? v : 0u));
 }
 
 __global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps) {
@@ -731,128 +724,110 @@ __global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps) {
     }
 }
 
+// Per-line constants of the line kernel.
+struct LineCtx {
+    const uint4* __restrict__ rec;
+    const int* lut;  // phi2 LUT (shared memory)
+    int gl;          // lane within the line's group
+    int n;           // pixels on the line
+    int steps;       // steps the warp runs (>= n)
+    int q;           // pixel index of the line's first pixel
+    int dp;          // pixel-index step along the line
+    int dummy;       // index of the zero record
+    int sign, off_sh;
+    bool off_hi;
+};
+
+// Operand pipeline of the line kernel: records of pixels j+1..j+S-1 and the
+// costs / phi2 of pixels j+1..j+S-1-GAP in registers at the step of pixel j.
 template <bool SN, int G, int K, int S, int GAP>
-__global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const uint4* __restrict__ rec,
-                                                               LineFlags fl, int total_lines, int caps,
-                                                               int stride) {
-    constexpr int LPW = 32 / G;
-    constexpr int PASS = G * K;
-    static_assert(S % 2 == 0, "static double-buffer parity needs an even pipeline depth");
-    extern __shared__ uint32_t smem[];
-    int* lut = reinterpret_cast<int*>(smem);
-    for (int i = threadIdx.x; i < 256; i += kWarps * 32)
-        lut[i] = static_cast<int>(a.phi2_lut[i]);
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = lane / G, gl = lane % G;
-    const int line = (blockIdx.x * kWarps + warp) * LPW + grp;
-    const int w = a.w, h = a.h;
-
-    int dx = 1, dy = 0, x = 0, y = 0, n = 0;
-    bool wide = false;
-    if (line < total_lines) {
-        locate_line(a, line, &dx, &dy, &x, &y);
-        const int nx = dx > 0 ? w - x : (dx < 0 ? x + 1 : 0x7FFFFFFF);
-        const int ny = dy > 0 ? h - y : (dy < 0 ? y + 1 : 0x7FFFFFFF);
-        n = min(nx, ny);
-        const uint32_t* f = dy == 0 ? fl.row + y
-                                    : (dx == 0 ? fl.col + x : (dx == dy ? fl.diag + (x - y + h - 1) : fl.anti + (x + y)));
-        wide = *f != 0u;
-    }
-    uint32_t* bufA;
-    uint32_t* bufB;
-    if (wide) {
-        const size_t gs = static_cast<size_t>(a.pmax) + 2 * kSent;
-        bufA = a.scratch + static_cast<size_t>(line) * 2 * gs + kSent;
-        bufB = bufA + gs;
-    } else {
-        bufA = smem + 256 + (warp * LPW + grp) * stride + kSent;
-        bufB = bufA + caps + 2 * kSent;
-    }
-    if (gl < kSent) {
-        bufA[-kSent + gl] = kSentinel;
-        bufB[-kSent + gl] = kSentinel;
-    }
-    __syncwarp();
-    const int nmax = static_cast<int>(__reduce_max_sync(0xFFFFFFFFu, static_cast<unsigned>(n)));
-
-    // SN: canonical slot of +-(dx, dy) and the direction's sign (sgm.cpp:72-87)
-    const int slot = dy == 0 ? 0 : (dx == 0 ? 1 : (dx == dy ? 2 : 3));
-    const int sign = (dy == 0 || dx == 0) ? dx + dy : dx;
-    const int off_sh = (slot & 1) * 16;
-    const bool off_hi = (slot >> 1) != 0;
-    const int phi1 = static_cast<int>(a.phi1);
-    const int dp = dy * w + dx;
-    const int dummy = w * h;
-
+struct LinePipe {
     uint4 R[S];
     uint32_t C[S][K];
     int PH[S];
-    int q = y * w + x;  // pixel of the next record load
-    int jn = 0;         // its step index along the line
-    auto load_rec = [&](uint4& r) {
-        const int idx = jn < n ? q : dummy;
+    int q, jn;
+
+    __device__ __forceinline__ void load_rec(const LineCtx& lc, uint4& r) {
+        const int idx = jn < lc.n ? q : lc.dummy;
         if (SN) {
-            r = __ldg(rec + idx);
+            r = __ldg(lc.rec + idx);
         } else {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(rec + idx));
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(lc.rec + idx));
             r.x = v.x;
             r.y = v.y;
             r.z = r.w = 0u;
         }
-        q += dp;
+        q += lc.dp;
         ++jn;
-    };
-    auto load_costs = [&](int si, int sp) {
+    }
+    __device__ __forceinline__ void load_costs(const SgmArgs& a, const LineCtx& lc, int si, int sp) {
         const uint32_t pk = R[si].y;
         const int c = rec_count(pk);
-        const uint16_t* cp = a.costs + (R[si].x + gl);
+        const uint16_t* cp = a.costs + (R[si].x + lc.gl);
 #pragma unroll
         for (int k = 0; k < K; ++k)
-            C[si][k] = gl + G * k < c ? cp[G * k] : 0u;
-        PH[si] = lut[abs(rec_img(pk) - rec_img(R[sp].y))];
-    };
-
+            C[si][k] = lc.gl + G * k < c ? cp[G * k] : 0u;
+        PH[si] = lc.lut[abs(rec_img(pk) - rec_img(R[sp].y))];
+    }
     // prologue: records of pixels 0..S-2, costs of pixels 0..S-2-GAP
+    __device__ __forceinline__ void start(const SgmArgs& a, const LineCtx& lc) {
+        q = lc.q;
+        jn = 0;
 #pragma unroll
-    for (int j = 0; j < S - 1; ++j)
-        load_rec(R[j]);
-    R[S - 1] = make_uint4(0u, 0u, 0u, 0u);
+        for (int j = 0; j < S - 1; ++j)
+            load_rec(lc, R[j]);
+        R[S - 1] = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-    for (int j = 0; j < S - 1 - GAP; ++j)
-        load_costs(j, (j + S - 1) % S);
+        for (int j = 0; j < S - 1 - GAP; ++j)
+            load_costs(a, lc, j, (j + S - 1) % S);
+    }
+    // at the step in slot u: record of pixel j+S-1 (into the slot of pixel
+    // j-1), costs of pixel j+S-1-GAP (its record arrived GAP steps ago)
+    __device__ __forceinline__ void advance(const SgmArgs& a, const LineCtx& lc, int u) {
+        load_rec(lc, R[(u + S - 1) % S]);
+        load_costs(a, lc, (u + S - 1 - GAP) % S, (u + S - 2 - GAP) % S);
+    }
+    __device__ __forceinline__ int shift(const LineCtx& lc, int u) const {
+        const uint32_t wd = lc.off_hi ? R[u].w : R[u].z;
+        return lc.sign * static_cast<int>(static_cast<int16_t>(wd >> lc.off_sh));
+    }
+};
 
+// Steps of the lines of a warp: any number of passes per pixel (pixels wider
+// than G*K hypotheses loop), each line's double buffer in shared memory or,
+// when the line is wide, in its global scratch (SHARED: no line of the warp
+// is wide, so the buffers are shared-memory typed). Each step is its own
+// basic block (the `c > 0` branch), which keeps the compiler from sinking the
+// pipelined record and cost loads towards their uses (measured: branch-free
+// step bodies, with the predecessor window loaded a step early, ran 1.8x
+// slower at level 0, with the same loads staged through shared memory by
+// cp.async too).
+template <bool SN, int G, int K, int S, int GAP, bool SHARED>
+__device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, uint32_t* bufA,
+                                          uint32_t* bufB) {
+    constexpr int PASS = G * K;
+    const int gl = lc.gl;
+    const int phi1 = static_cast<int>(a.phi1);
+    LinePipe<SN, G, K, S, GAP> P;
+    P.start(a, lc);
     int prev_first = 0, prev_count = 0, prev_min = 0;
     bool has_prev = false;
-    for (int j0 = 0; j0 < nmax; j0 += S) {
+    for (int j0 = 0; j0 < lc.steps; j0 += S) {
 #pragma unroll
         for (int u = 0; u < S; ++u) {
-            if (j0 + u >= nmax)
-                break;
-            // record of pixel j+S-1 (into the slot of pixel j-1), costs of
-            // pixel j+S-1-GAP (its record arrived GAP steps ago)
-            load_rec(R[(u + S - 1) % S]);
-            load_costs((u + S - 1 - GAP) % S, (u + S - 2 - GAP) % S);
-
-            // recurrence of pixel j (walk_line, sgm.cpp:97-195)
+            P.advance(a, lc, u);
             uint32_t* cur = (u & 1) ? bufA : bufB;
             const uint32_t* prev = (u & 1) ? bufB : bufA;
-            const uint32_t pk = R[u].y;
+            const uint32_t pk = P.R[u].y;
             const int c = rec_count(pk), f = rec_first(pk);
             uint32_t run_min = 0xFFFFFFFFu;
             if (c > 0) {
-                int shift = 0;
-                if (SN && has_prev) {
-                    const uint32_t wd = off_hi ? R[u].w : R[u].z;
-                    shift = sign * static_cast<int>(static_cast<int16_t>(wd >> off_sh));
-                }
+                const int shift = (SN && has_prev) ? P.shift(lc, u) : 0;
                 const int toff = has_prev ? f + shift - prev_first : -0x40000000;
                 const int pm = has_prev ? prev_min : 0;
-                const int bp = has_prev ? prev_min + PH[u] : 0;
+                const int bp = has_prev ? prev_min + P.PH[u] : 0;
                 const int tmax = prev_count + 1;
-                const uint32_t ib = R[u].x + gl;
-                // branch-free: every lane evaluates its K slots; the path
-                // buffer store and the aggregate RED are predicated on i < c
+                const uint32_t ib = P.R[u].x + gl;
                 auto pass = [&](int i0, const uint32_t* sc) {
                     uint32_t* ap = a.agg + (ib + i0);
                     uint32_t* cp = cur + (gl + i0);
@@ -863,12 +838,14 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
                         const int b3 = min(static_cast<int>(prev[t - 1]), static_cast<int>(prev[t + 1])) + phi1;
                         const int best = min(min(bp, static_cast<int>(prev[t])), b3);
                         const uint32_t v = sc[k] + static_cast<uint32_t>(best - pm);
-                        store_red<4 * G * k>(i < c, cp, ap, v);
+                        if (i < c)
+                            cp[G * k] = v;
+                        red_add<4 * G * k>(ap, i < c, v);
                         run_min = min(run_min, i < c ? v : 0xFFFFFFFFu);
                     });
                 };
-                pass(0, C[u]);
-                for (int i0 = PASS; i0 < c; i0 += PASS) {  // pixels wider than a pass
+                pass(0, P.C[u]);
+                for (int i0 = PASS; i0 < c; i0 += PASS) {
                     const uint16_t* cp = a.costs + (ib + i0);
                     uint32_t sc[K];
 #pragma unroll
@@ -888,6 +865,75 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
             }
             has_prev = c > 0;
         }
+    }
+}
+
+template <bool SN, int G, int K, int S, int GAP>
+__global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const uint4* __restrict__ rec,
+                                                               LineFlags fl, int total_lines, int stride) {
+    constexpr int LPW = 32 / G;
+    constexpr int PASS = G * K;
+    static_assert(S % 2 == 0, "static double-buffer parity needs an even pipeline depth");
+    extern __shared__ uint32_t smem[];
+    int* lut = reinterpret_cast<int*>(smem);
+    for (int i = threadIdx.x; i < 256; i += kWarps * 32)
+        lut[i] = static_cast<int>(a.phi2_lut[i]);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / G;
+    const int line = (blockIdx.x * kWarps + warp) * LPW + grp;
+    const int w = a.w, h = a.h;
+
+    int dx = 1, dy = 0, x = 0, y = 0, n = 0;
+    bool wide = false;
+    if (line < total_lines) {
+        locate_line(a, line, &dx, &dy, &x, &y);
+        const int nx = dx > 0 ? w - x : (dx < 0 ? x + 1 : 0x7FFFFFFF);
+        const int ny = dy > 0 ? h - y : (dy < 0 ? y + 1 : 0x7FFFFFFF);
+        n = min(nx, ny);
+        const uint32_t* f = dy == 0 ? fl.row + y
+                                    : (dx == 0 ? fl.col + x : (dx == dy ? fl.diag + (x - y + h - 1) : fl.anti + (x + y)));
+        wide = *f != 0u;
+    }
+    LineCtx lc;
+    lc.rec = rec;
+    lc.lut = lut;
+    lc.gl = lane % G;
+    lc.n = n;
+    const int nmax = static_cast<int>(__reduce_max_sync(0xFFFFFFFFu, static_cast<unsigned>(n)));
+    lc.steps = (nmax + S - 1) / S * S;  // padded: steps past a line's end see empty pixels
+    lc.q = y * w + x;
+    lc.dp = dy * w + dx;
+    lc.dummy = w * h;
+    // SN: canonical slot of +-(dx, dy) and the direction's sign (sgm.cpp:72-87)
+    const int slot = dy == 0 ? 0 : (dx == 0 ? 1 : (dx == dy ? 2 : 3));
+    lc.sign = (dy == 0 || dx == 0) ? dx + dy : dx;
+    lc.off_sh = (slot & 1) * 16;
+    lc.off_hi = (slot >> 1) != 0;
+
+    uint32_t* sA = smem + 256 + (warp * LPW + grp) * stride + kSent;
+    uint32_t* sB = sA + PASS + 2 * kSent;
+    if (lc.gl < kSent) {
+        sA[-kSent + lc.gl] = kSentinel;
+        sB[-kSent + lc.gl] = kSentinel;
+    }
+    if (__any_sync(0xFFFFFFFFu, wide)) {
+        uint32_t* bufA = sA;
+        uint32_t* bufB = sB;
+        if (wide) {
+            const size_t gs = static_cast<size_t>(a.pmax) + 2 * kSent;
+            bufA = a.scratch + static_cast<size_t>(line) * 2 * gs + kSent;
+            bufB = bufA + gs;
+            if (lc.gl < kSent) {
+                bufA[-kSent + lc.gl] = kSentinel;
+                bufB[-kSent + lc.gl] = kSentinel;
+            }
+        }
+        __syncwarp();
+        line_steps<SN, G, K, S, GAP, false>(a, lc, bufA, bufB);
+    } else {
+        __syncwarp();
+        line_steps<SN, G, K, S, GAP, true>(a, lc, sA, sB);
     }
 }
 
@@ -978,7 +1024,7 @@ void launch_lanes(const SgmArgs& a, int total, cudaStream_t s) {
 template <int VARIANT, typename V>
 void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
     const int g = a.group, k = a.kper;
-    if (g == 4 && k == 4)
+    if (g == 4 && (k == 4 || k == 3))  // K = 3 is a line-kernel blocking
         launch_lanes<VARIANT, V, 4, 4>(a, total, s);
     else if (g == 8 && k == 2)
         launch_lanes<VARIANT, V, 8, 2>(a, total, s);
@@ -994,12 +1040,13 @@ void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
         throw Error(FMVS_ERR_CONFIG, "sgm: unsupported lane blocking");
 }
 
-template <bool SN, int G, int K>
-void launch_line(const SgmArgs& a, int total, cudaStream_t s) {
+template <bool SN, int G, int K, int S, int GAP>
+void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
+
     constexpr int LPW = 32 / G;
-    constexpr int S = K >= 8 ? 4 : 6;
-    constexpr int GAP = K >= 8 ? 1 : 2;
-    const int caps = a.group_caps;
+    // a line is narrow when every pixel fits one pass (its shared buffers
+    // hold G*K slots); wider lines run from their global scratch
+    const int caps = G * K;
     int stride = 2 * (caps + 2 * kSent);
     stride += ((G % 32) - stride % 32 + 32) % 32;
     const int blocks = (total + kWarps * LPW - 1) / (kWarps * LPW);
@@ -1011,13 +1058,36 @@ void launch_line(const SgmArgs& a, int total, cudaStream_t s) {
     sgm_prep_kernel<<<(npx + 255) / 256, 256, 0, s>>>(a, rec, fl, caps);
     FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_line_kernel<SN, G, K, S, GAP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    sgm_line_kernel<SN, G, K, S, GAP><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, caps, stride);
+    sgm_line_kernel<SN, G, K, S, GAP><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
+}
+
+// Pipeline depth S (pixels whose records are in registers) and GAP (steps
+// between a pixel's record and cost loads): the cost loads of a refined level
+// miss L2 about half the time, so they are issued S-1-GAP steps ahead.
+template <bool SN, int G, int K>
+void launch_line(const SgmArgs& a, int total, cudaStream_t s) {
+    static const int depth = [] {
+        const char* e = std::getenv("FMVS_SGM_DEPTH");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (K >= 8)
+        launch_line_sg<SN, G, K, 4, 1>(a, total, s);
+    else if (depth == 6)
+        launch_line_sg<SN, G, K, 6, 2>(a, total, s);
+    else if (depth == 10)
+        launch_line_sg<SN, G, K, 10, 4>(a, total, s);
+    else if (depth == 12)
+        launch_line_sg<SN, G, K, 12, 5>(a, total, s);
+    else
+        launch_line_sg<SN, G, K, 8, 3>(a, total, s);
 }
 
 template <bool SN>
 bool launch_line_gk(const SgmArgs& a, int total, cudaStream_t s) {
     if (a.group == 4 && a.kper == 4)
         launch_line<SN, 4, 4>(a, total, s);
+    else if (a.group == 4 && a.kper == 3)
+        launch_line<SN, 4, 3>(a, total, s);
     else if (a.group == 32 && a.kper == 4)
         launch_line<SN, 32, 4>(a, total, s);
     else if (a.group == 32 && a.kper == 8)

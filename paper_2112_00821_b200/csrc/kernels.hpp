@@ -142,8 +142,9 @@ struct SgmArgs {
     uint64_t entries_bound;
 };
 void sgm(const SgmArgs& a, cudaStream_t s);
-// entries every aggregate allocation carries past the volume (the line
-// kernel's inactive lanes add 0 there)
+// entries every cost and aggregate allocation carries past the volume (the
+// line kernel's inactive lanes add 0 there; its cost staging reads aligned
+// 16-byte chunks that may extend up to 46 bytes past a pixel's last cost)
 constexpr size_t kAggSlack = 64;
 size_t sgm_line_scratch_words(int w, int h);
 int sgm_total_lines(int w, int h, int ndirs);

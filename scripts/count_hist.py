@@ -27,3 +27,5 @@ for lvl in range(cfg.pyramid_levels):
         ys, xs = np.nonzero(wide)
         d1 = len(np.unique(xs - ys)) / (hh + ww - 1)
         print(f"   cap {capv}: rows with a wide pixel {100*rows:.1f}%  cols {100*cols:.1f}%  diagonals {100*d1:.1f}%")
+    bc = np.bincount(np.minimum(cnt.ravel(), 40), minlength=41)
+    print("   count histogram (0..39, >=40):", " ".join(f"{i}:{v}" for i, v in enumerate(bc) if v))
