@@ -634,11 +634,15 @@ done:
 // Same recurrence and mapping as sgm_lanes_kernel (G lanes per scanline, K
 // hypotheses per lane and pass), restructured so that a step costs few
 // instructions:
-//  * every per-pixel operand of a step comes from ONE 16-byte record built
-//    per level by sgm_prep_kernel (32-bit entry index; first | count << 11 |
-//    intensity << 23; the four SN shifts), so a step issues one record load
-//    instead of meta + row base + image + SN loads and their 64-bit address
-//    arithmetic; records past the end of a line read a zero dummy record;
+//  * every per-pixel operand of a step comes from ONE 48-byte record built
+//    per level by sgm_prep_kernel: a 16-byte head (32-bit entry index; first
+//    | count << 11 | intensity << 23; the four SN shifts) and, for pixels of
+//    <= kEmbed hypotheses, a copy of the pixel's u16 costs laid out per lane
+//    (slot 4*gl + k holds hypothesis gl + 4k), so a step issues one head load
+//    and one 8-byte cost load per lane, both addressed by the pixel index
+//    alone: no load waits on another (instead of meta + row base + image +
+//    SN loads, then cost loads addressed by the meta); records past the end
+//    of a line read a zero dummy record;
 //  * the line's length is known at its start (no per-step inside tests, the
 //    warp runs max-length steps);
 //  * the path buffers of a line live in ONE address space for the whole line,
@@ -653,6 +657,8 @@ done:
 // Records hold 32-bit entry indices and <= kRecPlanes planes (host-checked;
 // other volumes take the general kernel).
 constexpr int kRecPlanes = 2048;
+constexpr int kRecWords = 12;  // 48-byte record: head + 16 embedded u16 costs
+constexpr int kEmbed = 16;     // pixels with more hypotheses keep only the head
 
 __device__ __forceinline__ int rec_first(uint32_t pk) { return static_cast<int>(pk & 0x7FFu); }
 __device__ __forceinline__ int rec_count(uint32_t pk) { return static_cast<int>((pk >> 11) & 0xFFFu); }
@@ -692,30 +698,53 @@ __device__ __forceinline__ void red_add(uint32_t* agg, bool p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0+%1], %2;" : : "l"(agg), "n"(OFF), "r"(p ? v : 0u));
 }
 
-__global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps) {
+__global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps, bool embed) {
     const int n = a.w * a.h;
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p > n)
         return;
+    uint4* r = rec + 3 * static_cast<size_t>(p);
     if (p == n) {  // the dummy record read past the end of a line
-        rec[p] = make_uint4(0u, 0u, 0u, 0u);
+        r[0] = r[1] = r[2] = make_uint4(0u, 0u, 0u, 0u);
         return;
     }
     const int y = p / a.w, x = p - y * a.w;
     const dev::VolMeta m = a.meta[p];
     const int c = dev::meta_count(m.fc);
-    uint4 r;
-    r.x = static_cast<uint32_t>(a.row_base[y] + m.rel);
-    r.y = (c > 0 ? static_cast<uint32_t>(dev::meta_first(m.fc)) : 0u) | static_cast<uint32_t>(c) << 11 |
+    const uint64_t base = a.row_base[y] + m.rel;
+    uint4 h;
+    h.x = static_cast<uint32_t>(base);
+    h.y = (c > 0 ? static_cast<uint32_t>(dev::meta_first(m.fc)) : 0u) | static_cast<uint32_t>(c) << 11 |
           static_cast<uint32_t>(a.image[p]) << 23;
     if (a.offsets) {
         const uint2 o = reinterpret_cast<const uint2*>(a.offsets)[p];
-        r.z = o.x;
-        r.w = o.y;
+        h.z = o.x;
+        h.w = o.y;
     } else {
-        r.z = r.w = 0u;
+        h.z = h.w = 0u;
     }
-    rec[p] = r;
+    r[0] = h;
+    if (!embed)
+        goto flags;
+    {
+    // embedded costs, lane-major: u16 slot 4*gl + k = hypothesis gl + 4k
+    uint32_t e[8];
+#pragma unroll
+    for (int sl = 0; sl < 16; sl += 2) {
+        uint32_t v2 = 0u;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int slot = sl + h2;
+            const int i = (slot >> 2) + 4 * (slot & 3);
+            if (c <= kEmbed && i < c)
+                v2 |= static_cast<uint32_t>(a.costs[base + i]) << (16 * h2);
+        }
+        e[sl >> 1] = v2;
+    }
+    r[1] = make_uint4(e[0], e[1], e[2], e[3]);
+    r[2] = make_uint4(e[4], e[5], e[6], e[7]);
+    }
+flags:
     if (c > caps) {
         atomicOr(fl.row + y, 1u);
         atomicOr(fl.col + x, 1u);
@@ -740,27 +769,50 @@ struct LineCtx {
 
 // Operand pipeline of the line kernel: records of pixels j+1..j+S-1 and the
 // costs / phi2 of pixels j+1..j+S-1-GAP in registers at the step of pixel j.
-template <bool SN, int G, int K, int S, int GAP>
+// EMB: the costs come with the record (embedded copy, G = 4, K <= 4) and phi2
+// is looked up at use; otherwise they are loaded GAP steps after the record.
+template <bool SN, int G, int K, int S, int GAP, bool EMB>
 struct LinePipe {
+    static_assert(!EMB || (G == 4 && K <= 4), "embedded costs hold 4 slots for 4 lanes");
     uint4 R[S];
-    uint32_t C[S][K];
-    int PH[S];
+    uint2 E[EMB ? S : 1];
+    uint32_t C[EMB ? 1 : S][K];
+    int PH[EMB ? 1 : S];
     int q, jn;
 
-    __device__ __forceinline__ void load_rec(const LineCtx& lc, uint4& r) {
+    __device__ __forceinline__ void load_rec(const LineCtx& lc, int si) {
         const int idx = jn < lc.n ? q : lc.dummy;
+        const uint4* r = lc.rec + 3 * idx;
         if (SN) {
-            r = __ldg(lc.rec + idx);
+            R[si] = __ldg(r);
         } else {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(lc.rec + idx));
-            r.x = v.x;
-            r.y = v.y;
-            r.z = r.w = 0u;
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(r));
+            R[si].x = v.x;
+            R[si].y = v.y;
+            R[si].z = R[si].w = 0u;
         }
+        if constexpr (EMB)
+            E[si] = __ldg(reinterpret_cast<const uint2*>(r + 1) + lc.gl);
         q += lc.dp;
         ++jn;
     }
+    // first-pass cost k of the pixel in slot u
+    __device__ __forceinline__ uint32_t cost(int u, int k) const {
+        if constexpr (EMB)
+            return ((k < 2 ? E[u].x : E[u].y) >> (16 * (k & 1))) & 0xFFFFu;
+        else
+            return C[u][k];
+    }
+    // phi2 of the transition into the pixel in slot u from intensity img_prev
+    __device__ __forceinline__ int phi2(const LineCtx& lc, int u, int img_prev) const {
+        if constexpr (EMB)
+            return lc.lut[abs(rec_img(R[u].y) - img_prev)];
+        else
+            return PH[u];
+    }
     __device__ __forceinline__ void load_costs(const SgmArgs& a, const LineCtx& lc, int si, int sp) {
+        if constexpr (EMB)
+            return;
         const uint32_t pk = R[si].y;
         const int c = rec_count(pk);
         const uint16_t* cp = a.costs + (R[si].x + lc.gl);
@@ -775,7 +827,7 @@ struct LinePipe {
         jn = 0;
 #pragma unroll
         for (int j = 0; j < S - 1; ++j)
-            load_rec(lc, R[j]);
+            load_rec(lc, j);
         R[S - 1] = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int j = 0; j < S - 1 - GAP; ++j)
@@ -784,7 +836,7 @@ struct LinePipe {
     // at the step in slot u: record of pixel j+S-1 (into the slot of pixel
     // j-1), costs of pixel j+S-1-GAP (its record arrived GAP steps ago)
     __device__ __forceinline__ void advance(const SgmArgs& a, const LineCtx& lc, int u) {
-        load_rec(lc, R[(u + S - 1) % S]);
+        load_rec(lc, (u + S - 1) % S);
         load_costs(a, lc, (u + S - 1 - GAP) % S, (u + S - 2 - GAP) % S);
     }
     __device__ __forceinline__ int shift(const LineCtx& lc, int u) const {
@@ -802,15 +854,15 @@ struct LinePipe {
 // step bodies, with the predecessor window loaded a step early, ran 1.8x
 // slower at level 0, with the same loads staged through shared memory by
 // cp.async too).
-template <bool SN, int G, int K, int S, int GAP, bool SHARED>
+template <bool SN, int G, int K, int S, int GAP, bool SHARED, bool EMB>
 __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, uint32_t* bufA,
                                           uint32_t* bufB) {
     constexpr int PASS = G * K;
     const int gl = lc.gl;
     const int phi1 = static_cast<int>(a.phi1);
-    LinePipe<SN, G, K, S, GAP> P;
+    LinePipe<SN, G, K, S, GAP, EMB> P;
     P.start(a, lc);
-    int prev_first = 0, prev_count = 0, prev_min = 0;
+    int prev_first = 0, prev_count = 0, prev_min = 0, img_prev = 0;
     bool has_prev = false;
     for (int j0 = 0; j0 < lc.steps; j0 += S) {
 #pragma unroll
@@ -825,7 +877,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                 const int shift = (SN && has_prev) ? P.shift(lc, u) : 0;
                 const int toff = has_prev ? f + shift - prev_first : -0x40000000;
                 const int pm = has_prev ? prev_min : 0;
-                const int bp = has_prev ? prev_min + P.PH[u] : 0;
+                const int bp = has_prev ? prev_min + P.phi2(lc, u, img_prev) : 0;
                 const int tmax = prev_count + 1;
                 const uint32_t ib = P.R[u].x + gl;
                 auto pass = [&](int i0, const uint32_t* sc) {
@@ -844,7 +896,11 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                         run_min = min(run_min, i < c ? v : 0xFFFFFFFFu);
                     });
                 };
-                pass(0, P.C[u]);
+                uint32_t sc0[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    sc0[k] = P.cost(u, k);
+                pass(0, sc0);
                 for (int i0 = PASS; i0 < c; i0 += PASS) {
                     const uint16_t* cp = a.costs + (ib + i0);
                     uint32_t sc[K];
@@ -864,11 +920,12 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                 prev_count = c;
             }
             has_prev = c > 0;
+            img_prev = rec_img(pk);
         }
     }
 }
 
-template <bool SN, int G, int K, int S, int GAP>
+template <bool SN, int G, int K, int S, int GAP, bool EMB>
 __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const uint4* __restrict__ rec,
                                                                LineFlags fl, int total_lines, int stride) {
     constexpr int LPW = 32 / G;
@@ -930,10 +987,10 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
             }
         }
         __syncwarp();
-        line_steps<SN, G, K, S, GAP, false>(a, lc, bufA, bufB);
+        line_steps<SN, G, K, S, GAP, false, false>(a, lc, bufA, bufB);
     } else {
         __syncwarp();
-        line_steps<SN, G, K, S, GAP, true>(a, lc, sA, sB);
+        line_steps<SN, G, K, S, GAP, true, EMB>(a, lc, sA, sB);
     }
 }
 
@@ -1052,13 +1109,25 @@ void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
     const int blocks = (total + kWarps * LPW - 1) / (kWarps * LPW);
     const size_t smem = (256 + static_cast<size_t>(kWarps) * LPW * stride) * sizeof(uint32_t);
     auto* rec = reinterpret_cast<uint4*>(a.line_scratch);
-    const LineFlags fl = line_flags(a.line_scratch + 4 * (static_cast<size_t>(a.w) * a.h + 1), a.w, a.h);
+    const LineFlags fl = line_flags(a.line_scratch + kRecWords * (static_cast<size_t>(a.w) * a.h + 1), a.w, a.h);
     FMVS_CUDA_CHECK(cudaMemsetAsync(fl.row, 0, line_flag_words(a.w, a.h) * sizeof(uint32_t), s));
     const int npx = a.w * a.h + 1;
-    sgm_prep_kernel<<<(npx + 255) / 256, 256, 0, s>>>(a, rec, fl, caps);
-    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_line_kernel<SN, G, K, S, GAP>,
+    // embedded costs (G = 4, K <= 4; FMVS_SGM_EMB=0 keeps them in the volume)
+    static const bool emb_on = [] {
+        const char* e = std::getenv("FMVS_SGM_EMB");
+        return !(e && e[0] == '0');
+    }();
+    constexpr bool kEmb = G == 4 && K <= 4;
+    const bool emb = kEmb && emb_on;
+    sgm_prep_kernel<<<(npx + 255) / 256, 256, 0, s>>>(a, rec, fl, caps, emb);
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_line_kernel<SN, G, K, S, GAP, kEmb>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    sgm_line_kernel<SN, G, K, S, GAP><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_line_kernel<SN, G, K, S, GAP, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (emb)
+        sgm_line_kernel<SN, G, K, S, GAP, kEmb><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
+    else
+        sgm_line_kernel<SN, G, K, S, GAP, false><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
 }
 
 // Pipeline depth S (pixels whose records are in registers) and GAP (steps
@@ -1098,7 +1167,7 @@ bool launch_line_gk(const SgmArgs& a, int total, cudaStream_t s) {
 }
 
 size_t sgm_line_scratch_words(int w, int h) {
-    return 4 * (static_cast<size_t>(w) * h + 1) + line_flag_words(w, h);
+    return static_cast<size_t>(kRecWords) * (static_cast<size_t>(w) * h + 1) + line_flag_words(w, h);
 }
 
 void sgm(const SgmArgs& a, cudaStream_t s) {
