@@ -258,7 +258,7 @@ struct fmvs_ctx {
     // optional per-stage CUDA-event timing (bench.py roofline numbers)
     bool timing = false;
     int sweep_exact = 0;  // FMVS_SWEEP_EXACT=1: force the exact per-hypothesis sweep
-    int sweep_stats = 0;  // FMVS_SWEEP_STATS=1: count certified-census fallbacks
+    int sweep_stats = 0;  // FMVS_SWEEP_STATS=1 (2 + l: level l only): count certified-census fallbacks
     // stage capture of one level (fmvs_ctx_set_capture)
     struct Capture {
         int level = -1;
@@ -589,7 +589,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         sa.disable_tiled = ctx->sweep_exact;
         sa.plane_slicing = l == L - 1;  // uniform ranges: every pixel sweeps the whole stack
         sa.narrow_max = l == L - 1 ? 65535 : 0;
-        if (ctx->sweep_stats)
+        if (ctx->sweep_stats == 1 || ctx->sweep_stats == 2 + l)
             sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(8);
         ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { launches += k::sweep(sa, s); });
         // the SGM accumulator of the level (make_accumulator, sgm.cpp:198-208)
@@ -842,7 +842,7 @@ int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
         if (const char* e = std::getenv("FMVS_SWEEP_EXACT"))
             ctx->sweep_exact = std::atoi(e) != 0;
         if (const char* e = std::getenv("FMVS_SWEEP_STATS"))
-            ctx->sweep_stats = std::atoi(e) != 0;
+            ctx->sweep_stats = std::atoi(e);  // 1: every level; 2 + l: level l only
         ctx->use();
         FMVS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         FMVS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->staged, cudaEventDisableTiming));

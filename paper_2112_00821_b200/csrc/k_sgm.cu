@@ -1187,6 +1187,7 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
     for (int d = 0; d < a.ndirs; ++d)
         unit = unit && std::abs(a.dirs[d][0]) <= 1 && std::abs(a.dirs[d][1]) <= 1 &&
                (a.dirs[d][0] != 0 || a.dirs[d][1] != 0);
+    static_assert(kAggSlack >= 32 * 8, "inactive lanes of a pass add 0 up to G*K - 1 entries past a pixel");
     if (line_on && a.line_scratch && a.scratch && fast32 && unit && a.group > 0 &&
         a.variant != FMVS_SGM_PATH_GRADIENT && a.nplanes <= kRecPlanes &&
         a.entries_bound + 1024 < (1ull << 32)) {

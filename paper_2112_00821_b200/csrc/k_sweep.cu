@@ -672,8 +672,10 @@ __device__ __forceinline__ float2 ncc_sample(uint32_t q, float ax, float ay, flo
     const float top = fmaf(ax, i10 - i00, i00);
     const float bot = fmaf(ax, i11 - i01, i01);
     const float f = fmaf(ay, bot - top, top);
-    // the float cast of (t - floor t) adds 2^-24 to the coordinate error
-    const float ddx = dx + 6.0e-8f, ddy = dy + 6.0e-8f;
+    // the float cast of (t - floor t) adds 2^-24 to the coordinate error; a
+    // negative dx / dy marks an axis certainly clamped at the view edge (the
+    // sample does not depend on it: no error along it)
+    const float ddx = dx < 0.0f ? 0.0f : dx + 6.0e-8f, ddy = dy < 0.0f ? 0.0f : dy + 6.0e-8f;
     const bool near_x = ax < ddx || ax > 1.0f - ddx;
     const bool near_y = ay < ddy || ay > 1.0f - ddy;
     const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
@@ -704,11 +706,33 @@ __device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const Vi
     const double fx = floor(tx), fy = floor(ty);
     int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
     float ax = __double2float_rn(tx - fx), ay = __double2float_rn(ty - fy);
-    if (X0 < 0) { X0 = 0; ax = 0.0f; }
-    else if (X0 >= vc.w - 1) { X0 = vc.w - 1; ax = 0.0f; }
-    if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
-    else if (Y0 >= vc.h - 1) { Y0 = vc.h - 1; ay = 0.0f; }
-    return ncc_sample(__ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0), ax, ay, tp.dx, tp.dy);
+    // edge clamp (raster.hpp:71-84); a coordinate certainly past the edge
+    // leaves the reference's sample independent of it (see the census path)
+    float ddx = tp.dx, ddy = tp.dy;
+    const double ex = double(tp.dx) + 1e-9, ey = double(tp.dy) + 1e-9;
+    if (X0 < 0) {
+        X0 = 0;
+        ax = 0.0f;
+        if (double(tp.xa) + tx + ex < 0.0)
+            ddx = -1.0f;
+    } else if (X0 >= vc.w - 1) {
+        X0 = vc.w - 1;
+        ax = 0.0f;
+        if (double(tp.xa) + tx - ex >= double(vc.w - 1))
+            ddx = -1.0f;
+    }
+    if (Y0 < 0) {
+        Y0 = 0;
+        ay = 0.0f;
+        if (double(tp.ya) + ty + ey < 0.0)
+            ddy = -1.0f;
+    } else if (Y0 >= vc.h - 1) {
+        Y0 = vc.h - 1;
+        ay = 0.0f;
+        if (double(tp.ya) + ty - ey >= double(vc.h - 1))
+            ddy = -1.0f;
+    }
+    return ncc_sample(__ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0), ax, ay, ddx, ddy);
 }
 
 // tile_sample64 of a kTileInterior tile: no clamping, no inside flag.
@@ -747,7 +771,13 @@ __device__ __forceinline__ float2 census_sample(uint32_t q, float ax, float ay, 
     const bool near_y = ay < dy || ay > 1.0f - dy;
     const float gx = near_x ? 255.0f : fmaxf(fabsf(i10 - i00), fabsf(i11 - i01));
     const float gy = near_y ? 255.0f : fmaxf(fabsf(i01 - i00), fabsf(i11 - i10));
-    const float e = fmaf(gx, dx, fmaf(gy, dy, 2.0e-4f));
+    // FP32 bilinear rounding: the tap differences are exact, top / bot / f
+    // each round once (<= 2^-17 below 256) and bot - top once, carrying the
+    // errors of top and bot: |f - f_exact| <= 5 * 2^-17 < 4e-5 (the
+    // reference's FP64 bilinear adds < 1e-13). A flat cell away from its edges
+    // (gx = gy = 0: four equal taps, the reference's sample provably in this
+    // cell) is exact in both: zero bound.
+    const float e = fmaf(gx, dx, fmaf(gy, dy, gx + gy > 0.0f ? 4.0e-5f : 0.0f));
     return make_float2(__fsub_rd(f, e), __fadd_ru(f, e));
 }
 
@@ -902,11 +932,35 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
                     const float fx = floorf(tcx), fy = floorf(tcy);
                     int X0 = tp.xa + static_cast<int>(fx), Y0 = tp.ya + static_cast<int>(fy);
                     float ax = tcx - fx, ay = tcy - fy;
-                    if (X0 < 0) { X0 = 0; ax = 0.0f; }
-                    else if (X0 >= vw - 1) { X0 = vw - 1; ax = 0.0f; }
-                    if (Y0 < 0) { Y0 = 0; ay = 0.0f; }
-                    else if (Y0 >= vh - 1) { Y0 = vh - 1; ay = 0.0f; }
-                    t[r] = census_sample(__ldg(quad + (Y0 * vw + X0)), ax, ay, tp.dx, tp.dy);
+                    // edge clamp (raster.hpp:71-84). When the reference's
+                    // coordinate is CERTAINLY past the edge its sample does not
+                    // depend on that coordinate at all (a = 0 there too): no
+                    // coordinate error along that axis (otherwise the clamped
+                    // a = 0 reads as "near a cell edge", Lipschitz 255)
+                    float ddx = tp.dx, ddy = tp.dy;
+                    if (X0 < 0) {
+                        X0 = 0;
+                        ax = 0.0f;
+                        if (__fadd_ru(tcx, tp.dx) < xlo)
+                            ddx = 0.0f;
+                    } else if (X0 >= vw - 1) {
+                        X0 = vw - 1;
+                        ax = 0.0f;
+                        if (__fsub_rd(tcx, tp.dx) >= xhi)
+                            ddx = 0.0f;
+                    }
+                    if (Y0 < 0) {
+                        Y0 = 0;
+                        ay = 0.0f;
+                        if (__fadd_ru(tcy, tp.dy) < ylo)
+                            ddy = 0.0f;
+                    } else if (Y0 >= vh - 1) {
+                        Y0 = vh - 1;
+                        ay = 0.0f;
+                        if (__fsub_rd(tcy, tp.dy) >= yhi)
+                            ddy = 0.0f;
+                    }
+                    t[r] = census_sample(__ldg(quad + (Y0 * vw + X0)), ax, ay, ddx, ddy);
                     du += kTPV % SW;
                     dv += kTPV / SW;
                     if (du >= SW) {
@@ -917,6 +971,8 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
             }
         }
         __syncthreads();  // T
+        if (a.stats && need)
+            atomicAdd(a.stats + 7, 1ull);  // useful (pixel, plane) slots of the iteration
         // ---- pass 1: FP32 census bits; undecided-bit masks only where needed
         BitsT bits[NM], uns[NM];
         uint32_t view_out = 0;    // bit m: window centre outside the view -> 255

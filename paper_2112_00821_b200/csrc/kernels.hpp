@@ -145,7 +145,7 @@ void sgm(const SgmArgs& a, cudaStream_t s);
 // entries every cost and aggregate allocation carries past the volume (the
 // line kernel's inactive lanes add 0 there; its cost staging reads aligned
 // 16-byte chunks that may extend up to 46 bytes past a pixel's last cost)
-constexpr size_t kAggSlack = 64;
+constexpr size_t kAggSlack = 256;  // >= the widest pass (G x K = 32 x 8)
 size_t sgm_line_scratch_words(int w, int h);
 int sgm_total_lines(int w, int h, int ndirs);
 // Lines of the given path directions (any step, sgm.cpp:213-219).

@@ -1,12 +1,25 @@
-# ncu evidence for the bench command: launch list (cold, serialised) and one
-# --set full capture per dominant kernel (L0 launch of bundle 2).
-set -x
-mkdir -p gpurun_out
-B="python bench.py --steps 2 --warmup 1 --inflight 1 --ring 2 --no-cpu-baseline"
+# ncu evidence for one bench workload ($WL, default c2): the launch list of the
+# bench command (cold, serialised) and one --set full capture of the level-0
+# launch of each stage's kernel (sweep_l0, sgm_l0), named by stage so
+# scripts/ncu_summary.py keys them the way bench.py reads them.
+#   WL=c3 bash scripts/ncu_capture.sh   -> gpurun_out/ncu_$WL/
+WL=${WL:-c2}
+OUT=gpurun_out/ncu_$WL
+mkdir -p $OUT
+B="python bench.py --workload $WL --steps 2 --warmup 1 --inflight 1 --ring 2 --no-cpu-baseline"
+case $WL in
+  c2|c2pg|c5) SW=sweep_census_tiled; SKIP=5 ;;   # 3 tiled sweeps / SGM launches per bundle: L2, L1, L0
+  c2ncc|c4)   SW=sweep_ncc_tiled; SKIP=5 ;;
+  c3)         SW=sweep_ncc_tiled; SKIP=2 ;;      # one level
+  c1)         SW=sweep_census_tiled; SKIP=2 ;;
+esac
+SG=sgm_line_kernel
+[ $WL = c2pg ] && SG=sgm_lanes_kernel
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1; echo launches rc=$?
-for k in ${NCU_KERNELS:-sweep_census_tiled sgm_lanes_kernel}; do
+  --log-file $OUT/launches.csv $B > $OUT/ncu_launch.log 2>&1; echo launches rc=$?
+for st in sweep_l0:$SW sgm_l0:$SG; do
+  name=${st%%:*}; k=${st#*:}
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k \
-    --launch-skip ${NCU_SKIP:-5} -c 1 -f -o gpurun_out/full_$k $B > gpurun_out/ncu_full_$k.log 2>&1
-  echo full $k rc=$?
+    --launch-skip $SKIP -c 1 -f -o $OUT/full_$name $B > $OUT/ncu_full_$name.log 2>&1
+  echo "full $name ($k) rc=$?"
 done

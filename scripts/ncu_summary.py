@@ -2,7 +2,7 @@
 (gpu__time_duration per launch, cold/serialised) -> per-kernel share; (2) one
 `--set full` capture per kernel -> key metrics incl. DRAM traffic per launch.
 
-usage: python scripts/ncu_summary.py <gpurun_out dir> <out prefix>
+usage: python scripts/ncu_summary.py <gpurun_out/ncu_WL dir> <out prefix> [command]
 writes <prefix>_launches.txt and <prefix>_full.json
 """
 import collections
@@ -74,7 +74,9 @@ for rep in sorted(glob.glob(os.path.join(src, "full_*.ncu-rep"))):
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             tb += m.get(k, 0.0) * scale.get(m.get(k + ".unit", "byte"), 1)
         m["dram_bytes_per_launch"] = tb
-        out[os.path.basename(rep).replace(".ncu-rep", "")] = {"kernel": d["Kernel Name"],
+        key = os.path.basename(rep).replace(".ncu-rep", "")
+        key = key[len("full_"):] if key.startswith("full_") else key  # stage name (bench.py)
+        out[key] = {"kernel": d["Kernel Name"],
                                                                "grid": d.get("launch__grid_size"), **m}
 with open(prefix + "_full.json", "w") as f:
     json.dump(out, f, indent=1)
