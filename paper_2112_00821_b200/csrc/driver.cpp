@@ -514,7 +514,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         size_t lines = 0;
         for (auto& P : lv)
             lines = std::max(lines, static_cast<size_t>(k::sgm_total_lines(P.w, P.h, 8)));
-        sgm_scratch = ctx->buf("sgm_scratch").as<uint32_t>(lines * 2 * (max_p + 8));
+        sgm_scratch = ctx->buf("sgm_scratch").as<uint32_t>(lines * 2 * (max_p + k::kSgmLinePad));
     }
     uint32_t* sgm_line = ctx->buf("sgm_line").as<uint32_t>(k::sgm_line_scratch_words(lv[0].w, lv[0].h));
 
@@ -1420,7 +1420,7 @@ int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         const int limit = (200 * 1024) / (4 * 2 * 4);
         if (pmax > limit || ga.group > 0) {
             const size_t lines = static_cast<size_t>(k::sgm_lines(w, h, ga.dirs, ga.ndirs));
-            ga.scratch = t.alloc<uint32_t>(lines * 2 * (pmax + 8));
+            ga.scratch = t.alloc<uint32_t>(lines * 2 * (pmax + k::kSgmLinePad));
         }
         ga.line_scratch = t.alloc<uint32_t>(k::sgm_line_scratch_words(w, h));
         ga.entries_bound = total;

@@ -803,13 +803,6 @@ struct LinePipe {
         else
             return C[u][k];
     }
-    // phi2 of the transition into the pixel in slot u from intensity img_prev
-    __device__ __forceinline__ int phi2(const LineCtx& lc, int u, int img_prev) const {
-        if constexpr (EMB)
-            return lc.lut[abs(rec_img(R[u].y) - img_prev)];
-        else
-            return PH[u];
-    }
     __device__ __forceinline__ void load_costs(const SgmArgs& a, const LineCtx& lc, int si, int sp) {
         if constexpr (EMB)
             return;
@@ -862,7 +855,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
     const int phi1 = static_cast<int>(a.phi1);
     LinePipe<SN, G, K, S, GAP, EMB> P;
     P.start(a, lc);
-    int prev_first = 0, prev_count = 0, prev_min = 0, img_prev = 0;
+    int prev_first = 0, prev_count = 0, prev_min = 0, ph = 0;
     bool has_prev = false;
     for (int j0 = 0; j0 < lc.steps; j0 += S) {
 #pragma unroll
@@ -877,7 +870,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                 const int shift = (SN && has_prev) ? P.shift(lc, u) : 0;
                 const int toff = has_prev ? f + shift - prev_first : -0x40000000;
                 const int pm = has_prev ? prev_min : 0;
-                const int bp = has_prev ? prev_min + P.phi2(lc, u, img_prev) : 0;
+                const int bp = has_prev ? prev_min + (EMB ? ph : P.PH[u]) : 0;
                 const int tmax = prev_count + 1;
                 const uint32_t ib = P.R[u].x + gl;
                 auto pass = [&](int i0, const uint32_t* sc) {
@@ -920,7 +913,8 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                 prev_count = c;
             }
             has_prev = c > 0;
-            img_prev = rec_img(pk);
+            if (EMB)  // phi2 of the transition into the next pixel, a step ahead
+                ph = lc.lut[abs(rec_img(P.R[(u + 1) % S].y) - rec_img(pk))];
         }
     }
 }

@@ -147,6 +147,9 @@ void sgm(const SgmArgs& a, cudaStream_t s);
 // 16-byte chunks that may extend up to 46 bytes past a pixel's last cost)
 constexpr size_t kAggSlack = 256;  // >= the widest pass (G x K = 32 x 8)
 size_t sgm_line_scratch_words(int w, int h);
+// per-line global path buffers (SgmArgs::scratch): 2 x (pmax + kSgmLinePad)
+// words per line (sentinel slots of either SGM kernel)
+constexpr int kSgmLinePad = 32;
 int sgm_total_lines(int w, int h, int ndirs);
 // Lines of the given path directions (any step, sgm.cpp:213-219).
 int sgm_lines(int w, int h, const int (*dirs)[2], int ndirs);
