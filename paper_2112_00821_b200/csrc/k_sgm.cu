@@ -855,8 +855,15 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
     const int phi1 = static_cast<int>(a.phi1);
     LinePipe<SN, G, K, S, GAP, EMB> P;
     P.start(a, lc);
-    int prev_first = 0, prev_count = 0, prev_min = 0, ph = 0;
+    int prev_count = 0, prev_min = 0, ph = 0, toff = -0x40000000;
     bool has_prev = false;
+    // first-pass predecessor window of the current pixel (prev[t-1], prev[t],
+    // prev[t+1] per slot), loaded at the end of the previous step so the
+    // loads overlap the group-minimum shuffles
+    int W0[K], W1[K], W2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        W0[k] = W1[k] = W2[k] = static_cast<int>(kSentinel);
     for (int j0 = 0; j0 < lc.steps; j0 += S) {
 #pragma unroll
         for (int u = 0; u < S; ++u) {
@@ -867,21 +874,28 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
             const int c = rec_count(pk), f = rec_first(pk);
             uint32_t run_min = 0xFFFFFFFFu;
             if (c > 0) {
-                const int shift = (SN && has_prev) ? P.shift(lc, u) : 0;
-                const int toff = has_prev ? f + shift - prev_first : -0x40000000;
                 const int pm = has_prev ? prev_min : 0;
                 const int bp = has_prev ? prev_min + (EMB ? ph : P.PH[u]) : 0;
                 const int tmax = prev_count + 1;
                 const uint32_t ib = P.R[u].x + gl;
-                auto pass = [&](int i0, const uint32_t* sc) {
+                auto pass = [&](int i0, const uint32_t* sc, bool first) {
                     uint32_t* ap = a.agg + (ib + i0);
                     uint32_t* cp = cur + (gl + i0);
                     static_for<K>([&](auto kc) {
                         constexpr int k = decltype(kc)::value;
                         const int i = i0 + gl + G * k;
-                        const int t = min(max(toff + i, -2), tmax);
-                        const int b3 = min(static_cast<int>(prev[t - 1]), static_cast<int>(prev[t + 1])) + phi1;
-                        const int best = min(min(bp, static_cast<int>(prev[t])), b3);
+                        int w0, w1, w2;
+                        if (first) {
+                            w0 = W0[k];
+                            w1 = W1[k];
+                            w2 = W2[k];
+                        } else {
+                            const int t = min(max(toff + i, -2), tmax);
+                            w0 = static_cast<int>(prev[t - 1]);
+                            w1 = static_cast<int>(prev[t]);
+                            w2 = static_cast<int>(prev[t + 1]);
+                        }
+                        const int best = min(min(bp, w1), min(w0, w2) + phi1);
                         const uint32_t v = sc[k] + static_cast<uint32_t>(best - pm);
                         if (i < c)
                             cp[G * k] = v;
@@ -893,23 +907,36 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
 #pragma unroll
                 for (int k = 0; k < K; ++k)
                     sc0[k] = P.cost(u, k);
-                pass(0, sc0);
+                pass(0, sc0, true);
                 for (int i0 = PASS; i0 < c; i0 += PASS) {
                     const uint16_t* cp = a.costs + (ib + i0);
                     uint32_t sc[K];
 #pragma unroll
                     for (int k = 0; k < K; ++k)
                         sc[k] = i0 + gl + G * k < c ? cp[G * k] : 0u;
-                    pass(i0, sc);
+                    pass(i0, sc, false);
                 }
                 if (gl < kSent)
                     cur[c + gl] = kSentinel;
             }
-            const uint32_t nmin = group_min<G>(run_min);
             __syncwarp();
+            // predecessor window of pixel j+1 in this pixel's buffer (an empty
+            // pixel leaves only the permanent left sentinels in reach)
+            {
+                const int u1 = (u + 1) % S;
+                const int shift = SN ? P.shift(lc, u1) : 0;
+                toff = c > 0 ? rec_first(P.R[u1].y) + shift - f : -0x40000000;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int t = min(max(toff + gl + G * k, -2), c + 1);
+                    W0[k] = static_cast<int>(cur[t - 1]);
+                    W1[k] = static_cast<int>(cur[t]);
+                    W2[k] = static_cast<int>(cur[t + 1]);
+                }
+            }
+            const uint32_t nmin = group_min<G>(run_min);
             if (c > 0) {
                 prev_min = static_cast<int>(nmin);
-                prev_first = f;
                 prev_count = c;
             }
             has_prev = c > 0;
