@@ -1178,6 +1178,8 @@ bool launch_line_gk(const SgmArgs& a, int total, cudaStream_t s) {
         launch_line<SN, 4, 4>(a, total, s);
     else if (a.group == 4 && a.kper == 3)
         launch_line<SN, 4, 3>(a, total, s);
+    else if (a.group == 8 && a.kper == 2)
+        launch_line<SN, 8, 2>(a, total, s);
     else if (a.group == 32 && a.kper == 4)
         launch_line<SN, 32, 4>(a, total, s);
     else if (a.group == 32 && a.kper == 8)
