@@ -160,37 +160,39 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
     using namespace dev;
     constexpr int RX = WW / 2, RY = WH / 2, NS = WW * WH;
     constexpr int NSP = KIND == FMVS_COST_NCC ? NS : 1;
-    __shared__ int s_prefix[kSeg + 1];
-    __shared__ int s_first[kSeg];
-    __shared__ uint32_t s_rel[kSeg];
-    __shared__ uint64_t s_bits[kSeg];
-    __shared__ double s_mean[kSeg], s_var[kSeg];
-    __shared__ float s_patch[kSeg][NSP];
-    __shared__ uint64_t s_base;
+    constexpr int kWarpsX = kThreads / 32;
+    // per-warp segment state: every warp owns one 32-pixel row segment at a
+    // time (no CTA barriers), so a level whose pixels are all narrow (the
+    // tiled kernels own them) costs one coalesced metadata load and a vote
+    // per segment
+    __shared__ int s_prefix[kWarpsX][kSeg + 1];
+    __shared__ int s_first[kWarpsX][kSeg];
+    __shared__ uint32_t s_rel[kWarpsX][kSeg];
+    __shared__ uint64_t s_bits[kWarpsX][kSeg];
+    __shared__ double s_mean[kWarpsX][kSeg], s_var[kWarpsX][kSeg];
+    __shared__ float s_patch[kWarpsX][kSeg][NSP];
 
-    const int t = threadIdx.x;
+    const int t = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const uint8_t* ref = a.ref_img;
-    // grid-stride over 32-pixel row segments: when every pixel is narrow (the
-    // tiled kernel owns them) a fixed-size grid only scans the metadata
     const int segs_per_row = (a.w + kSeg - 1) / kSeg;
     const int nseg = segs_per_row * a.h;
-    for (int seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
-    const int y = seg / segs_per_row;
-    const int x0 = (seg - y * segs_per_row) * kSeg;
-    const int npx = min(kSeg, a.w - x0);
+    for (int seg = blockIdx.x * kWarpsX + wp; seg < nseg; seg += gridDim.x * kWarpsX) {
+        const int y = seg / segs_per_row;
+        const int x0 = (seg - y * segs_per_row) * kSeg;
+        const int npx = min(kSeg, a.w - x0);
 
-    if (t < 32) {
         int cnt = 0;
+        VolMeta m{0u, 0u};
         if (t < npx) {
-            const VolMeta m = a.meta[static_cast<size_t>(y) * a.w + x0 + t];
+            m = a.meta[static_cast<size_t>(y) * a.w + x0 + t];
             cnt = meta_count(m.fc);
             if (cnt <= a.exact_above)
                 cnt = 0;  // narrow pixel: handled by the tiled certified kernel
-            s_first[t] = meta_first(m.fc);
-            s_rel[t] = m.rel;
-            if (t == 0)
-                s_base = a.row_base[y];
         }
+        if (!__any_sync(0xffffffffu, cnt > 0))
+            continue;
+        s_first[wp][t] = meta_first(m.fc);
+        s_rel[wp][t] = m.rel;
         int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -198,9 +200,9 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
             if (t >= o)
                 incl += v;
         }
-        s_prefix[t + 1] = incl;
+        s_prefix[wp][t + 1] = incl;
         if (t == 0)
-            s_prefix[0] = 0;
+            s_prefix[wp][0] = 0;
         if (t < npx && cnt > 0) {
             const int x = x0 + t;
             if constexpr (KIND == FMVS_COST_CENSUS) {
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
                         const int yy = min(max(y + dy, 0), a.h - 1);
                         bits = (bits << 1) | (ref[static_cast<size_t>(yy) * a.w + xx] < c ? 1u : 0u);
                     }
-                s_bits[t] = bits;
+                s_bits[wp][t] = bits;
             } else {
                 // reference patch, mean and two-pass variance (matching.cpp:199-210)
                 int s = 0;
@@ -223,56 +225,55 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(SweepArgs a) {
                     for (int dx = -RX; dx <= RX; ++dx) {
                         const int xx = min(max(x + dx, 0), a.w - 1);
                         const int yy = min(max(y + dy, 0), a.h - 1);
-                        s_patch[t][s++] = float(ref[static_cast<size_t>(yy) * a.w + xx]);
+                        s_patch[wp][t][s++] = float(ref[static_cast<size_t>(yy) * a.w + xx]);
                     }
                 double mean = 0.0, var = 0.0;
                 for (int i = 0; i < NS; ++i)
-                    mean = add(mean, double(s_patch[t][i]));
+                    mean = add(mean, double(s_patch[wp][t][i]));
                 mean = div(mean, double(NS));
                 for (int i = 0; i < NS; ++i) {
-                    const double d = sub(double(s_patch[t][i]), mean);
+                    const double d = sub(double(s_patch[wp][t][i]), mean);
                     var = add(var, mul(d, d));
                 }
-                s_mean[t] = mean;
-                s_var[t] = var;
+                s_mean[wp][t] = mean;
+                s_var[wp][t] = var;
             }
         }
-    }
-    __syncthreads();
+        __syncwarp();
 
-    const int total = s_prefix[npx];
-    const uint64_t base = s_base;
-    for (int e = t; e < total; e += kThreads) {
-        // pixel of entry e: largest j with prefix[j] <= e
-        int lo = 0, hi = npx;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_prefix[mid] <= e)
-                lo = mid;
-            else
-                hi = mid;
+        const int total = s_prefix[wp][npx];
+        const uint64_t base = a.row_base[y];
+        for (int e = t; e < total; e += 32) {
+            // pixel of entry e: largest j with prefix[j] <= e
+            int lo = 0, hi = npx;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_prefix[wp][mid] <= e)
+                    lo = mid;
+                else
+                    hi = mid;
+            }
+            const int j = lo;
+            const int plane = s_first[wp][j] + (e - s_prefix[wp][j]);
+            const double xd = double(x0 + j), yd = double(y);
+            int sum_l = 0, sum_r = 0;
+            for (int mm = 0; mm < a.nmatch; ++mm) {
+                const int2 sz = a.sizes[mm];
+                const int c = view_cost<KIND, WW, WH>(
+                    a.quads[mm], sz.x, sz.y, a.homs + (static_cast<size_t>(mm) * a.nplanes + plane) * 9,
+                    xd, yd, KIND == FMVS_COST_CENSUS ? s_bits[wp][j] : 0ull,
+                    KIND == FMVS_COST_NCC ? s_patch[wp][j] : nullptr,
+                    KIND == FMVS_COST_NCC ? s_mean[wp][j] : 0.0, KIND == FMVS_COST_NCC ? s_var[wp][j] : 0.0,
+                    a.census_lut);
+                if (mm < a.nleft)
+                    sum_l += c;
+                else
+                    sum_r += c;
+            }
+            const uint64_t o = base + s_rel[wp][j] + (e - s_prefix[wp][j]);
+            a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
         }
-        const int j = lo;
-        const int plane = s_first[j] + (e - s_prefix[j]);
-        const double xd = double(x0 + j), yd = double(y);
-        int sum_l = 0, sum_r = 0;
-        for (int m = 0; m < a.nmatch; ++m) {
-            const int2 sz = a.sizes[m];
-            const int c = view_cost<KIND, WW, WH>(
-                a.quads[m], sz.x, sz.y, a.homs + (static_cast<size_t>(m) * a.nplanes + plane) * 9,
-                xd, yd, KIND == FMVS_COST_CENSUS ? s_bits[j] : 0ull,
-                KIND == FMVS_COST_NCC ? s_patch[j] : nullptr,
-                KIND == FMVS_COST_NCC ? s_mean[j] : 0.0, KIND == FMVS_COST_NCC ? s_var[j] : 0.0,
-                a.census_lut);
-            if (m < a.nleft)
-                sum_l += c;
-            else
-                sum_r += c;
-        }
-        const uint64_t o = base + s_rel[j] + (e - s_prefix[j]);
-        a.costs[o] = static_cast<uint16_t>(min(sum_l, sum_r));
-    }
-    __syncthreads();  // the segment's shared state is rewritten next iteration
+        __syncwarp();  // the segment's shared state is rewritten next iteration
     }
 }
 
