@@ -259,6 +259,7 @@ struct fmvs_ctx {
     bool timing = false;
     int sweep_exact = 0;  // FMVS_SWEEP_EXACT=1: force the exact per-hypothesis sweep
     int sweep_stats = 0;  // FMVS_SWEEP_STATS=1 (2 + l: level l only): count certified-census fallbacks
+    bool agg16 = true;    // packed u16 SGM aggregate where provably exact (FMVS_SGM_AGG16=0: off)
     // stage capture of one level (fmvs_ctx_set_capture)
     struct Capture {
         int level = -1;
@@ -592,9 +593,6 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         if (ctx->sweep_stats == 1 || ctx->sweep_stats == 2 + l)
             sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(8);
         ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { launches += k::sweep(sa, s); });
-        // the SGM accumulator of the level (make_accumulator, sgm.cpp:198-208)
-        ctx->timed("zero", [&] { k::zero_entries(agg, rb + P.h, s); });
-        ++launches;
 
         int variant = cfg.sgm.variant;
         if (variant == FMVS_SGM_SURFACE_NORMAL && !have_prior)
@@ -658,6 +656,21 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         ga.scratch = (ga.group > 0 || np > pmax_smem_limit) ? sgm_scratch : nullptr;
         ga.line_scratch = sgm_line;
         ga.entries_bound = entries_bound;
+        // packed u16 aggregate when every sum provably fits (a view's cost is
+        // <= 255: census LUT / NCC truncation / outside; a pixel's the smaller
+        // side's sum, matching.cpp:283-292) AND the u32 aggregate would not
+        // stay in L2: then each RED misses and costs a DRAM read + write, and
+        // halving the bytes wins (C3: SGM 7.35 -> 5.59 ms); an L2-resident
+        // aggregate is faster unpacked (two lanes per word serialise their
+        // REDs: C2 L0 0.63 -> 0.79 ms; C4 L0, 100 M entries of ~12 per
+        // pixel, 2.36 -> 2.61 ms). Only the uniform (coarsest, one line per
+        // warp, long contiguous runs) levels qualify: C4 L2 1.8x less DRAM.
+        const uint64_t known_entries = have_prior ? 0 : entries_bound;
+        ga.agg16 = ctx->agg16 && known_entries > (uint64_t(48) << 20) &&
+                   k::sgm_agg16_ok(ga, 255ll * std::max(ref, nmatch - ref));
+        // the SGM accumulator of the level (make_accumulator, sgm.cpp:198-208)
+        ctx->timed("zero", [&] { k::zero_entries(agg, rb + P.h, s, ga.agg16 != 0); });
+        ++launches;
         ctx->timed(l == 0 ? "sgm_l0" : "sgm", [&] { k::sgm(ga, s); });
         ++launches;
 
@@ -667,6 +680,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         wa.meta = meta;
         wa.row_base = rb;
         wa.agg = agg;
+        wa.agg16 = ga.agg16;
         wa.depth = depth_raw;
         wa.intr = intr;
         wa.nx = nx;
@@ -698,7 +712,14 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
             c.costs.resize(entries);
             c.agg.resize(entries);
             FMVS_CUDA_CHECK(cudaMemcpyAsync(c.costs.data(), costs, entries * 2, cudaMemcpyDeviceToHost, s));
-            FMVS_CUDA_CHECK(cudaMemcpyAsync(c.agg.data(), agg, entries * 4, cudaMemcpyDeviceToHost, s));
+            if (ga.agg16) {  // packed u16 aggregate: widen to the reference's u32
+                std::vector<uint16_t> a16(entries);
+                FMVS_CUDA_CHECK(cudaMemcpyAsync(a16.data(), agg, entries * 2, cudaMemcpyDeviceToHost, s));
+                FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
+                std::copy(a16.begin(), a16.end(), c.agg.begin());
+            } else {
+                FMVS_CUDA_CHECK(cudaMemcpyAsync(c.agg.data(), agg, entries * 4, cudaMemcpyDeviceToHost, s));
+            }
             FMVS_CUDA_CHECK(cudaStreamSynchronize(s));
             c.level = -1;
         }
@@ -841,6 +862,8 @@ int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
         ctx->device = device;
         if (const char* e = std::getenv("FMVS_SWEEP_EXACT"))
             ctx->sweep_exact = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FMVS_SGM_AGG16"))
+            ctx->agg16 = std::atoi(e) != 0;
         if (const char* e = std::getenv("FMVS_SWEEP_STATS"))
             ctx->sweep_stats = std::atoi(e);  // 1: every level; 2 + l: level l only
         ctx->use();

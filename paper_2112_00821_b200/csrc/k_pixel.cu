@@ -58,11 +58,14 @@ __global__ void wta_depth_kernel(WtaArgs a) {
             a.depth[p] = 0.0f;
         return;
     }
-    const uint32_t* v = a.agg + a.row_base[y] + m.rel;
+    const uint64_t e0 = a.row_base[y] + m.rel;
+    const uint32_t* v32 = a.agg + e0;
+    const uint16_t* v16 = reinterpret_cast<const uint16_t*>(a.agg) + e0;
+    auto val = [&](int i) -> uint32_t { return a.agg16 ? v16[i] : v32[i]; };
     int best = 0;
-    uint32_t bv = v[0];
+    uint32_t bv = val(0);
     for (int i = 1; i < c; ++i) {
-        const uint32_t vi = v[i];
+        const uint32_t vi = val(i);
         if (vi < bv) {
             bv = vi;
             best = i;
@@ -83,8 +86,8 @@ __global__ void wta_depth_kernel(WtaArgs a) {
             const double d_lo = depth_from_plane_dev(denom, a.planes[win + 1]);
             const double d_hi = depth_from_plane_dev(denom, a.planes[win - 1]);
             if (d_lo > 0.0 && d_hi > 0.0 && d_lo < d_win && d_win < d_hi)
-                d = parabola_dev(d_lo, d_win, d_hi, double(v[best + 1]), double(v[best]),
-                                 double(v[best - 1]));
+                d = parabola_dev(d_lo, d_win, d_hi, double(val(best + 1)), double(val(best)),
+                                 double(val(best - 1)));
         }
         out = __double2float_rn(d);
     }

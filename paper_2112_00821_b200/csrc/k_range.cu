@@ -174,8 +174,9 @@ void range_rows(const RangeArgs& a, cudaStream_t s) {
 
 // agg[0 .. *count) = 0 with contiguous 16-byte stores; the entry count is read
 // on the device (row_base[h] of the level), so no host synchronisation.
-__global__ void zero_entries_kernel(uint32_t* __restrict__ agg, const uint64_t* __restrict__ count) {
-    const uint64_t n = *count;
+__global__ void zero_entries_kernel(uint32_t* __restrict__ agg, const uint64_t* __restrict__ count,
+                                    bool agg16) {
+    const uint64_t n = agg16 ? (*count + 1) / 2 : *count;  // 32-bit words
     const uint64_t n4 = n / 4;
     uint4* a4 = reinterpret_cast<uint4*>(agg);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -186,8 +187,8 @@ __global__ void zero_entries_kernel(uint32_t* __restrict__ agg, const uint64_t* 
         agg[r] = 0u;
 }
 
-void zero_entries(uint32_t* agg, const uint64_t* count, cudaStream_t s) {
-    zero_entries_kernel<<<148 * 4, 512, 0, s>>>(agg, count);
+void zero_entries(uint32_t* agg, const uint64_t* count, cudaStream_t s, bool agg16) {
+    zero_entries_kernel<<<148 * 4, 512, 0, s>>>(agg, count, agg16);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -847,7 +847,7 @@ struct LinePipe {
 // step bodies, with the predecessor window loaded a step early, ran 1.8x
 // slower at level 0, with the same loads staged through shared memory by
 // cp.async too).
-template <bool SN, int G, int K, int S, int GAP, bool SHARED, bool EMB>
+template <bool SN, int G, int K, int S, int GAP, bool SHARED, bool EMB, bool AGG16>
 __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, uint32_t* bufA,
                                           uint32_t* bufB) {
     constexpr int PASS = G * K;
@@ -879,7 +879,11 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                 const int tmax = prev_count + 1;
                 const uint32_t ib = P.R[u].x + gl;
                 auto pass = [&](int i0, const uint32_t* sc, bool first) {
-                    uint32_t* ap = a.agg + (ib + i0);
+                    // AGG16: entry e is u16 e of the aggregate (two per word);
+                    // the lanes' entries of a pass share e's parity (G even)
+                    const uint32_t e0 = ib + i0;
+                    uint32_t* ap = AGG16 ? a.agg + (e0 >> 1) : a.agg + e0;
+                    const int sh = AGG16 ? static_cast<int>(e0 & 1u) * 16 : 0;
                     uint32_t* cp = cur + (gl + i0);
                     static_for<K>([&](auto kc) {
                         constexpr int k = decltype(kc)::value;
@@ -899,7 +903,10 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                         const uint32_t v = sc[k] + static_cast<uint32_t>(best - pm);
                         if (i < c)
                             cp[G * k] = v;
-                        red_add<4 * G * k>(ap, i < c, v);
+                        if constexpr (AGG16)
+                            red_add<2 * G * k>(ap, i < c, v << sh);
+                        else
+                            red_add<4 * G * k>(ap, i < c, v);
                         run_min = min(run_min, i < c ? v : 0xFFFFFFFFu);
                     });
                 };
@@ -946,7 +953,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
     }
 }
 
-template <bool SN, int G, int K, int S, int GAP, bool EMB>
+template <bool SN, int G, int K, int S, int GAP, bool EMB, bool AGG16>
 __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const uint4* __restrict__ rec,
                                                                LineFlags fl, int total_lines, int stride) {
     constexpr int LPW = 32 / G;
@@ -1008,10 +1015,10 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
             }
         }
         __syncwarp();
-        line_steps<SN, G, K, S, GAP, false, false>(a, lc, bufA, bufB);
+        line_steps<SN, G, K, S, GAP, false, false, AGG16>(a, lc, bufA, bufB);
     } else {
         __syncwarp();
-        line_steps<SN, G, K, S, GAP, true, EMB>(a, lc, sA, sB);
+        line_steps<SN, G, K, S, GAP, true, EMB, AGG16>(a, lc, sA, sB);
     }
 }
 
@@ -1120,7 +1127,6 @@ void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
 
 template <bool SN, int G, int K, int S, int GAP>
 void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
-
     constexpr int LPW = 32 / G;
     // a line is narrow when every pixel fits one pass (its shared buffers
     // hold G*K slots); wider lines run from their global scratch
@@ -1141,33 +1147,28 @@ void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
     constexpr bool kEmb = G == 4 && K <= 4;
     const bool emb = kEmb && emb_on;
     sgm_prep_kernel<<<(npx + 255) / 256, 256, 0, s>>>(a, rec, fl, caps, emb);
-    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_line_kernel<SN, G, K, S, GAP, kEmb>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_line_kernel<SN, G, K, S, GAP, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (emb)
-        sgm_line_kernel<SN, G, K, S, GAP, kEmb><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
+    auto go = [&](auto kernel) {
+        FMVS_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+        kernel<<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
+    };
+    if (emb && a.agg16)
+        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, true>);
+    else if (emb)
+        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, false>);
+    else if (a.agg16)
+        go(sgm_line_kernel<SN, G, K, S, GAP, false, true>);
     else
-        sgm_line_kernel<SN, G, K, S, GAP, false><<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
+        go(sgm_line_kernel<SN, G, K, S, GAP, false, false>);
 }
 
-// Pipeline depth S (pixels whose records are in registers) and GAP (steps
-// between a pixel's record and cost loads): the cost loads of a refined level
-// miss L2 about half the time, so they are issued S-1-GAP steps ahead.
+// Pipeline depth S (pixels whose records are in registers; measured 6 / 8 /
+// 10 / 12 at C2 L0: 8 best) and GAP (steps between a pixel's record and its
+// cost loads when the costs are not embedded).
 template <bool SN, int G, int K>
 void launch_line(const SgmArgs& a, int total, cudaStream_t s) {
-    static const int depth = [] {
-        const char* e = std::getenv("FMVS_SGM_DEPTH");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (K >= 8)
+    if constexpr (K >= 8)
         launch_line_sg<SN, G, K, 4, 1>(a, total, s);
-    else if (depth == 6)
-        launch_line_sg<SN, G, K, 6, 2>(a, total, s);
-    else if (depth == 10)
-        launch_line_sg<SN, G, K, 10, 4>(a, total, s);
-    else if (depth == 12)
-        launch_line_sg<SN, G, K, 12, 5>(a, total, s);
     else
         launch_line_sg<SN, G, K, 8, 3>(a, total, s);
 }
@@ -1178,8 +1179,6 @@ bool launch_line_gk(const SgmArgs& a, int total, cudaStream_t s) {
         launch_line<SN, 4, 4>(a, total, s);
     else if (a.group == 4 && a.kper == 3)
         launch_line<SN, 4, 3>(a, total, s);
-    else if (a.group == 8 && a.kper == 2)
-        launch_line<SN, 8, 2>(a, total, s);
     else if (a.group == 32 && a.kper == 4)
         launch_line<SN, 32, 4>(a, total, s);
     else if (a.group == 32 && a.kper == 8)
@@ -1193,14 +1192,11 @@ size_t sgm_line_scratch_words(int w, int h) {
     return static_cast<size_t>(kRecWords) * (static_cast<size_t>(w) * h + 1) + line_flag_words(w, h);
 }
 
-void sgm(const SgmArgs& a, cudaStream_t s) {
-    const int total = sgm_lines(a.w, a.h, a.dirs, a.ndirs);
-    if (total == 0)
-        return;
-    // int32 recurrence is exact when every intermediate stays below 2^31:
-    // path values <= 65535 + phi2_max, candidates <= value + max(phi1, phi2).
-    const bool fast32 = a.phi1 >= 0 && a.phi2_max >= 0 && a.phi1 < (1ll << 28) &&
-                        a.phi2_max < (1ll << 28);
+bool sgm_fast32(const SgmArgs& a) {
+    return a.phi1 >= 0 && a.phi2_max >= 0 && a.phi1 < (1ll << 28) && a.phi2_max < (1ll << 28);
+}
+
+bool sgm_line_applicable(const SgmArgs& a) {
     // line kernel: Plane / SN, int32, unit directions, 32-bit entry indices
     static const bool line_on = [] {
         const char* e = std::getenv("FMVS_SGM_LINE");
@@ -1210,16 +1206,39 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
     for (int d = 0; d < a.ndirs; ++d)
         unit = unit && std::abs(a.dirs[d][0]) <= 1 && std::abs(a.dirs[d][1]) <= 1 &&
                (a.dirs[d][0] != 0 || a.dirs[d][1] != 0);
+    const bool gk = (a.group == 4 && (a.kper == 3 || a.kper == 4)) ||
+                    (a.group == 32 && (a.kper == 4 || a.kper == 8));
+    return line_on && a.line_scratch && a.scratch && sgm_fast32(a) && unit && gk &&
+           a.variant != FMVS_SGM_PATH_GRADIENT && a.nplanes <= kRecPlanes &&
+           a.entries_bound + 1024 < (1ull << 32);
+}
+
+bool sgm_agg16_ok(const SgmArgs& a, long long cost_max) {
+    // every path value lies in [0, cost + phi2_max] (its best candidate is at
+    // most prev_min + phi2), so the aggregate of `ndirs` paths stays below
+    // ndirs * (cost_max + phi2_max): two aggregates per 32-bit word never carry
+    return sgm_line_applicable(a) && cost_max >= 0 &&
+           static_cast<long long>(a.ndirs) * (cost_max + a.phi2_max) < 65536;
+}
+
+void sgm(const SgmArgs& a, cudaStream_t s) {
+    const int total = sgm_lines(a.w, a.h, a.dirs, a.ndirs);
+    if (total == 0)
+        return;
+    // int32 recurrence is exact when every intermediate stays below 2^31:
+    // path values <= 65535 + phi2_max, candidates <= value + max(phi1, phi2).
+    const bool fast32 = sgm_fast32(a);
     static_assert(kAggSlack >= 32 * 8, "inactive lanes of a pass add 0 up to G*K - 1 entries past a pixel");
-    if (line_on && a.line_scratch && a.scratch && fast32 && unit && a.group > 0 &&
-        a.variant != FMVS_SGM_PATH_GRADIENT && a.nplanes <= kRecPlanes &&
-        a.entries_bound + 1024 < (1ull << 32)) {
-        const bool done = a.offsets ? launch_line_gk<true>(a, total, s) : launch_line_gk<false>(a, total, s);
-        if (done) {
-            FMVS_CUDA_CHECK(cudaGetLastError());
-            return;
-        }
+    if (sgm_line_applicable(a)) {
+        if (a.offsets)
+            launch_line_gk<true>(a, total, s);
+        else
+            launch_line_gk<false>(a, total, s);
+        FMVS_CUDA_CHECK(cudaGetLastError());
+        return;
     }
+    if (a.agg16)
+        throw Error(FMVS_ERR_CONFIG, "sgm: packed u16 aggregate needs the line kernel");
     if (a.group > 0) {
         // lane-blocked kernel; scratch (global overflow buffers) is mandatory here
         if (a.variant == FMVS_SGM_PATH_GRADIENT) {

@@ -64,7 +64,7 @@ void range_rows(const RangeArgs& a, cudaStream_t s);
 void scan_rows(const uint32_t* row_total, int h, uint64_t* row_base, cudaStream_t s);
 // agg[0 .. *count) = 0 (the SGM accumulator of a level; count on the device,
 // 16-byte aligned agg).
-void zero_entries(uint32_t* agg, const uint64_t* count, cudaStream_t s);
+void zero_entries(uint32_t* agg, const uint64_t* count, cudaStream_t s, bool agg16 = false);
 
 // ---- K4: plane-sweep cost volume (matching.cpp:116-294) ------------------
 struct SweepArgs {
@@ -140,7 +140,16 @@ struct SgmArgs {
     // the level's entry count (the records hold 32-bit entry indices).
     uint32_t* line_scratch;
     uint64_t entries_bound;
+    // packed aggregate: entry e is the u16 at index e of `agg` (two per 32-bit
+    // word; set only when sgm_agg16_ok proved every sum fits 16 bits)
+    int agg16;
 };
+// the line kernel runs this configuration (else the general kernel)
+bool sgm_line_applicable(const SgmArgs& a);
+bool sgm_fast32(const SgmArgs& a);
+// a packed u16 aggregate is exact for this configuration, per-pixel matching
+// costs <= cost_max
+bool sgm_agg16_ok(const SgmArgs& a, long long cost_max);
 void sgm(const SgmArgs& a, cudaStream_t s);
 // entries every cost and aggregate allocation carries past the volume (the
 // line kernel's inactive lanes add 0 there; its cost staging reads aligned
@@ -160,6 +169,7 @@ struct WtaArgs {
     const dev::VolMeta* meta;
     const uint64_t* row_base;
     const uint32_t* agg;
+    int agg16;                       // packed u16 aggregate (SgmArgs::agg16)
     int32_t* winners;                // optional
     float* depth;                    // optional (needs intr/planes)
     dev::Intr intr;
