@@ -274,25 +274,31 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_kernel(SgmArgs a, int total_l
 // decreasing stack the bracket d[lo] >= delta > d[lo + 1] is unique, so the
 // result is identical, and along a smooth path it is within a few planes of
 // the previous winner.
+// Only the rounded index is needed, so the division is skipped where its
+// outcome is certain: beyond either end of the stack f <= 0 or f >= n - 1
+// (clamped to 0 / n - 1); inside, llround(lo + frac) is lo + 1 exactly when
+// frac >= 1/2, decided from 2 * num against den with a 2^-30 relative margin
+// (far above the division's and the addition's rounding for lo < 2^11);
+// ties within the margin take the reference's exact expression.
 __device__ __forceinline__ int nearest_index_from(const double* __restrict__ d, int n, double delta,
                                                   int hint) {
     using namespace dev;
-    double f;
-    if (n <= 1) {
-        f = 0.0;
-    } else if (delta >= d[0]) {
-        f = div(-sub(delta, d[0]), sub(d[0], d[1]));
-    } else if (delta <= d[n - 1]) {
-        f = add(double(n - 1), div(sub(d[n - 1], delta), sub(d[n - 2], d[n - 1])));
-    } else {
-        int lo = min(max(hint, 0), n - 2);
-        while (!(d[lo] >= delta))
-            --lo;
-        while (d[lo + 1] >= delta)
-            ++lo;
-        f = add(double(lo), div(sub(d[lo], delta), sub(d[lo], d[lo + 1])));
-    }
-    const int i = static_cast<int>(llround(f));
+    if (n <= 1 || delta >= d[0])
+        return 0;
+    if (delta <= d[n - 1])
+        return n - 1;
+    int lo = min(max(hint, 0), n - 2);
+    while (!(d[lo] >= delta))
+        --lo;
+    while (d[lo + 1] >= delta)
+        ++lo;
+    const double num = sub(d[lo], delta), den = sub(d[lo], d[lo + 1]);
+    const double twice = 2.0 * num;
+    if (twice < den * (1.0 - 9.313225746154785e-10))
+        return lo;
+    if (twice > den * (1.0 + 9.313225746154785e-10))
+        return min(lo + 1, n - 1);
+    const int i = static_cast<int>(llround(add(double(lo), div(num, den))));
     return i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
 }
 
@@ -765,6 +771,7 @@ struct LineCtx {
     int dummy;       // index of the zero record
     int sign, off_sh;
     bool off_hi;
+    int x0, y0, dx, dy;  // first pixel and step of the line (PG scene points)
 };
 
 // Operand pipeline of the line kernel: records of pixels j+1..j+S-1 and the
@@ -847,7 +854,7 @@ struct LinePipe {
 // step bodies, with the predecessor window loaded a step early, ran 1.8x
 // slower at level 0, with the same loads staged through shared memory by
 // cp.async too).
-template <bool SN, int G, int K, int S, int GAP, bool SHARED, bool EMB, bool AGG16>
+template <bool SN, int G, int K, int S, int GAP, bool SHARED, bool EMB, bool AGG16, bool PG>
 __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, uint32_t* bufA,
                                           uint32_t* bufB) {
     constexpr int PASS = G * K;
@@ -857,6 +864,12 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
     P.start(a, lc);
     int prev_count = 0, prev_min = 0, ph = 0, toff = -0x40000000;
     bool has_prev = false;
+    // PG: minimum-cost history of the line (sgm.cpp:28-43), the same in every
+    // lane of the group; the pixel's coordinates for its scene point
+    bool h1 = false, h2 = false;
+    dev::D3 p1{0.0, 0.0, 0.0}, p2{0.0, 0.0, 0.0};
+    int h1_index = 0;
+    int px = lc.x0, py = lc.y0;
     // first-pass predecessor window of the current pixel (prev[t-1], prev[t],
     // prev[t+1] per slot), loaded at the end of the previous step so the
     // loads overlap the group-minimum shuffles
@@ -873,6 +886,16 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
             const uint32_t pk = P.R[u].y;
             const int c = rec_count(pk), f = rec_first(pk);
             uint32_t run_min = 0xFFFFFFFFu;
+            int run_arg = 0x7FFFFFFF;  // PG: lowest index attaining run_min (lanes scan i upwards)
+            // PG: the pixel's viewing ray and its plane-normal dot (scene_point,
+            // sgm.cpp:46-58), computed before the recurrence so the divisions
+            // stay off the winner -> shift dependency chain
+            dev::D3 ray{0.0, 0.0, 1.0};
+            double denom = 0.0;
+            if constexpr (PG) {
+                ray = dev::unproject(a.intr, double(px), double(py));
+                denom = dev::dot3(dev::D3{a.nx, a.ny, a.nz}, ray);
+            }
             if (c > 0) {
                 const int pm = has_prev ? prev_min : 0;
                 const int bp = has_prev ? prev_min + (EMB ? ph : P.PH[u]) : 0;
@@ -907,7 +930,14 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                             red_add<2 * G * k>(ap, i < c, v << sh);
                         else
                             red_add<4 * G * k>(ap, i < c, v);
-                        run_min = min(run_min, i < c ? v : 0xFFFFFFFFu);
+                        if constexpr (PG) {
+                            if (i < c && v < run_min) {
+                                run_min = v;
+                                run_arg = i;
+                            }
+                        } else {
+                            run_min = min(run_min, i < c ? v : 0xFFFFFFFFu);
+                        }
                     });
                 };
                 uint32_t sc0[K];
@@ -927,11 +957,44 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                     cur[c + gl] = kSentinel;
             }
             __syncwarp();
+            int pg_shift = 0;
+            if constexpr (PG) {
+                // winner of this pixel (sgm.cpp:166-174) and its scene point
+                // (:176-185), then the predicted shift of the next pixel
+                // (:131-140, nearest_index by a local bracket search)
+                const uint32_t nmin_pg = group_min<G>(run_min);
+                const int arg = static_cast<int>(
+                    group_min<G>(run_min == nmin_pg ? static_cast<uint32_t>(run_arg) : 0x7FFFFFFFu));
+                if (c > 0) {
+                    const double t = fabs(denom) < 1e-12 ? 0.0 : dev::div(-a.planes[f + arg], denom);
+                    if (t > 0.0) {
+                        h2 = h1;
+                        p2 = p1;
+                        h1 = true;
+                        p1 = dev::scale3(t, ray);
+                        h1_index = f + arg;
+                    } else {
+                        h1 = h2 = false;
+                    }
+                    if (h1 && h2) {
+                        const dev::D3 pred = dev::add3(p1, dev::sub3(p1, p2));
+                        const double delta_pred = -dev::dot3(dev::D3{a.nx, a.ny, a.nz}, pred);
+                        if (delta_pred > 0.0) {
+                            const int pi = nearest_index_from(a.planes, a.nplanes, delta_pred, h1_index);
+                            pg_shift = min(max(h1_index - pi, -3), 3);
+                        }
+                    }
+                } else {
+                    h1 = h2 = false;  // an empty pixel resets the path (sgm.cpp:101-106)
+                }
+                px += lc.dx;
+                py += lc.dy;
+            }
             // predecessor window of pixel j+1 in this pixel's buffer (an empty
             // pixel leaves only the permanent left sentinels in reach)
             {
                 const int u1 = (u + 1) % S;
-                const int shift = SN ? P.shift(lc, u1) : 0;
+                const int shift = SN ? P.shift(lc, u1) : pg_shift;
                 toff = c > 0 ? rec_first(P.R[u1].y) + shift - f : -0x40000000;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -953,7 +1016,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
     }
 }
 
-template <bool SN, int G, int K, int S, int GAP, bool EMB, bool AGG16>
+template <bool SN, int G, int K, int S, int GAP, bool EMB, bool AGG16, bool PG>
 __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const uint4* __restrict__ rec,
                                                                LineFlags fl, int total_lines, int stride) {
     constexpr int LPW = 32 / G;
@@ -995,6 +1058,10 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
     lc.sign = (dy == 0 || dx == 0) ? dx + dy : dx;
     lc.off_sh = (slot & 1) * 16;
     lc.off_hi = (slot >> 1) != 0;
+    lc.x0 = x;
+    lc.y0 = y;
+    lc.dx = dx;
+    lc.dy = dy;
 
     uint32_t* sA = smem + 256 + (warp * LPW + grp) * stride + kSent;
     uint32_t* sB = sA + PASS + 2 * kSent;
@@ -1015,10 +1082,10 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
             }
         }
         __syncwarp();
-        line_steps<SN, G, K, S, GAP, false, false, AGG16>(a, lc, bufA, bufB);
+        line_steps<SN, G, K, S, GAP, false, false, AGG16, PG>(a, lc, bufA, bufB);
     } else {
         __syncwarp();
-        line_steps<SN, G, K, S, GAP, true, EMB, AGG16>(a, lc, sA, sB);
+        line_steps<SN, G, K, S, GAP, true, EMB, AGG16, PG>(a, lc, sA, sB);
     }
 }
 
@@ -1125,7 +1192,7 @@ void launch_group_g(const SgmArgs& a, int total, cudaStream_t s) {
         throw Error(FMVS_ERR_CONFIG, "sgm: unsupported lane blocking");
 }
 
-template <bool SN, int G, int K, int S, int GAP>
+template <bool SN, bool PG, int G, int K, int S, int GAP>
 void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
     constexpr int LPW = 32 / G;
     // a line is narrow when every pixel fits one pass (its shared buffers
@@ -1153,36 +1220,36 @@ void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
         kernel<<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
     };
     if (emb && a.agg16)
-        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, true>);
+        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, true, PG>);
     else if (emb)
-        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, false>);
+        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, false, PG>);
     else if (a.agg16)
-        go(sgm_line_kernel<SN, G, K, S, GAP, false, true>);
+        go(sgm_line_kernel<SN, G, K, S, GAP, false, true, PG>);
     else
-        go(sgm_line_kernel<SN, G, K, S, GAP, false, false>);
+        go(sgm_line_kernel<SN, G, K, S, GAP, false, false, PG>);
 }
 
 // Pipeline depth S (pixels whose records are in registers; measured 6 / 8 /
 // 10 / 12 at C2 L0: 8 best) and GAP (steps between a pixel's record and its
 // cost loads when the costs are not embedded).
-template <bool SN, int G, int K>
+template <bool SN, bool PG, int G, int K>
 void launch_line(const SgmArgs& a, int total, cudaStream_t s) {
     if constexpr (K >= 8)
-        launch_line_sg<SN, G, K, 4, 1>(a, total, s);
+        launch_line_sg<SN, PG, G, K, 4, 1>(a, total, s);
     else
-        launch_line_sg<SN, G, K, 8, 3>(a, total, s);
+        launch_line_sg<SN, PG, G, K, 8, 3>(a, total, s);
 }
 
-template <bool SN>
+template <bool SN, bool PG>
 bool launch_line_gk(const SgmArgs& a, int total, cudaStream_t s) {
     if (a.group == 4 && a.kper == 4)
-        launch_line<SN, 4, 4>(a, total, s);
+        launch_line<SN, PG, 4, 4>(a, total, s);
     else if (a.group == 4 && a.kper == 3)
-        launch_line<SN, 4, 3>(a, total, s);
+        launch_line<SN, PG, 4, 3>(a, total, s);
     else if (a.group == 32 && a.kper == 4)
-        launch_line<SN, 32, 4>(a, total, s);
+        launch_line<SN, PG, 32, 4>(a, total, s);
     else if (a.group == 32 && a.kper == 8)
-        launch_line<SN, 32, 8>(a, total, s);
+        launch_line<SN, PG, 32, 8>(a, total, s);
     else
         return false;
     return true;
@@ -1197,7 +1264,7 @@ bool sgm_fast32(const SgmArgs& a) {
 }
 
 bool sgm_line_applicable(const SgmArgs& a) {
-    // line kernel: Plane / SN, int32, unit directions, 32-bit entry indices
+    // line kernel: any variant, int32, unit directions, 32-bit entry indices
     static const bool line_on = [] {
         const char* e = std::getenv("FMVS_SGM_LINE");
         return !(e && e[0] == '0');
@@ -1208,8 +1275,7 @@ bool sgm_line_applicable(const SgmArgs& a) {
                (a.dirs[d][0] != 0 || a.dirs[d][1] != 0);
     const bool gk = (a.group == 4 && (a.kper == 3 || a.kper == 4)) ||
                     (a.group == 32 && (a.kper == 4 || a.kper == 8));
-    return line_on && a.line_scratch && a.scratch && sgm_fast32(a) && unit && gk &&
-           a.variant != FMVS_SGM_PATH_GRADIENT && a.nplanes <= kRecPlanes &&
+    return line_on && a.line_scratch && a.scratch && sgm_fast32(a) && unit && gk && a.nplanes <= kRecPlanes &&
            a.entries_bound + 1024 < (1ull << 32);
 }
 
@@ -1230,10 +1296,12 @@ void sgm(const SgmArgs& a, cudaStream_t s) {
     const bool fast32 = sgm_fast32(a);
     static_assert(kAggSlack >= 32 * 8, "inactive lanes of a pass add 0 up to G*K - 1 entries past a pixel");
     if (sgm_line_applicable(a)) {
-        if (a.offsets)
-            launch_line_gk<true>(a, total, s);
+        if (a.variant == FMVS_SGM_PATH_GRADIENT)
+            launch_line_gk<false, true>(a, total, s);
+        else if (a.offsets)
+            launch_line_gk<true, false>(a, total, s);
         else
-            launch_line_gk<false>(a, total, s);
+            launch_line_gk<false, false>(a, total, s);
         FMVS_CUDA_CHECK(cudaGetLastError());
         return;
     }
