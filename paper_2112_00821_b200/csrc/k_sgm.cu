@@ -772,6 +772,7 @@ struct LineCtx {
     int sign, off_sh;
     bool off_hi;
     int x0, y0, dx, dy;  // first pixel and step of the line (PG scene points)
+    const double* planes;  // PG: the plane stack (shared-memory copy)
 };
 
 // Operand pipeline of the line kernel: records of pixels j+1..j+S-1 and the
@@ -966,7 +967,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                 const int arg = static_cast<int>(
                     group_min<G>(run_min == nmin_pg ? static_cast<uint32_t>(run_arg) : 0x7FFFFFFFu));
                 if (c > 0) {
-                    const double t = fabs(denom) < 1e-12 ? 0.0 : dev::div(-a.planes[f + arg], denom);
+                    const double t = fabs(denom) < 1e-12 ? 0.0 : dev::div(-lc.planes[f + arg], denom);
                     if (t > 0.0) {
                         h2 = h1;
                         p2 = p1;
@@ -980,7 +981,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
                         const dev::D3 pred = dev::add3(p1, dev::sub3(p1, p2));
                         const double delta_pred = -dev::dot3(dev::D3{a.nx, a.ny, a.nz}, pred);
                         if (delta_pred > 0.0) {
-                            const int pi = nearest_index_from(a.planes, a.nplanes, delta_pred, h1_index);
+                            const int pi = nearest_index_from(lc.planes, a.nplanes, delta_pred, h1_index);
                             pg_shift = min(max(h1_index - pi, -3), 3);
                         }
                     }
@@ -1026,6 +1027,12 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
     int* lut = reinterpret_cast<int*>(smem);
     for (int i = threadIdx.x; i < 256; i += kWarps * 32)
         lut[i] = static_cast<int>(a.phi2_lut[i]);
+    // PG: the plane stack after the path buffers (its bracket searches and
+    // scene points sit on the step's dependency chain)
+    double* s_planes = reinterpret_cast<double*>(smem + ((256 + kWarps * LPW * stride + 1) & ~1));
+    if (PG)
+        for (int i = threadIdx.x; i < a.nplanes; i += kWarps * 32)
+            s_planes[i] = a.planes[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / G;
@@ -1058,6 +1065,7 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
     lc.sign = (dy == 0 || dx == 0) ? dx + dy : dx;
     lc.off_sh = (slot & 1) * 16;
     lc.off_hi = (slot >> 1) != 0;
+    lc.planes = s_planes;
     lc.x0 = x;
     lc.y0 = y;
     lc.dx = dx;
@@ -1201,7 +1209,8 @@ void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
     int stride = 2 * (caps + 2 * kSent);
     stride += ((G % 32) - stride % 32 + 32) % 32;
     const int blocks = (total + kWarps * LPW - 1) / (kWarps * LPW);
-    const size_t smem = (256 + static_cast<size_t>(kWarps) * LPW * stride) * sizeof(uint32_t);
+    const size_t smem = (256 + static_cast<size_t>(kWarps) * LPW * stride + 1) * sizeof(uint32_t) +
+                        (PG ? static_cast<size_t>(a.nplanes) * sizeof(double) : 0);
     auto* rec = reinterpret_cast<uint4*>(a.line_scratch);
     const LineFlags fl = line_flags(a.line_scratch + kRecWords * (static_cast<size_t>(a.w) * a.h + 1), a.w, a.h);
     FMVS_CUDA_CHECK(cudaMemsetAsync(fl.row, 0, line_flag_words(a.w, a.h) * sizeof(uint32_t), s));
