@@ -105,49 +105,78 @@ constexpr int kMedianComparators = 191;
 __device__ constexpr int8_t kMedianA[kMedianComparators] = {0,2,4,6,8,10,12,14,16,18,20,22,24,26,28,30,0,1,4,5,8,9,12,13,16,17,20,21,24,25,28,29,1,5,9,13,17,21,25,29,0,1,2,3,8,9,10,11,16,17,18,19,24,25,26,27,2,3,10,11,18,19,26,27,1,3,5,9,11,13,17,19,21,25,27,29,0,1,2,3,4,5,6,7,16,17,18,19,20,21,22,23,4,5,6,7,20,21,22,23,2,3,6,7,10,11,18,19,22,23,26,27,1,3,5,7,9,11,13,17,19,21,23,25,27,29,0,1,2,3,4,5,6,7,8,9,10,11,12,13,14,15,8,9,10,11,12,13,14,15,4,5,6,7,12,13,14,15,20,21,22,23,2,3,6,7,10,11,14,15,18,19,22,23,26,27,1,3,5,7,9,11,13,15,17,19,21,23,25,27,29};
 __device__ constexpr int8_t kMedianB[kMedianComparators] = {1,3,5,7,9,11,13,15,17,19,21,23,25,27,29,31,2,3,6,7,10,11,14,15,18,19,22,23,26,27,30,31,2,6,10,14,18,22,26,30,4,5,6,7,12,13,14,15,20,21,22,23,28,29,30,31,4,5,12,13,20,21,28,29,2,4,6,10,12,14,18,20,22,26,28,30,8,9,10,11,12,13,14,15,24,25,26,27,28,29,30,31,8,9,10,11,24,25,26,27,4,5,8,9,12,13,20,21,24,25,28,29,2,4,6,8,10,12,14,18,20,22,24,26,28,30,16,17,18,19,20,21,22,23,24,25,26,27,28,29,30,31,16,17,18,19,20,21,22,23,8,9,10,11,16,17,18,19,24,25,26,27,4,5,8,9,12,13,16,17,20,21,24,25,28,29,2,4,6,8,10,12,14,16,18,20,22,24,26,28,30};
 
-__global__ void median5_kernel(const float* __restrict__ in, int w, int h,
-                               float* __restrict__ out) {
+// The same network pruned for the median of 25 values (element 12): only the
+// comparators that can still move a value into slot 12 (132 of the 165 that
+// touch real samples), used when the whole window is valid (checked against
+// full sorts of random and tied windows in tests/test_median_network.py).
+constexpr int kMedian25Comparators = 132;
+__device__ constexpr int8_t kMed25A[kMedian25Comparators] = {0,2,4,6,8,10,12,14,16,18,20,22,24,0,1,4,5,8,9,12,13,16,17,20,21,24,1,5,9,13,17,21,0,1,2,3,8,9,10,11,16,17,18,19,24,2,3,10,11,18,19,1,3,5,9,11,13,17,19,21,0,1,2,3,4,5,6,7,16,17,18,19,20,21,22,23,4,5,6,7,20,21,22,23,2,3,6,7,10,11,18,19,22,23,1,3,5,7,9,11,13,17,19,21,23,0,1,2,3,4,5,6,7,8,9,10,11,12,13,8,9,10,11,12,13,6,7,12,13,10,11,11};
+__device__ constexpr int8_t kMed25B[kMedian25Comparators] = {1,3,5,7,9,11,13,15,17,19,21,23,25,2,3,6,7,10,11,14,15,18,19,22,23,26,2,6,10,14,18,22,4,5,6,7,12,13,14,15,20,21,22,23,28,4,5,12,13,20,21,2,4,6,10,12,14,18,20,22,8,9,10,11,12,13,14,15,24,25,26,27,28,29,30,31,8,9,10,11,24,25,26,27,4,5,8,9,12,13,20,21,24,25,2,4,6,8,10,12,14,18,20,22,24,16,17,18,19,20,21,22,23,24,25,26,27,28,29,16,17,18,19,20,21,10,11,16,17,12,13,12};
+
+// The 5x5 window of every pixel of a 32x8 tile comes from a shared-memory copy
+// of the tile + 2-pixel halo (invalid / outside samples stored as +inf); the
+// window's in-image count follows from the position.
+__global__ void __launch_bounds__(256) median5_kernel(const float* __restrict__ in, int w, int h,
+                                                      float* __restrict__ out) {
     using namespace dev;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    constexpr int TW = 32, TH = 8, SW = TW + 4, SH = TH + 4;
+    __shared__ float s_t[SH][SW];
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+    const int tid = threadIdx.y * TW + threadIdx.x;
+    for (int r = tid; r < SW * SH; r += TW * TH) {
+        const int ty = r / SW, tx = r - ty * SW;
+        const int xx = x0 + tx - 2, yy = y0 + ty - 2;
+        float d = INFINITY;
+        if (xx >= 0 && yy >= 0 && xx < w && yy < h) {
+            d = __ldg(in + static_cast<size_t>(yy) * w + xx);
+            if (!depth_ok(d))
+                d = INFINITY;
+        }
+        s_t[ty][tx] = d;
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
     if (x >= w || y >= h)
         return;
     constexpr int N = 32;
     float v[N];
-    int in_image = 0, valid = 0;
+    int valid = 0;
 #pragma unroll
-    for (int dy = -2; dy <= 2; ++dy)
+    for (int dy = 0; dy < 5; ++dy)
 #pragma unroll
-        for (int dx = -2; dx <= 2; ++dx) {
-            const int xx = x + dx, yy = y + dy;
-            const int i = (dy + 2) * 5 + dx + 2;
-            float d = INFINITY;
-            if (xx >= 0 && yy >= 0 && xx < w && yy < h) {
-                ++in_image;
-                d = __ldg(in + static_cast<size_t>(yy) * w + xx);
-                if (depth_ok(d))
-                    ++valid;
-                else
-                    d = INFINITY;
-            }
-            v[i] = d;
+        for (int dx = 0; dx < 5; ++dx) {
+            const float d = s_t[threadIdx.y + dy][threadIdx.x + dx];
+            valid += d != INFINITY ? 1 : 0;
+            v[dy * 5 + dx] = d;
         }
+    const int in_image = (min(x + 2, w - 1) - max(x - 2, 0) + 1) * (min(y + 2, h - 1) - max(y - 2, 0) + 1);
 #pragma unroll
     for (int i = 25; i < N; ++i)
-        v[i] = INFINITY;
-#pragma unroll
-    for (int c = 0; c < kMedianComparators; ++c) {
-        const float lo = fminf(v[kMedianA[c]], v[kMedianB[c]]);
-        const float hi = fmaxf(v[kMedianA[c]], v[kMedianB[c]]);
-        v[kMedianA[c]] = lo;
-        v[kMedianB[c]] = hi;
-    }
+        v[i] = INFINITY;  // padding slots (both networks route through them)
     float res = 0.0f;
-    if (!(2 * valid < in_image)) {
-        const int k = valid / 2;
+    if (valid == 25) {
 #pragma unroll
-        for (int i = 0; i < 25; ++i)
-            res = k == i ? v[i] : res;
+        for (int c = 0; c < kMedian25Comparators; ++c) {
+            const float lo = fminf(v[kMed25A[c]], v[kMed25B[c]]);
+            const float hi = fmaxf(v[kMed25A[c]], v[kMed25B[c]]);
+            v[kMed25A[c]] = lo;
+            v[kMed25B[c]] = hi;
+        }
+        res = v[12];
+    } else {
+#pragma unroll
+        for (int c = 0; c < kMedianComparators; ++c) {
+            const float lo = fminf(v[kMedianA[c]], v[kMedianB[c]]);
+            const float hi = fmaxf(v[kMedianA[c]], v[kMedianB[c]]);
+            v[kMedianA[c]] = lo;
+            v[kMedianB[c]] = hi;
+        }
+        if (!(2 * valid < in_image)) {
+            const int k = valid / 2;
+#pragma unroll
+            for (int i = 0; i < 25; ++i)
+                res = k == i ? v[i] : res;
+        }
     }
     out[static_cast<size_t>(y) * w + x] = res;
 }
