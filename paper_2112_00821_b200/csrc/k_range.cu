@@ -70,13 +70,28 @@ __device__ __forceinline__ void pixel_range(const RangeArgs& a, int x, int y, fl
     *hi_f = hi;
 }
 
+// Plane stacks up to this size are staged in shared memory: the binary
+// searches of every pixel read them on their dependency chains.
+constexpr int kSmemPlanes = 2048;
+
 __global__ void __launch_bounds__(kRangeThreads) range_rows_kernel(RangeArgs a) {
     using namespace dev;
     using Scan = cub::BlockScan<uint32_t, kRangeThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ uint32_t carry;
+    extern __shared__ double s_stack[];  // [nplanes | ncoarser] when both fit
     const int y = blockIdx.x;
     const int w = a.intr.w;
+    if (a.nplanes <= kSmemPlanes && (!a.coarser || a.ncoarser <= kSmemPlanes)) {
+        for (int i = threadIdx.x; i < a.nplanes; i += kRangeThreads)
+            s_stack[i] = a.planes[i];
+        if (a.coarser)
+            for (int i = threadIdx.x; i < a.ncoarser; i += kRangeThreads)
+                s_stack[a.nplanes + i] = a.coarser[i];
+        a.planes = s_stack;
+        if (a.coarser)
+            a.coarser = s_stack + a.nplanes;
+    }
     if (threadIdx.x == 0)
         carry = 0;
     __syncthreads();
@@ -105,7 +120,7 @@ __global__ void __launch_bounds__(kRangeThreads) range_rows_kernel(RangeArgs a) 
                 int l = 0, r = n;
                 while (l < r) {
                     const int m = (l + r) >> 1;
-                    if (mul(scale, __ldg(a.planes + m)) > hid)
+                    if (mul(scale, a.planes[m]) > hid)
                         l = m + 1;
                     else
                         r = m;
@@ -116,7 +131,7 @@ __global__ void __launch_bounds__(kRangeThreads) range_rows_kernel(RangeArgs a) 
                 r = n;
                 while (l < r) {
                     const int m = (l + r) >> 1;
-                    if (mul(scale, __ldg(a.planes + m)) < lod)
+                    if (mul(scale, a.planes[m]) < lod)
                         r = m;
                     else
                         l = m + 1;
@@ -168,7 +183,12 @@ __global__ void __launch_bounds__(1024) scan_rows_kernel(const uint32_t* __restr
 }  // namespace
 
 void range_rows(const RangeArgs& a, cudaStream_t s) {
-    range_rows_kernel<<<a.intr.h, kRangeThreads, 0, s>>>(a);
+    const size_t smem = (a.nplanes <= kSmemPlanes && (!a.coarser || a.ncoarser <= kSmemPlanes))
+                            ? sizeof(double) * (a.nplanes + (a.coarser ? a.ncoarser : 0))
+                            : 0;
+    // <= 32 KB: within the default dynamic shared-memory limit (no attribute
+    // call -- concurrent host threads would race on a per-launch setting)
+    range_rows_kernel<<<a.intr.h, kRangeThreads, smem, s>>>(a);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

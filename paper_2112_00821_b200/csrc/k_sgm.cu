@@ -1098,8 +1098,18 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
 }
 
 // compute_normal_offsets (sgm.cpp:252-299) on the upscaled prior maps.
+constexpr int kOffsetSmemPlanes = 4096;
+
 __global__ void normal_offsets_kernel(OffsetArgs a) {
     using namespace dev;
+    // the plane stack in shared memory (binary searches on every pixel's chain)
+    extern __shared__ double s_stack[];
+    if (a.nplanes <= kOffsetSmemPlanes) {
+        for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < a.nplanes; i += blockDim.x * blockDim.y)
+            s_stack[i] = a.planes[i];
+        a.planes = s_stack;
+        __syncthreads();
+    }
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.w || y >= a.h)
@@ -1150,17 +1160,21 @@ __global__ void normal_offsets_kernel(OffsetArgs a) {
 
 }  // namespace
 
+// Dynamic shared-memory attributes are set to each kernel's LARGEST possible
+// size, a constant: contexts on other host threads launch the same kernels
+// with other sizes, and a per-launch setting could shrink the limit between
+// another thread's set and launch.
+constexpr int kSgmSmemMax = 200 * 1024;  // sgm_kernel: kWarps x 2 x pmax words, pmax <= sgm_smem_pmax_limit()
+
 template <int VARIANT>
 void launch_sgm(const SgmArgs& a, int total, int blocks, size_t smem, bool fast32, cudaStream_t s) {
     if (fast32) {
         FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_kernel<VARIANT, int>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem)));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSgmSmemMax));
         sgm_kernel<VARIANT, int><<<blocks, kWarps * 32, smem, s>>>(a, total);
     } else {
         FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_kernel<VARIANT, long long>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem)));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSgmSmemMax));
         sgm_kernel<VARIANT, long long><<<blocks, kWarps * 32, smem, s>>>(a, total);
     }
 }
@@ -1175,9 +1189,14 @@ void launch_lanes(const SgmArgs& a, int total, cudaStream_t s) {
     stride += ((G % 32) - stride % 32 + 32) % 32;
     const int blocks = (total + kWarps * LPW - 1) / (kWarps * LPW);
     const size_t smem = static_cast<size_t>(kWarps) * LPW * stride * sizeof(uint32_t);
+    // largest: group_caps <= 1024 with one line per warp (dense coarsest
+    // levels), 32 otherwise (refined levels, stage API)
+    constexpr int kCapsMax = G == 32 ? 1024 : 32;
+    if (caps > kCapsMax)
+        throw Error(FMVS_ERR_CONFIG, "sgm: path buffer capacity exceeds the kernel's shared memory");
+    const int smem_max = kWarps * LPW * (2 * (kCapsMax + 2 * kSent) + 32) * static_cast<int>(sizeof(uint32_t));
     FMVS_CUDA_CHECK(cudaFuncSetAttribute(sgm_lanes_kernel<VARIANT, V, G, K>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     sgm_lanes_kernel<VARIANT, V, G, K><<<blocks, kWarps * 32, smem, s>>>(a, total, caps, stride);
 }
 
@@ -1223,9 +1242,13 @@ void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
     constexpr bool kEmb = G == 4 && K <= 4;
     const bool emb = kEmb && emb_on;
     sgm_prep_kernel<<<(npx + 255) / 256, 256, 0, s>>>(a, rec, fl, caps, emb);
+    // the attribute is set to this instantiation's largest possible size (a
+    // constant: contexts on other host threads launch the same kernel)
+    const int smem_max = static_cast<int>((256 + static_cast<size_t>(kWarps) * LPW * stride + 1) *
+                                              sizeof(uint32_t) +
+                                          (PG ? static_cast<size_t>(kRecPlanes) * sizeof(double) : 0));
     auto go = [&](auto kernel) {
-        FMVS_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem)));
+        FMVS_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
         kernel<<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
     };
     if (emb && a.agg16)
@@ -1370,7 +1393,10 @@ int sgm_smem_pmax_limit() { return (200 * 1024) / (kWarps * 2 * 4); }
 void normal_offsets(const OffsetArgs& a, cudaStream_t s) {
     const dim3 block(32, 8);
     const dim3 grid((a.w + 31) / 32, (a.h + 7) / 8);
-    normal_offsets_kernel<<<grid, block, 0, s>>>(a);
+    const size_t smem = a.nplanes <= kOffsetSmemPlanes ? sizeof(double) * a.nplanes : 0;
+    // <= 32 KB: within the default dynamic shared-memory limit (no attribute
+    // call -- concurrent host threads would race on a per-launch setting)
+    normal_offsets_kernel<<<grid, block, smem, s>>>(a);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -1645,9 +1645,13 @@ void launch_ncc_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
     const size_t smem = (sizeof(int) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1) +
                         sizeof(int16_t) * NM * kTiledThreads + 16 +
                         (a.plane_slicing ? sizeof(uint16_t) * kTiledThreads * (kRunNcc + 2) : 0);
+    // attribute: the largest size (with the dense-level run staging), a
+    // constant -- contexts on other host threads launch the same kernel
+    const int smem_max = static_cast<int>((sizeof(int) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1) +
+                                          sizeof(int16_t) * NM * kTiledThreads + 16 +
+                                          sizeof(uint16_t) * kTiledThreads * (kRunNcc + 2));
     FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_ncc_tiled<WW, WH, NM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     sweep_ncc_tiled<WW, WH, NM><<<grid, kTiledThreads, smem, s>>>(a);
 }
 
