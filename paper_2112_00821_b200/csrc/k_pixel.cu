@@ -237,11 +237,16 @@ __device__ __forceinline__ float conf_of(float nx, float ny, float nz, double co
 // of every thread re-loading its 5x5 neighbourhood from L1. Same arithmetic,
 // same order as smooth_conf_kernel below.
 constexpr int kSmMaxR = 4;
+// R: the smoothing radius as a compile-time constant (1..kSmMaxR) so the
+// neighbour loop unrolls and every weight / normal load is issued ahead of the
+// FP64 accumulation chain; R = 0: runtime radius.
+template <int R>
 __global__ void smooth_conf_tiled_kernel(const float* __restrict__ raw, const uint8_t* __restrict__ img,
-                                         int w, int h, int radius, const double* __restrict__ wt,
+                                         int w, int h, int radius_rt, const double* __restrict__ wt,
                                          float* __restrict__ out, float* __restrict__ conf,
                                          double cos_rho, double pdv, double sx, double sy, double sz) {
     using namespace dev;
+    const int radius = R > 0 ? R : radius_rt;
     constexpr int TW = 32 + 2 * kSmMaxR, TH = 8 + 2 * kSmMaxR;
     __shared__ float s_n[3][TH][TW];
     __shared__ int s_i[TH][TW];  // intensity, or -1 where the normal is invalid / outside
@@ -276,18 +281,29 @@ __global__ void smooth_conf_tiled_kernel(const float* __restrict__ raw, const ui
     if (s_i[cy0][cx0] >= 0) {
         double sx_ = double(cx), sy_ = double(cy), sz_ = double(cz);
         const int ic = s_i[cy0][cx0];
-        for (int dy = -radius; dy <= radius; ++dy)
-            for (int dx = -radius; dx <= radius; ++dx) {
+#pragma unroll
+        for (int dy = -(R > 0 ? R : kSmMaxR); dy <= (R > 0 ? R : kSmMaxR); ++dy) {
+            if (R == 0 && (dy < -radius || dy > radius))
+                continue;
+#pragma unroll
+            for (int dx = -(R > 0 ? R : kSmMaxR); dx <= (R > 0 ? R : kSmMaxR); ++dx) {
+                if (R == 0 && (dx < -radius || dx > radius))
+                    continue;
                 if (dx == 0 && dy == 0)
                     continue;
                 const int iq = s_i[cy0 + dy][cx0 + dx];
-                if (iq < 0)
-                    continue;  // outside the image or invalid normal (surface.cpp:63-67)
-                const double wq = __ldg(wt + (dx * dx + dy * dy) * 256 + abs(iq - ic));
-                sx_ = add(sx_, mul(wq, double(s_n[0][cy0 + dy][cx0 + dx])));
-                sy_ = add(sy_, mul(wq, double(s_n[1][cy0 + dy][cx0 + dx])));
-                sz_ = add(sz_, mul(wq, double(s_n[2][cy0 + dy][cx0 + dx])));
+                // outside the image or invalid normal: skipped (surface.cpp:63-67)
+                // -- a select, so the sums keep the reference's exact sequence
+                const bool use = iq >= 0;
+                const double wq = __ldg(wt + (dx * dx + dy * dy) * 256 + (use ? abs(iq - ic) : 0));
+                const double ax = add(sx_, mul(wq, double(s_n[0][cy0 + dy][cx0 + dx])));
+                const double ay = add(sy_, mul(wq, double(s_n[1][cy0 + dy][cx0 + dx])));
+                const double az = add(sz_, mul(wq, double(s_n[2][cy0 + dy][cx0 + dx])));
+                sx_ = use ? ax : sx_;
+                sy_ = use ? ay : sy_;
+                sz_ = use ? az : sz_;
             }
+        }
         const double len = norm3(D3{sx_, sy_, sz_});
         if (len > 1e-15) {
             ox = __double2float_rn(div(sx_, len));
@@ -402,10 +418,18 @@ void normals_raw(const float* depth, int w, int h, dev::Intr intr, float* out_xy
 void smooth_conf(const float* raw_xyz, const uint8_t* img, int w, int h, int radius,
                  const double* weights, float* out_xyz, float* conf, double cos_rho,
                  double plane_dot_view, double nx, double ny, double nz, cudaStream_t s) {
-    if (radius <= kSmMaxR)
-        smooth_conf_tiled_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(raw_xyz, img, w, h, radius, weights,
-                                                                      out_xyz, conf, cos_rho,
-                                                                      plane_dot_view, nx, ny, nz);
+    auto tiled = [&](auto kernel) {
+        kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(raw_xyz, img, w, h, radius, weights, out_xyz, conf,
+                                                     cos_rho, plane_dot_view, nx, ny, nz);
+    };
+    if (radius == 1)
+        tiled(smooth_conf_tiled_kernel<1>);
+    else if (radius == 2)
+        tiled(smooth_conf_tiled_kernel<2>);
+    else if (radius == 3)
+        tiled(smooth_conf_tiled_kernel<3>);
+    else if (radius <= kSmMaxR)
+        tiled(smooth_conf_tiled_kernel<0>);
     else
         smooth_conf_kernel<<<grid2(w, h), dim3(32, 8), 0, s>>>(raw_xyz, img, w, h, radius, weights,
                                                                 out_xyz, conf, cos_rho,
