@@ -1129,7 +1129,14 @@ __global__ void normal_offsets_kernel(OffsetArgs a) {
     if (normal_ok(nfx, nfy, nfz) && depth_ok(depth)) {
         const D3 n{double(nfx), double(nfy), double(nfz)};
         const D3 pn{a.nx, a.ny, a.nz};
-        const D3 ray = unproject(a.intr, double(x), double(y));
+        // the rays of (x, y) and of its 4 canonical predecessors share five
+        // coordinate divisions (unproject, geometry.hpp:28-30)
+        const double ux0 = div(sub(double(x), a.intr.cx), a.intr.fx);
+        const double ux1 = div(sub(double(x - 1), a.intr.cx), a.intr.fx);
+        const double uy0 = div(sub(double(y), a.intr.cy), a.intr.fy);
+        const double uym = div(sub(double(y - 1), a.intr.cy), a.intr.fy);
+        const double uyp = div(sub(double(y + 1), a.intr.cy), a.intr.fy);
+        const D3 ray{ux0, uy0, 1.0};
         const double denom0 = dot3(pn, ray);
         if (!(fabs(denom0) < 1e-12 || div(-1.0, denom0) <= 0.0)) {
             const double delta_anchor = mul(double(depth), -denom0);
@@ -1137,9 +1144,7 @@ __global__ void normal_offsets_kernel(OffsetArgs a) {
             const D3 anchor = scale3(div(-a.planes[i0], denom0), ray);
             const int cd[4][2] = {{1, 0}, {0, 1}, {1, 1}, {1, -1}};
             for (int c = 0; c < 4; ++c) {
-                const double qx = double(x - cd[c][0]);
-                const double qy = double(y - cd[c][1]);
-                const D3 ray_q = unproject(a.intr, qx, qy);
+                const D3 ray_q{cd[c][0] ? ux1 : ux0, cd[c][1] == 0 ? uy0 : (cd[c][1] > 0 ? uym : uyp), 1.0};
                 const double denom_t = dot3(n, ray_q);
                 if (fabs(denom_t) < 1e-12)
                     continue;
