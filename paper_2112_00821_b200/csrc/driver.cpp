@@ -673,8 +673,8 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         // pixel, 2.36 -> 2.61 ms). Only the uniform (coarsest, one line per
         // warp, long contiguous runs) levels qualify: C4 L2 1.8x less DRAM.
         const uint64_t known_entries = have_prior ? 0 : entries_bound;
-        ga.agg16 = ctx->agg16 && known_entries > (uint64_t(48) << 20) &&
-                   k::sgm_agg16_ok(ga, 255ll * std::max(ref, nmatch - ref));
+        ga.cost_max = 255 * std::max(ref, nmatch - ref);
+        ga.agg16 = ctx->agg16 && known_entries > (uint64_t(48) << 20) && k::sgm_agg16_ok(ga, ga.cost_max);
         // the SGM accumulator of the level (make_accumulator, sgm.cpp:198-208)
         ctx->timed("zero", [&] { k::zero_entries(agg, rb + P.h, s, ga.agg16 != 0); });
         ++launches;
@@ -1420,6 +1420,7 @@ int aggregate_impl(fmvs_ctx* ctx, int32_t w, int32_t h, const fmvs_plane_stack* 
         ga.row_base = t.upload(rb.data(), rb.size(), s);
         ga.costs = t.upload(costs, total, s);
         ga.agg = t.alloc<uint32_t>(total + k::kAggSlack);
+        ga.cost_max = total > 0 ? static_cast<int>(*std::max_element(costs, costs + total)) : -1;
         FMVS_CUDA_CHECK(cudaMemsetAsync(ga.agg, 0, std::max<uint64_t>(total, 1) * 4, s));
         ga.image = t.upload(image, px, s);
         ga.variant = cfg->variant;

@@ -704,14 +704,19 @@ __device__ __forceinline__ void red_add(uint32_t* agg, bool p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0+%1], %2;" : : "l"(agg), "n"(OFF), "r"(p ? v : 0u));
 }
 
-__global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps, bool embed) {
+// embed: 0 head only (16-byte records), 1 + u16 costs (48 bytes: slot 4*gl + k
+// = hypothesis gl + 4k), 2 + 10-bit costs (32 bytes: lane gl's word holds
+// hypotheses gl + 4k, k < 3, at bits 10k); see LinePipe.
+__global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps, int embed) {
     const int n = a.w * a.h;
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p > n)
         return;
-    uint4* r = rec + 3 * static_cast<size_t>(p);
+    const int rs = embed == 0 ? 1 : (embed == 1 ? 3 : 2);
+    uint4* r = rec + static_cast<size_t>(rs) * p;
     if (p == n) {  // the dummy record read past the end of a line
-        r[0] = r[1] = r[2] = make_uint4(0u, 0u, 0u, 0u);
+        for (int k = 0; k < rs; ++k)
+            r[k] = make_uint4(0u, 0u, 0u, 0u);
         return;
     }
     const int y = p / a.w, x = p - y * a.w;
@@ -730,27 +735,37 @@ __global__ void sgm_prep_kernel(SgmArgs a, uint4* rec, LineFlags fl, int caps, b
         h.z = h.w = 0u;
     }
     r[0] = h;
-    if (!embed)
-        goto flags;
-    {
-    // embedded costs, lane-major: u16 slot 4*gl + k = hypothesis gl + 4k
-    uint32_t e[8];
+    if (embed == 1) {
+        uint32_t e[8];
 #pragma unroll
-    for (int sl = 0; sl < 16; sl += 2) {
-        uint32_t v2 = 0u;
+        for (int sl = 0; sl < 16; sl += 2) {
+            uint32_t v2 = 0u;
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-            const int slot = sl + h2;
-            const int i = (slot >> 2) + 4 * (slot & 3);
-            if (c <= kEmbed && i < c)
-                v2 |= static_cast<uint32_t>(a.costs[base + i]) << (16 * h2);
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int slot = sl + h2;
+                const int i = (slot >> 2) + 4 * (slot & 3);
+                if (c <= kEmbed && i < c)
+                    v2 |= static_cast<uint32_t>(a.costs[base + i]) << (16 * h2);
+            }
+            e[sl >> 1] = v2;
         }
-        e[sl >> 1] = v2;
+        r[1] = make_uint4(e[0], e[1], e[2], e[3]);
+        r[2] = make_uint4(e[4], e[5], e[6], e[7]);
+    } else if (embed == 2) {
+        uint32_t e[4];
+#pragma unroll
+        for (int gl = 0; gl < 4; ++gl) {
+            uint32_t wd = 0u;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int i = gl + 4 * k;
+                if (c <= 12 && i < c)
+                    wd |= (static_cast<uint32_t>(a.costs[base + i]) & 0x3FFu) << (10 * k);
+            }
+            e[gl] = wd;
+        }
+        r[1] = make_uint4(e[0], e[1], e[2], e[3]);
     }
-    r[1] = make_uint4(e[0], e[1], e[2], e[3]);
-    r[2] = make_uint4(e[4], e[5], e[6], e[7]);
-    }
-flags:
     if (c > caps) {
         atomicOr(fl.row + y, 1u);
         atomicOr(fl.col + x, 1u);
@@ -773,24 +788,30 @@ struct LineCtx {
     bool off_hi;
     int x0, y0, dx, dy;  // first pixel and step of the line (PG scene points)
     const double* planes;  // PG: the plane stack (shared-memory copy)
+    int rs;                // record stride in 16-byte units (1: head only, 3: + u16 costs, 2: + 10-bit costs)
 };
 
 // Operand pipeline of the line kernel: records of pixels j+1..j+S-1 and the
 // costs / phi2 of pixels j+1..j+S-1-GAP in registers at the step of pixel j.
 // EMB: the costs come with the record (embedded copy, G = 4, K <= 4) and phi2
 // is looked up at use; otherwise they are loaded GAP steps after the record.
-template <bool SN, int G, int K, int S, int GAP, bool EMB>
+// EMB: 0 costs from the volume (loaded GAP steps after the record), 1 u16
+// costs embedded in the record, 2 10-bit costs packed one word per lane (K <=
+// 3, every cost < 1024); with 1 and 2 phi2 is looked up a step ahead.
+template <bool SN, int G, int K, int S, int GAP, int EMB>
 struct LinePipe {
     static_assert(!EMB || (G == 4 && K <= 4), "embedded costs hold 4 slots for 4 lanes");
+    static_assert(EMB != 2 || K <= 3, "three 10-bit costs per lane word");
     uint4 R[S];
-    uint2 E[EMB ? S : 1];
+    uint2 E[EMB == 1 ? S : 1];
+    uint32_t E10[EMB == 2 ? S : 1];
     uint32_t C[EMB ? 1 : S][K];
     int PH[EMB ? 1 : S];
     int q, jn;
 
     __device__ __forceinline__ void load_rec(const LineCtx& lc, int si) {
         const int idx = jn < lc.n ? q : lc.dummy;
-        const uint4* r = lc.rec + 3 * idx;
+        const uint4* r = lc.rec + lc.rs * idx;
         if (SN) {
             R[si] = __ldg(r);
         } else {
@@ -799,15 +820,19 @@ struct LinePipe {
             R[si].y = v.y;
             R[si].z = R[si].w = 0u;
         }
-        if constexpr (EMB)
+        if constexpr (EMB == 1)
             E[si] = __ldg(reinterpret_cast<const uint2*>(r + 1) + lc.gl);
+        else if constexpr (EMB == 2)
+            E10[si] = __ldg(reinterpret_cast<const uint32_t*>(r + 1) + lc.gl);
         q += lc.dp;
         ++jn;
     }
     // first-pass cost k of the pixel in slot u
     __device__ __forceinline__ uint32_t cost(int u, int k) const {
-        if constexpr (EMB)
+        if constexpr (EMB == 1)
             return ((k < 2 ? E[u].x : E[u].y) >> (16 * (k & 1))) & 0xFFFFu;
+        else if constexpr (EMB == 2)
+            return (E10[u] >> (10 * k)) & 0x3FFu;
         else
             return C[u][k];
     }
@@ -855,7 +880,7 @@ struct LinePipe {
 // step bodies, with the predecessor window loaded a step early, ran 1.8x
 // slower at level 0, with the same loads staged through shared memory by
 // cp.async too).
-template <bool SN, int G, int K, int S, int GAP, bool SHARED, bool EMB, bool AGG16, bool PG>
+template <bool SN, int G, int K, int S, int GAP, bool SHARED, int EMB, bool AGG16, bool PG>
 __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, uint32_t* bufA,
                                           uint32_t* bufB) {
     constexpr int PASS = G * K;
@@ -1017,7 +1042,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
     }
 }
 
-template <bool SN, int G, int K, int S, int GAP, bool EMB, bool AGG16, bool PG>
+template <bool SN, int G, int K, int S, int GAP, int EMB, bool AGG16, bool PG>
 __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const uint4* __restrict__ rec,
                                                                LineFlags fl, int total_lines, int stride) {
     constexpr int LPW = 32 / G;
@@ -1066,6 +1091,7 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
     lc.off_sh = (slot & 1) * 16;
     lc.off_hi = (slot >> 1) != 0;
     lc.planes = s_planes;
+    lc.rs = EMB == 0 ? 1 : (EMB == 1 ? 3 : 2);
     lc.x0 = x;
     lc.y0 = y;
     lc.dx = dx;
@@ -1090,7 +1116,7 @@ __global__ void __launch_bounds__(kWarps * 32) sgm_line_kernel(SgmArgs a, const 
             }
         }
         __syncwarp();
-        line_steps<SN, G, K, S, GAP, false, false, AGG16, PG>(a, lc, bufA, bufB);
+        line_steps<SN, G, K, S, GAP, false, 0, AGG16, PG>(a, lc, bufA, bufB);
     } else {
         __syncwarp();
         line_steps<SN, G, K, S, GAP, true, EMB, AGG16, PG>(a, lc, sA, sB);
@@ -1244,8 +1270,10 @@ void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
         const char* e = std::getenv("FMVS_SGM_EMB");
         return !(e && e[0] == '0');
     }();
-    constexpr bool kEmb = G == 4 && K <= 4;
-    const bool emb = kEmb && emb_on;
+    // 10-bit packing when every cost of the volume is < 1024 (the host's
+    // bound, SgmArgs::cost_max) and a lane holds <= 3 hypotheses
+    constexpr int kEmb = (G == 4 && K <= 4) ? ((K <= 3) ? 2 : 1) : 0;
+    const int emb = !emb_on ? 0 : (kEmb == 2 && !(a.cost_max >= 0 && a.cost_max < 1024) ? 1 : kEmb);
     sgm_prep_kernel<<<(npx + 255) / 256, 256, 0, s>>>(a, rec, fl, caps, emb);
     // the attribute is set to this instantiation's largest possible size (a
     // constant: contexts on other host threads launch the same kernel)
@@ -1256,14 +1284,19 @@ void launch_line_sg(const SgmArgs& a, int total, cudaStream_t s) {
         FMVS_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
         kernel<<<blocks, kWarps * 32, smem, s>>>(a, rec, fl, total, stride);
     };
-    if (emb && a.agg16)
+    constexpr int kEmb1 = kEmb ? 1 : 0;
+    if (emb == 2 && a.agg16)
         go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, true, PG>);
-    else if (emb)
+    else if (emb == 2)
         go(sgm_line_kernel<SN, G, K, S, GAP, kEmb, false, PG>);
+    else if (emb == 1 && a.agg16)
+        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb1, true, PG>);
+    else if (emb == 1)
+        go(sgm_line_kernel<SN, G, K, S, GAP, kEmb1, false, PG>);
     else if (a.agg16)
-        go(sgm_line_kernel<SN, G, K, S, GAP, false, true, PG>);
+        go(sgm_line_kernel<SN, G, K, S, GAP, 0, true, PG>);
     else
-        go(sgm_line_kernel<SN, G, K, S, GAP, false, false, PG>);
+        go(sgm_line_kernel<SN, G, K, S, GAP, 0, false, PG>);
 }
 
 // Pipeline depth S (pixels whose records are in registers; measured 6 / 8 /

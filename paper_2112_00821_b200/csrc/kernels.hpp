@@ -143,6 +143,8 @@ struct SgmArgs {
     // packed aggregate: entry e is the u16 at index e of `agg` (two per 32-bit
     // word; set only when sgm_agg16_ok proved every sum fits 16 bits)
     int agg16;
+    // upper bound of every matching cost in the volume (-1: unknown, u16)
+    int cost_max;
 };
 // the line kernel runs this configuration (else the general kernel)
 bool sgm_line_applicable(const SgmArgs& a);
