@@ -105,13 +105,39 @@ __global__ void blur_halve_batch_kernel(ImgBatch b, double k0, double k1, double
     j.out[static_cast<size_t>(y) * j.wout + x] = static_cast<uint8_t>(v);
 }
 
+// Four quads per thread from two aligned 32-bit row loads (+ the byte right
+// of them) and byte permutes, written as one 16-byte store; images whose
+// rows or buffers are not 4 / 16-byte aligned take the per-pixel path.
 __global__ void pack_quads_batch_kernel(ImgBatch b) {
     const ImgJob& j = b.job[blockIdx.z];
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int w = j.win, h = j.hin;
+    const bool vec = (w & 3) == 0 && (reinterpret_cast<uintptr_t>(j.in) & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(j.quad) & 15) == 0;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (vec) {
+        const int x0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+        if (x0 >= w || y >= h)
+            return;
+        const int y1 = min(y + 1, h - 1);
+        const uint8_t* r0 = j.in + static_cast<size_t>(y) * w;
+        const uint8_t* r1 = j.in + static_cast<size_t>(y1) * w;
+        const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(r0 + x0));
+        const uint32_t c = __ldg(reinterpret_cast<const uint32_t*>(r1 + x0));
+        const int xr = min(x0 + 4, w - 1);  // x1 of the group's last pixel (edge clamp)
+        const uint32_t a4 = __ldg(r0 + xr), c4 = __ldg(r1 + xr);
+        uint32_t q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t top = __byte_perm(a, a4, static_cast<uint32_t>(k | ((k + 1) << 4)));
+            const uint32_t bot = __byte_perm(c, c4, static_cast<uint32_t>(k | ((k + 1) << 4)));
+            q[k] = __byte_perm(top, bot, 0x5410);
+        }
+        *reinterpret_cast<uint4*>(j.quad + static_cast<size_t>(y) * w + x0) = make_uint4(q[0], q[1], q[2], q[3]);
+        return;
+    }
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= j.win || y >= j.hin)
         return;
-    const int w = j.win, h = j.hin;
     const int x1 = min(x + 1, w - 1), y1 = min(y + 1, h - 1);
     const uint8_t* r0 = j.in + static_cast<size_t>(y) * w;
     const uint8_t* r1 = j.in + static_cast<size_t>(y1) * w;
@@ -135,8 +161,11 @@ void blur_halve_batch(const ImgBatch& b, int n, const double k3[3], cudaStream_t
 void pack_quads_batch(const ImgBatch& b, int n, cudaStream_t s) {
     int mw = 1, mh = 1;
     for (int i = 0; i < n; ++i) {
-        mw = max(mw, b.job[i].win);
-        mh = max(mh, b.job[i].hin);
+        const ImgJob& j = b.job[i];
+        const bool vec = (j.win & 3) == 0 && (reinterpret_cast<uintptr_t>(j.in) & 3) == 0 &&
+                         (reinterpret_cast<uintptr_t>(j.quad) & 15) == 0;
+        mw = max(mw, vec ? j.win / 4 : j.win);  // threads along x (4 pixels each when vec)
+        mh = max(mh, j.hin);
     }
     pack_quads_batch_kernel<<<dim3((mw + 31) / 32, (mh + 7) / 8, n), dim3(32, 8), 0, s>>>(b);
     FMVS_CUDA_CHECK(cudaGetLastError());
