@@ -19,6 +19,11 @@ namespace dev {
 struct Intr {
     double fx, fy, cx, cy;
     int w, h;
+    // optional per-level unprojection tables (device): ux[x + 1] =
+    // (x - cx) / fx for x in [-1, w], uy[y + 1] likewise -- the exact values
+    // of unproject's two divisions, built on the host (IEEE division)
+    const double* ux = nullptr;
+    const double* uy = nullptr;
 };
 inline Intr make_intr(const fmvs_intrinsics& k) { return {k.fx, k.fy, k.cx, k.cy, k.width, k.height}; }
 
@@ -57,6 +62,13 @@ __device__ __forceinline__ double norm3(D3 a) { return sqrt_(dot3(a, a)); }
 // Intrinsics::unproject (geometry.hpp:28-30).
 __device__ __forceinline__ D3 unproject(const Intr& k, double x, double y) {
     return {div(sub(x, k.cx), k.fx), div(sub(y, k.cy), k.fy), 1.0};
+}
+// unproject of an integer pixel, from the tables when the level has them
+__device__ __forceinline__ D3 unproject_px(const Intr& k, int x, int y) {
+    if (k.ux && static_cast<unsigned>(x + 1) <= static_cast<unsigned>(k.w + 1) &&
+        static_cast<unsigned>(y + 1) <= static_cast<unsigned>(k.h + 1))
+        return {k.ux[x + 1], k.uy[y + 1], 1.0};
+    return unproject(k, double(x), double(y));
 }
 
 // float validity predicates (raster.hpp:64-65), evaluated in float.

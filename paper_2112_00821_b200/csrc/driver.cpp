@@ -171,6 +171,7 @@ struct LevelPlan {
     std::vector<double> homs;           // [nmatch][P][9]
     // offsets into the uploaded plan blob (in doubles)
     size_t off_planes = 0, off_homs = 0;
+    size_t off_ux = 0, off_uy = 0;      // the reference view's unprojection tables
     size_t img_off = 0;                 // per-level byte offset of the image block
     size_t quad_off = 0;                // per-level u32 offset of the quad block
 };
@@ -372,6 +373,10 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         nd += P.planes.size();
         P.off_homs = nd;
         nd += P.homs.size();
+        P.off_ux = nd;
+        nd += static_cast<size_t>(P.intr[ref].width) + 2;
+        P.off_uy = nd;
+        nd += static_cast<size_t>(P.intr[ref].height) + 2;
     }
     const size_t off_swt = nd;
     nd += swt.size();
@@ -403,6 +408,12 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
     for (auto& P : lv) {
         std::memcpy(h_blob + P.off_planes, P.planes.data(), P.planes.size() * 8);
         std::memcpy(h_blob + P.off_homs, P.homs.data(), P.homs.size() * 8);
+        // unproject's divisions (geometry.hpp:28-30), x / y in [-1, size]
+        const fmvs_intrinsics& k = P.intr[ref];
+        for (int x = -1; x <= k.width; ++x)
+            h_blob[P.off_ux + x + 1] = (double(x) - k.cx) / k.fx;
+        for (int y = -1; y <= k.height; ++y)
+            h_blob[P.off_uy + y + 1] = (double(y) - k.cy) / k.fy;
     }
     std::memcpy(h_blob + off_swt, swt.data(), swt.size() * 8);
     std::memcpy(h_blob + off_phi2, phi2.data(), 256 * 8);
@@ -536,7 +547,9 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         const LevelPlan& P = lv[l];
         const int np = static_cast<int>(P.planes.size());
         const double* d_planes = d_blob + P.off_planes;
-        const fmvs::dev::Intr intr = intr_of(P.intr[ref]);
+        fmvs::dev::Intr intr = intr_of(P.intr[ref]);
+        intr.ux = d_blob + P.off_ux;
+        intr.uy = d_blob + P.off_uy;
         uint64_t* rb = row_base + static_cast<size_t>(l) * (max_h + 1);
         const bool have_prior = l < L - 1;
 

@@ -77,7 +77,7 @@ __global__ void wta_depth_kernel(WtaArgs a) {
     if (!a.depth)
         return;
     // pipeline.cpp:263-288
-    const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject(a.intr, double(x), double(y)));
+    const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject_px(a.intr, x, y));
     const double d_win = depth_from_plane_dev(denom, a.planes[win]);
     float out = 0.0f;
     if (d_win > 0.0) {
@@ -196,10 +196,10 @@ __global__ void normals_raw_kernel(const float* __restrict__ depth, int w, int h
         const float dl = depth[p - 1], dr = depth[p + 1];
         const float du = depth[p - w], dd = depth[p + w];
         if (depth_ok(dc) && depth_ok(dl) && depth_ok(dr) && depth_ok(du) && depth_ok(dd)) {
-            const D3 pr = scale3(double(dr), unproject(k, double(x + 1), double(y)));
-            const D3 pl = scale3(double(dl), unproject(k, double(x - 1), double(y)));
-            const D3 pd = scale3(double(dd), unproject(k, double(x), double(y + 1)));
-            const D3 pu = scale3(double(du), unproject(k, double(x), double(y - 1)));
+            const D3 pr = scale3(double(dr), unproject_px(k, x + 1, y));
+            const D3 pl = scale3(double(dl), unproject_px(k, x - 1, y));
+            const D3 pd = scale3(double(dd), unproject_px(k, x, y + 1));
+            const D3 pu = scale3(double(du), unproject_px(k, x, y - 1));
             const D3 hv = sub3(pr, pl);
             const D3 vv = sub3(pd, pu);
             D3 n = cross3(hv, vv);

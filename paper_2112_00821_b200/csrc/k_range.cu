@@ -43,7 +43,7 @@ __device__ __forceinline__ void pixel_range(const RangeArgs& a, int x, int y, fl
             double dd = a.policy_value;
             bool keep = true;
             if (a.policy == FMVS_RANGE_SPACING_MULTIPLE) {
-                const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject(a.intr, double(x), double(y)));
+                const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject_px(a.intr, x, y));
                 if (fabs(denom) < 1e-12) {
                     keep = false;
                 } else {
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kRangeThreads) range_rows_kernel(RangeArgs a) 
                 a.hi_out[p] = hi;
             }
             // pixel_depth_scale (matching.cpp:84-90)
-            const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject(a.intr, double(x), double(y)));
+            const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject_px(a.intr, x, y));
             double scale = 0.0;
             if (!(fabs(denom) < 1e-12)) {
                 const double s = div(-1.0, denom);

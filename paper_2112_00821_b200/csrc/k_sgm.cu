@@ -919,7 +919,7 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
             dev::D3 ray{0.0, 0.0, 1.0};
             double denom = 0.0;
             if constexpr (PG) {
-                ray = dev::unproject(a.intr, double(px), double(py));
+                ray = dev::unproject_px(a.intr, px, py);
                 denom = dev::dot3(dev::D3{a.nx, a.ny, a.nz}, ray);
             }
             if (c > 0) {
@@ -1157,11 +1157,9 @@ __global__ void normal_offsets_kernel(OffsetArgs a) {
         const D3 pn{a.nx, a.ny, a.nz};
         // the rays of (x, y) and of its 4 canonical predecessors share five
         // coordinate divisions (unproject, geometry.hpp:28-30)
-        const double ux0 = div(sub(double(x), a.intr.cx), a.intr.fx);
-        const double ux1 = div(sub(double(x - 1), a.intr.cx), a.intr.fx);
-        const double uy0 = div(sub(double(y), a.intr.cy), a.intr.fy);
-        const double uym = div(sub(double(y - 1), a.intr.cy), a.intr.fy);
-        const double uyp = div(sub(double(y + 1), a.intr.cy), a.intr.fy);
+        const D3 r00 = unproject_px(a.intr, x, y), r10 = unproject_px(a.intr, x - 1, y - 1),
+                 r01 = unproject_px(a.intr, x, y + 1);
+        const double ux0 = r00.x, ux1 = r10.x, uy0 = r00.y, uym = r10.y, uyp = r01.y;
         const D3 ray{ux0, uy0, 1.0};
         const double denom0 = dot3(pn, ray);
         if (!(fabs(denom0) < 1e-12 || div(-1.0, denom0) <= 0.0)) {
