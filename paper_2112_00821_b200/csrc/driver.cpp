@@ -268,6 +268,8 @@ struct fmvs_ctx {
     int sweep_exact = 0;  // FMVS_SWEEP_EXACT=1: force the exact per-hypothesis sweep
     int sweep_stats = 0;  // FMVS_SWEEP_STATS=1 (2 + l: level l only): count certified-census fallbacks
     bool agg16 = true;    // packed u16 SGM aggregate where provably exact (FMVS_SGM_AGG16=0: off)
+    uint64_t agg16_min = uint64_t(48) << 20;  // ... on uniform levels above this many entries
+                                              // (FMVS_SGM_AGG16_MIN: test hook)
     // stage capture of one level (fmvs_ctx_set_capture)
     struct Capture {
         int level = -1;
@@ -687,7 +689,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         // warp, long contiguous runs) levels qualify: C4 L2 1.8x less DRAM.
         const uint64_t known_entries = have_prior ? 0 : entries_bound;
         ga.cost_max = 255 * std::max(ref, nmatch - ref);
-        ga.agg16 = ctx->agg16 && known_entries > (uint64_t(48) << 20) && k::sgm_agg16_ok(ga, ga.cost_max);
+        ga.agg16 = ctx->agg16 && known_entries > ctx->agg16_min && k::sgm_agg16_ok(ga, ga.cost_max);
         // the SGM accumulator of the level (make_accumulator, sgm.cpp:198-208)
         ctx->timed("zero", [&] { k::zero_entries(agg, rb + P.h, s, ga.agg16 != 0); });
         ++launches;
@@ -884,6 +886,8 @@ int fmvs_ctx_create(int32_t device, fmvs_ctx** out) {
             ctx->sweep_exact = std::atoi(e) != 0;
         if (const char* e = std::getenv("FMVS_SGM_AGG16"))
             ctx->agg16 = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FMVS_SGM_AGG16_MIN"))
+            ctx->agg16_min = std::strtoull(e, nullptr, 10);
         if (const char* e = std::getenv("FMVS_SWEEP_STATS"))
             ctx->sweep_stats = std::atoi(e);  // 1: every level; 2 + l: level l only
         ctx->use();

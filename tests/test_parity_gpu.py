@@ -3,6 +3,8 @@
 inputs. Integer stages must be bit-exact; the float stages are designed to be
 bit-exact as well (same FP64 expression trees, no FMA), and are asserted so.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -313,7 +315,13 @@ DIRS = [(1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1), (1, -1), (-1, 1)]
 
 def _blocking(monkeypatch, gk):
     """Lane blocking of the SGM kernel: 'GxK' (G lanes per line, K hypotheses
-    per lane and pass) or '0' (one line per warp)."""
+    per lane and pass), '0' (one line per warp) or 'default' (the library's
+    choice: G=4 x K=3 line kernel with 10-bit packed step records for the
+    default range policy)."""
+    if gk == "default":
+        monkeypatch.delenv("FMVS_SGM_G", raising=False)
+        monkeypatch.delenv("FMVS_SGM_K", raising=False)
+        return
     g, _, k = gk.partition("x")
     monkeypatch.setenv("FMVS_SGM_G", g)
     monkeypatch.setenv("FMVS_SGM_K", k or "1")
@@ -487,6 +495,9 @@ def test_tail_maps_bitexact(b200, oracle, rng):
 
 
 # ---------------------------------------------------------- end to end ----
+PKG = __import__("paper_2112_00821_b200")
+from conftest import ROOT  # noqa: E402
+
 E2E = [
     # (name, scene kwargs, config kwargs)
     ("c4_fronto_ncc_pi", dict(kind="fronto", w=160, h=120, focal=160.0, depth=10.0, step=0.5, texture=0.35),
@@ -528,10 +539,12 @@ E2E = [
 ]
 
 
-@pytest.mark.parametrize("group,arena", [("4x4", None), ("8x2", None), ("4x4", "1000")])
+@pytest.mark.parametrize("group,arena", [("default", None), ("4x4", None), ("8x2", None), ("4x4", "1000")])
 @pytest.mark.parametrize("name,scene,cfg", E2E, ids=[e[0] for e in E2E])
 def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg, group, arena, monkeypatch):
-    """arena="1000": per-level compact cost-volume arenas (the 4K path)."""
+    """arena="1000": per-level compact cost-volume arenas (the 4K path);
+    group "4x4": K = 4 with u16 costs in 48-byte SGM records, "8x2": the
+    general SGM kernel, "default": the library's own blocking."""
     _blocking(monkeypatch, group)
     if arena:
         monkeypatch.setenv("FMVS_ARENA_ENTRIES", arena)
@@ -545,6 +558,32 @@ def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg, group, arena, 
     assert_same(a.normals, b.normals, "normals")
     assert_same(a.confidence, b.confidence, "confidence")
     assert (b.depth > 0).mean() > 0.5
+
+
+@pytest.mark.parametrize("name", ["dense_216_planes", "c4_fronto_ncc_pi", "census_sn_3lvl", "c5_slanted_pg"])
+def test_estimate_bundle_packed_aggregate(oracle, name, monkeypatch):
+    """The packed u16 SGM aggregate (two entries per 32-bit RED word), which
+    the library uses on uniform levels too large for L2 (C3, C4), forced on
+    small uniform levels: results bit-identical."""
+    monkeypatch.setenv("FMVS_SGM_AGG16_MIN", "0")
+    # a context of its own, created with the hook set (not the shared one)
+    b200 = PKG.Backend(os.path.join(ROOT, "paper_2112_00821_b200", "_lib", "libfmvs.so"), "fmvs_", 0)
+    try:
+        _, scene, cfg = next(e for e in E2E if e[0] == name)
+        scene = dict(scene)
+        kind = scene.pop("kind")
+        bundle, _, _ = render(oracle, kind, **scene)
+        c = config(**cfg)
+        a = b200.estimate_bundle(bundle, c)
+        b = oracle.estimate_bundle(bundle, c)
+        assert_same(a.depth, b.depth, "depth")
+        assert_same(a.normals, b.normals, "normals")
+        assert_same(a.confidence, b.confidence, "confidence")
+        cap = b200.estimate_bundle_captured(bundle, c, level=c.pyramid_levels - 1)
+        ref = oracle.estimate_bundle_captured(bundle, c, level=c.pyramid_levels - 1)
+        assert_same(cap["aggregate"], ref["aggregate"], "coarsest-level aggregate")
+    finally:
+        b200.close()
 
 
 def test_estimate_bundle_deterministic(b200, oracle):
