@@ -640,3 +640,43 @@ def test_estimate_bundle_shapes(b200, oracle, case):
     assert_same(a.depth, b.depth, "depth")
     assert_same(a.normals, b.normals, "normals")
     assert_same(a.confidence, b.confidence, "confidence")
+
+
+def test_contexts_on_concurrent_host_threads(oracle):
+    """One context per host thread, bundles of different configurations
+    (level sizes, plane counts, SGM variants, census / NCC) launched
+    concurrently: every result bit-identical to the oracle's. Guards the
+    per-kernel launch attributes that concurrent contexts share."""
+    import threading
+    cases = [E2E[i] for i in (0, 1, 2, 6, 8)]
+    inputs = []
+    for name, scene, cfg in cases:
+        scene = dict(scene)
+        kind = scene.pop("kind")
+        bundle, _, _ = render(oracle, kind, **scene)
+        c = config(**cfg)
+        inputs.append((name, bundle, c, oracle.estimate_bundle(bundle, c)))
+    path = os.path.join(ROOT, "paper_2112_00821_b200", "_lib", "libfmvs.so")
+    errors = []
+
+    def worker(k):
+        b = PKG.Backend(path, "fmvs_", 0)
+        try:
+            for rep in range(3):
+                for j in range(len(inputs)):
+                    name, bundle, c, want = inputs[(j + k) % len(inputs)]
+                    got = b.estimate_bundle(bundle, c)
+                    if not (np.array_equal(got.depth, want.depth) and np.array_equal(got.normals, want.normals)
+                            and np.array_equal(got.confidence, want.confidence)):
+                        errors.append(f"thread {k} rep {rep}: {name} differs")
+        except Exception as e:  # reported below
+            errors.append(f"thread {k}: {type(e).__name__}: {e}")
+        finally:
+            b.close()
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
