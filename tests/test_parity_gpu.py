@@ -327,7 +327,7 @@ def _blocking(monkeypatch, gk):
     monkeypatch.setenv("FMVS_SGM_K", k or "1")
 
 
-@pytest.mark.parametrize("group", ["0", "4x4", "8x2", "8x4", "32x1", "32x4"])
+@pytest.mark.parametrize("group", ["0", "4x3", "4x4", "8x2", "8x4", "32x1", "32x4"])
 @pytest.mark.parametrize("adaptive", [False, True])
 def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive, group, monkeypatch):
     _blocking(monkeypatch, group)
@@ -345,7 +345,7 @@ def test_aggregate_single_paths_bitexact(b200, oracle, rng, adaptive, group, mon
 STEPS = [(2, 1), (-1, 3), (3, 0), (0, -2), (-2, -2), (4, -3), (20, 0), (0, 0), (1, 0), (-1, 1)]
 
 
-@pytest.mark.parametrize("group", ["0", "4x4", "32x4"])
+@pytest.mark.parametrize("group", ["0", "4x3", "4x4", "32x4"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.PathGradient])
 def test_aggregate_single_path_any_step(b200, oracle, rng, variant, group, monkeypatch):
     """aggregate_single_path walks any integer step (sgm.cpp:210-229): lines
@@ -376,7 +376,7 @@ def test_aggregate_single_path_sn_noncanonical(b200, rng):
         b200.aggregate_single_path(vol, img, SgmConfig(SgmVariant.SurfaceNormal), intr, 2, 1, pn, pd)
 
 
-@pytest.mark.parametrize("group", ["0", "4x4", "8x2", "32x4"])
+@pytest.mark.parametrize("group", ["0", "4x3", "4x4", "8x2", "32x4"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.SurfaceNormal, SgmVariant.PathGradient])
 @pytest.mark.parametrize("paths", [8, 4])
 def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths, group, monkeypatch):
@@ -400,7 +400,7 @@ def test_aggregate_variants_bitexact(b200, oracle, rng, variant, paths, group, m
     assert_same(b200.wta(a), oracle.wta(b), "wta")
 
 
-@pytest.mark.parametrize("group", ["4x4", "8x4", "32x1", "32x4", "32x8"])
+@pytest.mark.parametrize("group", ["4x3", "4x4", "8x4", "32x1", "32x4", "32x8"])
 @pytest.mark.parametrize("variant", [SgmVariant.Plane, SgmVariant.PathGradient])
 def test_aggregate_dense_wide(b200, oracle, rng, group, variant, monkeypatch):
     """Dense coarsest-level shape: >32 hypotheses per pixel (multi-pass lanes,
