@@ -775,10 +775,10 @@ __device__ __forceinline__ float2 census_sample(uint32_t q, float ax, float ay, 
     // FP32 bilinear rounding: the tap differences are exact, top / bot / f
     // each round once (<= 2^-17 below 256) and bot - top once, carrying the
     // errors of top and bot: |f - f_exact| <= 5 * 2^-17 < 4e-5 (the
-    // reference's FP64 bilinear adds < 1e-13). A flat cell away from its edges
-    // (gx = gy = 0: four equal taps, the reference's sample provably in this
-    // cell) is exact in both: zero bound.
-    const float e = fmaf(gx, dx, fmaf(gy, dy, gx + gy > 0.0f ? 4.0e-5f : 0.0f));
+    // reference's FP64 bilinear adds < 1e-13). No zero bound even for a flat
+    // cell: the reference's (1 - a) * I + a * I is not always exactly I in
+    // FP64 (a with bits below 2^-52, i.e. coordinates below 1).
+    const float e = fmaf(gx, dx, fmaf(gy, dy, 4.0e-5f));
     return make_float2(__fsub_rd(f, e), __fadd_ru(f, e));
 }
 
