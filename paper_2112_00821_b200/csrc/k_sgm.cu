@@ -302,6 +302,27 @@ __device__ __forceinline__ int nearest_index_from(const double* __restrict__ d, 
     return i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
 }
 
+// PlaneStack::fractional_index (geometry.cpp:75-93) with the bracket found by
+// a local search from `hint` (the neighbours' planes lie near the anchor's):
+// the bracket d[lo] >= delta > d[lo + 1] of a strictly decreasing stack is
+// unique, so the result equals the bisection's.
+__device__ __forceinline__ double fractional_index_from(const double* __restrict__ d, int n, double delta,
+                                                        int hint) {
+    using namespace dev;
+    if (n <= 1)
+        return 0.0;
+    if (delta >= d[0])
+        return div(-sub(delta, d[0]), sub(d[0], d[1]));
+    if (delta <= d[n - 1])
+        return add(double(n - 1), div(sub(d[n - 1], delta), sub(d[n - 2], d[n - 1])));
+    int lo = min(max(hint, 0), n - 2);
+    while (!(d[lo] >= delta))
+        --lo;
+    while (d[lo + 1] >= delta)
+        ++lo;
+    return add(double(lo), div(sub(d[lo], delta), sub(d[lo], d[lo + 1])));
+}
+
 // Minimum over the G-lane group of the calling lane (G a power of two): a
 // full-warp REDUX for G = 32, an xor butterfly otherwise (a group-masked
 // REDUX with per-group masks serialises into one pass per group).
@@ -1178,7 +1199,7 @@ __global__ void normal_offsets_kernel(OffsetArgs a) {
                 const double delta_q = -dot3(pn, scale3(t, ray_q));
                 if (delta_q <= 0.0)
                     continue;
-                double df = sub(dev::fractional_index(a.planes, a.nplanes, delta_q), double(i0));
+                double df = sub(fractional_index_from(a.planes, a.nplanes, delta_q, i0), double(i0));
                 df = df < -32000.0 ? -32000.0 : (32000.0 < df ? 32000.0 : df);
                 o[c] = static_cast<short>(lround(df));
             }
