@@ -14,7 +14,7 @@ case $WL in
   c1)         SW=sweep_census_tiled; SKIP=2 ;;
 esac
 SG=sgm_line_kernel
-[ $WL = c2pg ] && SG=sgm_lanes_kernel
+
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $OUT/launches.csv $B > $OUT/ncu_launch.log 2>&1; echo launches rc=$?
 for st in sweep_l0:$SW sgm_l0:$SG; do
