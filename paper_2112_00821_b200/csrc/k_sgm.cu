@@ -940,7 +940,9 @@ __device__ __forceinline__ void line_steps(const SgmArgs& a, const LineCtx& lc, 
             dev::D3 ray{0.0, 0.0, 1.0};
             double denom = 0.0;
             if constexpr (PG) {
-                ray = dev::unproject_px(a.intr, px, py);
+                // the divisions, not the table: a table load here sits on
+                // the step's dependency chain (measured slower)
+                ray = dev::unproject(a.intr, double(px), double(py));
                 denom = dev::dot3(dev::D3{a.nx, a.ny, a.nz}, ray);
             }
             if (c > 0) {
