@@ -577,6 +577,7 @@ struct ViewConst {
 struct TileParams64 {
     double ax, bx, cx, ay, by, cy, az, bz, cz;
     float dx, dy;
+    float eb;  // tile-uniform sample bound, or < 0: per-sample bounds
     int xa, ya;
     int exact;
 };
@@ -642,6 +643,15 @@ __device__ TileParams64 make_tile_params64(const double* __restrict__ hp, int u0
     }
     tp.dx = __double2float_ru(dx);
     tp.dy = __double2float_ru(dy);
+    // The bilinear interpolant of byte images is 255-Lipschitz along each
+    // axis, across cell edges and clamped borders included, so 255*(dx + dy)
+    // bounds the effect of the coordinate error on every sample of the tile;
+    // + the float cast of the cell fraction (<= 2^-25 per axis) and the FP32
+    // bilinear arithmetic (< 4e-5, see ncc_sample). When the coordinate term
+    // is negligible (the usual ~1e-10 px) this tile-wide bound replaces the
+    // per-sample ones.
+    const float lip = 255.0f * (tp.dx + tp.dy);
+    tp.eb = lip < 1.0e-5f ? (lip + 255.0f * 6.0e-8f + 4.0e-5f) * 1.0001f : -1.0f;
     tp.xa = static_cast<int>(xa);
     tp.ya = static_cast<int>(ya);
     tp.exact = tile_interior(H, U, V, DU, DV, double(tp.dx), double(tp.dy), vw, vh) ? kTileInterior : 0;
@@ -668,11 +678,15 @@ __device__ __forceinline__ void tile_coords64(const TileParams64& tp, double du,
 // cell quad q at (ax, ay); the bound is the cell's Lipschitz constant times
 // the coordinate error (255 within the error of a cell edge) plus the FP32
 // bilinear rounding.
+// BOUND false: the value only (tiles with a uniform bound, TileParams64::eb).
+template <bool BOUND>
 __device__ __forceinline__ float2 ncc_sample(uint32_t q, float ax, float ay, float dx, float dy) {
     const float i00 = byte_f<0>(q), i10 = byte_f<1>(q), i01 = byte_f<2>(q), i11 = byte_f<3>(q);
     const float top = fmaf(ax, i10 - i00, i00);
     const float bot = fmaf(ax, i11 - i01, i01);
     const float f = fmaf(ay, bot - top, top);
+    if (!BOUND)
+        return make_float2(f, 0.0f);
     // the float cast of (t - floor t) adds 2^-24 to the coordinate error; a
     // negative dx / dy marks an axis certainly clamped at the view edge (the
     // sample does not depend on it: no error along it)
@@ -687,6 +701,7 @@ __device__ __forceinline__ float2 ncc_sample(uint32_t q, float ax, float ay, flo
 
 // Sample of the tile at (du, dv): FP64 residual coordinates, FP32 bilinear;
 // returns (value, bound) like the FP32-coordinate path.
+template <bool BOUND>
 __device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const ViewConst& vc,
                                                 double du, double dv, uint8_t* in_flag) {
     double tx, ty;
@@ -733,10 +748,11 @@ __device__ __forceinline__ float2 tile_sample64(const TileParams64& tp, const Vi
         if (double(tp.ya) + ty - ey >= double(vc.h - 1))
             ddy = -1.0f;
     }
-    return ncc_sample(__ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0), ax, ay, ddx, ddy);
+    return ncc_sample<BOUND>(__ldg(vc.quad + static_cast<uint32_t>(Y0 * vc.w + X0)), ax, ay, ddx, ddy);
 }
 
 // tile_sample64 of a kTileInterior tile: no clamping, no inside flag.
+template <bool BOUND>
 __device__ __forceinline__ float2 tile_sample64_interior(const TileParams64& tp, const ViewConst& vc,
                                                          double du, double dv) {
     double tx, ty;
@@ -745,7 +761,37 @@ __device__ __forceinline__ float2 tile_sample64_interior(const TileParams64& tp,
     const double fx = floor_small(tx, &ix), fy = floor_small(ty, &iy);
     const int X0 = tp.xa + ix, Y0 = tp.ya + iy;
     const float ax = __double2float_rn(tx - fx), ay = __double2float_rn(ty - fy);
-    return ncc_sample(__ldg(vc.quad + static_cast<size_t>(Y0) * vc.w + X0), ax, ay, tp.dx, tp.dy);
+    return ncc_sample<BOUND>(__ldg(vc.quad + static_cast<uint32_t>(Y0 * vc.w + X0)), ax, ay, tp.dx, tp.dy);
+}
+
+// One view's part of the NCC tile build (this thread's samples r, r + KTPV,
+// ...): quantised samples F = rint(f * 2^16) into t, inside flags into fl
+// (general tiles); returns the thread's max sample bound.
+template <bool BOUND, int SW, int SN, int KTPV>
+__device__ __forceinline__ float build_ncc_tile(const TileParams64& tp, const ViewConst& vc, int* t,
+                                                uint8_t* fl, int r) {
+    int dv = r / SW, du = r - dv * SW;
+    float emax = BOUND ? 0.0f : tp.eb;
+    for (; r < SN; r += KTPV) {
+        float2 v;
+        if (tp.exact == kTileInterior) {
+            v = tile_sample64_interior<BOUND>(tp, vc, double(du), double(dv));
+        } else {
+            uint8_t f = 2;
+            v = tile_sample64<BOUND>(tp, vc, double(du), double(dv), &f);
+            fl[r] = f;
+        }
+        t[r] = __float2int_rn(v.x * 65536.0f);  // exact scaling, |F/2^16 - f| <= 2^-17
+        if (BOUND)
+            emax = fmaxf(emax, v.y);
+        du += KTPV % SW;
+        dv += KTPV / SW;
+        if (du >= SW) {
+            du -= SW;
+            ++dv;
+        }
+    }
+    return emax;
 }
 
 // Exact FP64 census cost of one view (views whose tile certification is
@@ -1234,6 +1280,15 @@ struct NccSums {
 };
 
 // Certified NCC cost of one window from its exact sums, or -1.
+//   var_q = (n SF^2 - (SF)^2) / (n 2^32), cov_q = (n SrF - Sr SF) / (n 2^16)
+// are the quantised window's exact centred sums (FP32-rounded: < 2e-7 rel.).
+// The reference's sqrt(var_b) lies within D = e_norm + 1e-6 sv of
+// sv = sqrt(var_q) and its covariance within dc of cov_q, so its ncc lies
+// within  dn = (dc + |n| rho D) / (rho (sv - D))  of n = cov_q / (rho sv);
+// with D <= sv/128, 1/(sv - D) <= 1.01/sv. The cost 255 min(1 - ncc, 1)
+// clamped to [0, 255] is monotone and 255-Lipschitz in ncc, so if both ends
+// of its interval round (half up) to the same integer that is the
+// reference's cost.
 template <int NS>
 __device__ __forceinline__ int ncc_certify(const NccSums& S, int rsum, float rho, float e_norm) {
     // n^2 * var_q * 2^32 and n * cov_q * 2^16, exact
@@ -1244,32 +1299,24 @@ __device__ __forceinline__ int ncc_certify(const NccSums& S, int rsum, float rho
     constexpr float inv_nv = 1.0f / (float(NS) * 4294967296.0f);  // relative error < 1e-7
     constexpr float inv_nc = 1.0f / (float(NS) * 65536.0f);
     const float var_q = float(nv) * inv_nv;
-    if (!(var_q >= 1.0f))
-        return -1;  // near-flat window: the reference's FP64 rounding is not negligible
-    const float sv = var_q * rsqrtf(var_q);         // sqrt(var_q), rel. error < 4e-7
-    const float s_lo = sv * 0.999999f - e_norm;    // bounds of sqrt(var_b)
-    const float s_hi = sv * 1.000001f + e_norm;
-    if (!(s_lo > 0.5f))
+    const float sv = var_q * rsqrtf(var_q);  // sqrt(var_q), rel. error < 4e-7 (NaN if var_q <= 0)
+    const float D = fmaf(sv, 1.0e-6f, e_norm);
+    // var_q >= 1: near-flat windows, where the reference's FP64 rounding is
+    // not negligible, are left to the exact walk
+    if (!(var_q >= 1.0f) || !(128.0f * D <= sv))
         return -1;
     const float c_q = float(nc) * inv_nc;
-    const float dc = rho * e_norm + 1e-6f * fabsf(c_q) + 1e-6f;
-    const float c_lo = c_q - dc, c_hi = c_q + dc;
-    float r_lo, r_hi;  // 1/(rho s): MUFU reciprocal, rel. error < 2^-22 (in the slack)
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r_lo) : "f"(rho * s_lo));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r_hi) : "f"(rho * s_hi));
-    float n_hi = c_hi * (c_hi >= 0.0f ? r_lo : r_hi);
-    float n_lo = c_lo * (c_lo >= 0.0f ? r_hi : r_lo);
-    // FP32 bound arithmetic (conversions, products, MUFU rsqrt / rcp; < 1e-6 rel.)
-    // and the reference's FP64 rounding (< 1e-7 abs. with var >= 1)
-    const float slack = 2e-6f * (fabsf(n_hi) + fabsf(n_lo)) + 1e-6f;
-    n_hi += slack;
-    n_lo -= slack;
-    float t_lo = 255.0f * fminf(1.0f - n_hi, 1.0f);
-    float t_hi = 255.0f * fminf(1.0f - n_lo, 1.0f);
-    t_lo = fminf(fmaxf(t_lo, 0.0f), 255.0f) - 1e-4f;
-    t_hi = fminf(fmaxf(t_hi, 0.0f), 255.0f) + 1e-4f;
-    const int k_lo = static_cast<int>(floorf(fmaxf(t_lo, 0.0f) + 0.5f));
-    const int k_hi = static_cast<int>(floorf(fminf(t_hi, 255.0f) + 0.5f));
+    const float dc = fmaf(rho, e_norm, fmaf(fabsf(c_q), 1.0e-6f, 1.0e-6f));
+    float inv;  // 1/(rho sv): MUFU reciprocal, rel. error < 2^-22 (in the slack)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(rho * sv));
+    const float n = c_q * inv;
+    // FP32 bound arithmetic (conversions, products, MUFU rsqrt / rcp; < 1e-6
+    // rel.) and the reference's FP64 rounding (< 1e-7 abs. with var >= 1)
+    const float dn = fmaf(fmaf(fabsf(n) * rho, D, dc), inv * 1.01f, fmaf(fabsf(n), 4.0e-6f, 2.0e-6f));
+    const float t = fminf(fmaxf(255.0f * fminf(1.0f - n, 1.0f), 0.0f), 255.0f) + 0.5f;
+    const float w = fmaf(255.0f, dn, 2.0e-4f);
+    const int k_lo = static_cast<int>(floorf(t - w));
+    const int k_hi = static_cast<int>(floorf(t + w));
     return k_lo == k_hi ? k_lo : -1;
 }
 
@@ -1419,29 +1466,11 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             const ViewConst vc = s_vc[m];
             int* t = s_F + m * SN;
             uint8_t* fl = s_in + m * SN;
-            int r = threadIdx.x - m * kTPV;
-            int dv = r / SW, du = r - dv * SW;
+            const int r = threadIdx.x - m * kTPV;
             float emax = 0.0f;
-            if (tp.exact != kTileExact) {
-                for (; r < SN; r += kTPV) {
-                    float2 v;
-                    if (tp.exact == kTileInterior) {
-                        v = tile_sample64_interior(tp, vc, double(du), double(dv));
-                    } else {
-                        uint8_t f = 2;
-                        v = tile_sample64(tp, vc, double(du), double(dv), &f);
-                        fl[r] = f;
-                    }
-                    t[r] = __float2int_rn(v.x * 65536.0f);  // exact scaling, |F/2^16 - f| <= 2^-17
-                    emax = fmaxf(emax, v.y);
-                    du += kTPV % SW;
-                    dv += kTPV / SW;
-                    if (du >= SW) {
-                        du -= SW;
-                        ++dv;
-                    }
-                }
-            }
+            if (tp.exact != kTileExact)
+                emax = tp.eb > 0.0f ? build_ncc_tile<false, SW, SN, kTPV>(tp, vc, t, fl, r)
+                                    : build_ncc_tile<true, SW, SN, kTPV>(tp, vc, t, fl, r);
             // tile maximum of the bounds (positive floats: their bit patterns
             // order like them); lanes of one warp may serve different views
             const unsigned grp = __match_any_sync(__activemask(), m);
@@ -1508,40 +1537,47 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
         __syncthreads();  // C
         if (threadIdx.x < NM)
             s_emax[threadIdx.x] = 0u;  // next written after this plane's barrier B
-        // ---- pass 1: certified costs, or NS exact work items per view
-        int cost[NM];
+        // ---- pass 1: per-side sums of the certified costs; NS exact work
+        // items per undecided view (added in pass 3)
+        int sum_l = 0, sum_r = 0;
         uint32_t view_unsure = 0, view_exact = 0;
         int my_items = 0;
+        if (need) {
+            const bool flat = !(s_rho[threadIdx.x] > 0.0f);  // ref_var <= 0
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
-            cost[m] = 255;
-            if (!need)
-                continue;
-            const int tpe = s_tp[slot][m].exact;
-            if (tpe == kTileExact) {
-                view_exact |= 1u << m;
-                continue;
-            }
-            const ViewConst& vc = s_vc[m];
-            bool inside = true;
-            if (tpe != kTileInterior) {
-                const uint8_t fl = s_in[m * SN + (ty + RY) * SW + tx + RX];
-                inside = fl == 2 ? exact_inside(vc.homs + static_cast<size_t>(p) * 9, vc.w, vc.h, xd, yd)
-                                 : fl == 1;
-            }
-            if (!inside || ref_var <= 0.0)
-                continue;  // 255 (matching.cpp:224-232, 262-263)
-            const int c = s_cost[m * kTiledThreads + threadIdx.x];
-            if (c >= 0) {
-                cost[m] = c;
-            } else {
-                view_unsure |= 1u << m;
-                my_items += NS;
-            }
-            if (a.stats) {
-                atomicAdd(a.stats + 0, 1ull);
-                if (c < 0)
-                    atomicAdd(a.stats + 1, 1ull);
+            for (int m = 0; m < NM; ++m) {
+                int c = 255;
+                const int tpe = s_tp[slot][m].exact;
+                if (tpe == kTileExact) {
+                    view_exact |= 1u << m;
+                    c = 0;
+                } else {
+                    bool inside = true;
+                    if (tpe != kTileInterior) {
+                        const uint8_t fl = s_in[m * SN + (ty + RY) * SW + tx + RX];
+                        inside = fl == 2 ? exact_inside(s_vc[m].homs + static_cast<size_t>(p) * 9, s_vc[m].w,
+                                                        s_vc[m].h, double(x), double(y))
+                                         : fl == 1;
+                    }
+                    // else 255 (matching.cpp:224-232, 262-263)
+                    if (inside && !flat) {
+                        c = s_cost[m * kTiledThreads + threadIdx.x];
+                        if (c < 0) {
+                            view_unsure |= 1u << m;
+                            my_items += NS;
+                        }
+                        if (a.stats) {
+                            atomicAdd(a.stats + 0, 1ull);
+                            if (c < 0)
+                                atomicAdd(a.stats + 1, 1ull);
+                        }
+                        c = max(c, 0);
+                    }
+                }
+                if (m < a.nleft)
+                    sum_l += c;
+                else
+                    sum_r += c;
             }
         }
         // CTA-wide list of the exact samples (slots from a shared-memory
@@ -1596,16 +1632,20 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             s_count = 0;  // next plane allocates after its barrier C
         // ---- pass 3: costs of undecided views from their exact samples, per-side sums
         if (need) {
-            int sum_l = 0, sum_r = 0, k = off;
-#pragma unroll
-            for (int m = 0; m < NM; ++m) {
+            int k = off;
+            uint32_t todo = view_exact | view_unsure;
+            while (todo) {
+                const int m = __ffs(todo) - 1;
+                todo &= todo - 1;
                 const ViewConst& vc = s_vc[m];
                 const double* hp = vc.homs + static_cast<size_t>(p) * 9;
-                int c = cost[m];
+                const double xd = double(x), yd = double(y);
+                const double ref_mean = s_rmean[threadIdx.x], ref_var = s_rvar[threadIdx.x];
+                int c;
                 if ((view_exact >> m) & 1u) {
                     c = ncc_view_exact<WW, WH>(vc.quad, vc.w, vc.h, hp, xd, yd, s_ref + ty * SW + tx, SW,
                                                ref_mean, ref_var, a.census_lut);
-                } else if ((view_unsure >> m) & 1u) {
+                } else {
                     if (k + NS <= kNccItemCap) {
                         c = s_vcost[k / NS];  // resolved by pass 2b
                     } else {
