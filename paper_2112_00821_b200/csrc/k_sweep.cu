@@ -1237,6 +1237,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_CENSUS_MINB(WW * WH)) swee
 // ===================================================================
 
 constexpr int kNccItemCap = 2048;
+constexpr int kNccPend = 128;  // pending (pixel, plane) entries per batch
 
 // sqrt(x) for bounds: MUFU rsqrt based (relative error < 1e-6), 0 for x <= 0.
 __device__ __forceinline__ float sqrt_up(float x) { return x > 0.0f ? x * rsqrtf(x) * 1.0001f : 0.0f; }
@@ -1339,13 +1340,19 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
     __shared__ TileParams64 s_tp[kPlaneChunk][NM];
     __shared__ ViewConst s_vc[NM];
     __shared__ int s_pmin, s_pmax;
-    __shared__ int s_count;  // exact samples listed for the current plane
-    __shared__ unsigned s_emax[NM];                  // max sample bound of the tile (float bits)
+    __shared__ int s_count;  // exact samples listed for the current batch of planes
+    __shared__ int s_npend;  // pending (pixel, plane) entries of the batch
+    // max sample bound of the tile (float bits), by plane parity: reset for
+    // plane p + 1 between barriers T and C of plane p
+    __shared__ unsigned s_emax[2][NM];
     __shared__ int s_rsum[kTiledThreads];            // sum r of each pixel's window
     __shared__ float s_rho[kTiledThreads];           // sqrt(ref_var), 0 if ref_var <= 0
-    __shared__ int s_first[kTiledThreads], s_cnt[kTiledThreads];
-    __shared__ uint32_t s_items[kNccItemCap];
+    __shared__ uint32_t s_items[kNccItemCap];        // t | m << 8 | pos << 12 | slot << 19
     __shared__ double s_vals[kNccItemCap];
+    // (sum_l | sum_r << 16, t | slot << 8 | undecided views << 11 | first view index << 19)
+    __shared__ uint2 s_pend[kNccPend];
+    int* s_first = reinterpret_cast<int*>(s_vals);  // prologue only (aliases s_vals)
+    int* s_cnt = s_first + kTiledThreads;
     __shared__ int s_vcost[kNccItemCap / NS + 1];  // pass 2b results
     __shared__ double s_rmean[kTiledThreads], s_rvar[kTiledThreads];
     constexpr int kTPV = kTiledThreads / NM;  // tile-build threads per view
@@ -1377,13 +1384,15 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
         s_pmin = 0x7FFFFFFF;
         s_pmax = -1;
         s_count = 0;
+        s_npend = 0;
     }
     if (threadIdx.x < NM) {
         const int m = threadIdx.x;
         const int2 sz = a.sizes[m];
         s_vc[m] = ViewConst{a.quads[m], a.homs + static_cast<size_t>(m) * a.nplanes * 9, sz.x, sz.y,
                             m < a.nleft ? 1 : 0};
-        s_emax[m] = 0u;
+        s_emax[0][m] = 0u;
+        s_emax[1][m] = 0u;
     }
     __syncthreads();
     // reference patch mean and two-pass variance, exactly as matching.cpp:199-210
@@ -1455,9 +1464,10 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             }
             __syncthreads();
         }
-        // Five barriers per plane: tile complete (T), box costs complete (C),
-        // exact-sample list complete (I), exact samples taken (P), view costs
-        // resolved (B).
+        // Two barriers per plane: tile complete (T), box costs complete (C);
+        // at the end of each batch of kRunNcc planes: exact-sample lists
+        // complete (I), exact samples taken (P), view costs resolved (B) and,
+        // on dense levels, the staged run complete (R).
         // ---- tile build: each thread serves one view (parameters in
         // registers); quantised samples, the tile's max sample bound
         if (threadIdx.x < NM * kTPV) {
@@ -1476,9 +1486,32 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             const unsigned grp = __match_any_sync(__activemask(), m);
             const unsigned eb = __reduce_max_sync(grp, __float_as_uint(emax));
             if ((threadIdx.x & 31) == __ffs(grp) - 1)
-                atomicMax(&s_emax[m], eb);
+                atomicMax(&s_emax[p & 1][m], eb);
         }
         __syncthreads();  // T
+        if (threadIdx.x < NM)
+            s_emax[(p + 1) & 1][threadIdx.x] = 0u;
+        // per-view flags of this pixel for pass 1 (s_tp and s_in are rewritten
+        // by the next planes before pass 1 of this one may run)
+        const int bslot = (p - pmin) % kRunNcc;  // plane's slot in its batch
+        uint32_t view_in = 0, view_exact = 0;
+        if (need) {
+#pragma unroll
+            for (int m = 0; m < NM; ++m) {
+                const int tpe = s_tp[slot][m].exact;
+                if (tpe == kTileExact) {
+                    view_exact |= 1u << m;
+                } else if (tpe == kTileInterior) {
+                    view_in |= 1u << m;
+                } else {
+                    const uint8_t fl = s_in[m * SN + (ty + RY) * SW + tx + RX];
+                    if (fl == 2 ? exact_inside(s_vc[m].homs + static_cast<size_t>(p) * 9, s_vc[m].w, s_vc[m].h,
+                                               double(x), double(y))
+                                : fl == 1)
+                        view_in |= 1u << m;
+                }
+            }
+        }
         // ---- box pass: exact window sums by sliding row sums, certified cost
         // per (view, pixel) into s_cost; job = (view m, tile column bc,
         // pixel rows bh*4 .. bh*4+3)
@@ -1495,7 +1528,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
                 const int* F = s_F + m * SN;
                 // ||e|| <= sqrt(n) * (E_max + 2^-17), rounded up
                 const float e_norm =
-                    sqrtf(float(NS)) * (__uint_as_float(s_emax[m]) + 7.7e-6f) * 1.0001f;
+                    sqrtf(float(NS)) * (__uint_as_float(s_emax[p & 1][m]) + 7.7e-6f) * 1.0001f;
                 auto row_sum = [&](int row) {
                     NccSums R{0u, 0ull, 0ull};
 #pragma unroll
@@ -1535,43 +1568,33 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             }
         }
         __syncthreads();  // C
-        if (threadIdx.x < NM)
-            s_emax[threadIdx.x] = 0u;  // next written after this plane's barrier B
-        // ---- pass 1: per-side sums of the certified costs; NS exact work
-        // items per undecided view (added in pass 3)
-        int sum_l = 0, sum_r = 0;
-        uint32_t view_unsure = 0, view_exact = 0;
-        int my_items = 0;
+        // ---- pass 1: per-side sums of the certified costs. Pixels with
+        // undecided views list NS exact work items per view and a pending
+        // entry; the exact samples of a whole batch of planes (a staged run)
+        // are taken and resolved together at its end.
         if (need) {
+            int sum_l = 0, sum_r = 0, nun = 0;
+            uint32_t unsure = 0;
             const bool flat = !(s_rho[threadIdx.x] > 0.0f);  // ref_var <= 0
 #pragma unroll
             for (int m = 0; m < NM; ++m) {
-                int c = 255;
-                const int tpe = s_tp[slot][m].exact;
-                if (tpe == kTileExact) {
-                    view_exact |= 1u << m;
-                    c = 0;
-                } else {
-                    bool inside = true;
-                    if (tpe != kTileInterior) {
-                        const uint8_t fl = s_in[m * SN + (ty + RY) * SW + tx + RX];
-                        inside = fl == 2 ? exact_inside(s_vc[m].homs + static_cast<size_t>(p) * 9, s_vc[m].w,
-                                                        s_vc[m].h, double(x), double(y))
-                                         : fl == 1;
+                int c = 255;  // outside / flat reference (matching.cpp:224-232, 262-263)
+                if ((view_exact >> m) & 1u) {
+                    c = ncc_view_exact<WW, WH>(s_vc[m].quad, s_vc[m].w, s_vc[m].h,
+                                               s_vc[m].homs + static_cast<size_t>(p) * 9, double(x), double(y),
+                                               s_ref + ty * SW + tx, SW, s_rmean[threadIdx.x],
+                                               s_rvar[threadIdx.x], a.census_lut);
+                } else if (((view_in >> m) & 1u) && !flat) {
+                    c = s_cost[m * kTiledThreads + threadIdx.x];
+                    if (a.stats) {
+                        atomicAdd(a.stats + 0, 1ull);
+                        if (c < 0)
+                            atomicAdd(a.stats + 1, 1ull);
                     }
-                    // else 255 (matching.cpp:224-232, 262-263)
-                    if (inside && !flat) {
-                        c = s_cost[m * kTiledThreads + threadIdx.x];
-                        if (c < 0) {
-                            view_unsure |= 1u << m;
-                            my_items += NS;
-                        }
-                        if (a.stats) {
-                            atomicAdd(a.stats + 0, 1ull);
-                            if (c < 0)
-                                atomicAdd(a.stats + 1, 1ull);
-                        }
-                        c = max(c, 0);
+                    if (c < 0) {
+                        unsure |= 1u << m;
+                        ++nun;
+                        c = 0;
                     }
                 }
                 if (m < a.nleft)
@@ -1579,104 +1602,128 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
                 else
                     sum_r += c;
             }
-        }
-        // CTA-wide list of the exact samples (slots from a shared-memory
-        // atomic; each thread reads back exactly its own slots)
-        int off = 0;
-        if (my_items)
-            off = atomicAdd(&s_count, my_items);
-        if (my_items) {
-            int k = off;
-#pragma unroll
-            for (int m = 0; m < NM; ++m) {
-                if (!((view_unsure >> m) & 1u))
-                    continue;
-                for (int s = 0; s < NS; ++s, ++k)
-                    if (k < kNccItemCap)
-                        s_items[k] = threadIdx.x | (m << 8) | (s << 12);
-            }
-        }
-        __syncthreads();  // I
-        const int total = s_count;
-        const int nitems = min(total, kNccItemCap);
-        if (a.stats && threadIdx.x == 0)
-            atomicAdd(a.stats + 6, static_cast<unsigned long long>(total));
-        for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
-            const uint32_t item = s_items[it];
-            const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = item >> 12;
-            const ViewConst& vc = s_vc[m];
-            s_vals[it] = exact_window_sample(vc.homs + static_cast<size_t>(p) * 9, vc.quad, vc.w,
-                                             vc.h, double(x0 + t % kTW), double(y0 + t / kTW), RX,
-                                             RY, pos / WW, pos % WW);
-        }
-        __syncthreads();  // P
-        // ---- pass 2b: the reference's sums and NCC of each undecided view
-        // (matching.cpp:265-279, same order), one thread per view
-        const int nviews_u = nitems / NS;
-        for (int v = threadIdx.x; v < nviews_u; v += kTiledThreads) {
-            const int k0 = v * NS;
-            const int t = s_items[k0] & 0xFF;
-            const int ttx = t % kTW, tty = t / kTW;
-            double sb = 0.0, sbb = 0.0, sab = 0.0;
-            for (int s = 0; s < NS; ++s) {
-                const int i = s / WW, j = s - (s / WW) * WW;
-                const double val = s_vals[k0 + s];
-                sb = add(sb, val);
-                sbb = add(sbb, mul(val, val));
-                sab = add(sab, mul(double(s_ref[(tty + i) * SW + ttx + j]), val));
-            }
-            s_vcost[v] = ncc_tail<NS>(sb, sbb, sab, s_rmean[t], s_rvar[t]);
-        }
-        __syncthreads();  // B
-        if (threadIdx.x == 0)
-            s_count = 0;  // next plane allocates after its barrier C
-        // ---- pass 3: costs of undecided views from their exact samples, per-side sums
-        if (need) {
-            int k = off;
-            uint32_t todo = view_exact | view_unsure;
-            while (todo) {
-                const int m = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const ViewConst& vc = s_vc[m];
-                const double* hp = vc.homs + static_cast<size_t>(p) * 9;
-                const double xd = double(x), yd = double(y);
-                const double ref_mean = s_rmean[threadIdx.x], ref_var = s_rvar[threadIdx.x];
-                int c;
-                if ((view_exact >> m) & 1u) {
-                    c = ncc_view_exact<WW, WH>(vc.quad, vc.w, vc.h, hp, xd, yd, s_ref + ty * SW + tx, SW,
-                                               ref_mean, ref_var, a.census_lut);
+            bool done = unsure == 0;
+            if (!done) {
+                const int e = atomicAdd(&s_npend, 1);
+                const int off = e < kNccPend ? atomicAdd(&s_count, nun * NS) : kNccItemCap;
+                const uint32_t tag = threadIdx.x | (bslot << 19);
+                if (off + nun * NS <= kNccItemCap) {
+                    int k = off;
+                    for (uint32_t u = unsure; u; u &= u - 1) {
+                        const uint32_t mt = tag | ((__ffs(u) - 1) << 8);
+                        for (int q = 0; q < NS; ++q)
+                            s_items[k++] = mt | (q << 12);
+                    }
+                    s_pend[e] = make_uint2(static_cast<uint32_t>(sum_l) | (static_cast<uint32_t>(sum_r) << 16),
+                                           threadIdx.x | (bslot << 8) | (unsure << 11) |
+                                               (static_cast<uint32_t>(off / NS) << 19));
                 } else {
-                    if (k + NS <= kNccItemCap) {
-                        c = s_vcost[k / NS];  // resolved by pass 2b
-                    } else {
-                        // list overflow (pathological inputs): the owner walks it
+                    // list overflow (pathological inputs): the owner walks its
+                    // views; reserved slots get harmless dummy items
+                    if (e < kNccPend) {
+                        for (int k = off; k < min(off + nun * NS, kNccItemCap); ++k)
+                            s_items[k] = tag | ((__ffs(unsure) - 1) << 8);
+                        s_pend[e] = make_uint2(0u, 0xFFFFFFFFu);
+                    }
+                    for (uint32_t u = unsure; u; u &= u - 1) {
+                        const int m = __ffs(u) - 1;
+                        const ViewConst& vc = s_vc[m];
+                        const double* hp = vc.homs + static_cast<size_t>(p) * 9;
                         double sb = 0.0, sbb = 0.0, sab = 0.0;
-                        for (int s = 0; s < NS; ++s) {
-                            const int i = s / WW, j = s - (s / WW) * WW;
-                            const double v = exact_window_sample(hp, vc.quad, vc.w, vc.h, xd, yd, RX,
-                                                                 RY, i, j);
+                        for (int q = 0; q < NS; ++q) {
+                            const int i = q / WW, j = q - (q / WW) * WW;
+                            const double v = exact_window_sample(hp, vc.quad, vc.w, vc.h, double(x), double(y),
+                                                                 RX, RY, i, j);
                             sb = add(sb, v);
                             sbb = add(sbb, mul(v, v));
                             sab = add(sab, mul(double(s_ref[(ty + i) * SW + tx + j]), v));
                         }
-                        c = ncc_tail<NS>(sb, sbb, sab, ref_mean, ref_var);
+                        const int c = ncc_tail<NS>(sb, sbb, sab, s_rmean[threadIdx.x], s_rvar[threadIdx.x]);
+                        if (m < a.nleft)
+                            sum_l += c;
+                        else
+                            sum_r += c;
                     }
-                    k += NS;
+                    done = true;
                 }
-                if (m < a.nleft)
-                    sum_l += c;
-                else
-                    sum_r += c;
             }
-            const uint16_t v = static_cast<uint16_t>(min(sum_l, sum_r));
-            if (a.plane_slicing)
-                s_run[threadIdx.x * (kRunNcc + 2) + (p - pmin) % kRunNcc] = v;
-            else
-                a.costs[base + static_cast<uint64_t>(p - first)] = v;
+            if (done) {
+                const uint16_t v = static_cast<uint16_t>(min(sum_l, sum_r));
+                if (a.plane_slicing)
+                    s_run[threadIdx.x * (kRunNcc + 2) + bslot] = v;
+                else
+                    a.costs[base + static_cast<uint64_t>(p - first)] = v;
+            }
         }
-        if (a.plane_slicing && ((p - pmin) % kRunNcc == kRunNcc - 1 || p == pmax))
-            flush_run<kRunNcc>(a.costs, s_run + threadIdx.x * (kRunNcc + 2), p - (p - pmin) % kRunNcc, p, first,
-                               count, base);
+        if (bslot == kRunNcc - 1 || p == pmax) {
+            const int pb = p - bslot;  // first plane of the batch
+            __syncthreads();  // I: item and pending lists complete
+            const int total = s_count;
+            const int npend = min(s_npend, kNccPend);
+            const int nitems = min(total, kNccItemCap);
+            if (a.stats && threadIdx.x == 0)
+                atomicAdd(a.stats + 6, static_cast<unsigned long long>(total));
+            // ---- pass 2: the exact samples, one per thread
+            for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
+                const uint32_t item = s_items[it];
+                const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = (item >> 12) & 0x7F;
+                const ViewConst& vc = s_vc[m];
+                s_vals[it] = exact_window_sample(vc.homs + static_cast<size_t>(pb + (item >> 19)) * 9, vc.quad,
+                                                 vc.w, vc.h, double(x0 + t % kTW), double(y0 + t / kTW), RX, RY,
+                                                 pos / WW, pos % WW);
+            }
+            __syncthreads();  // P
+            if (threadIdx.x == 0) {
+                s_count = 0;  // read by every thread before P; next appended after C
+                s_npend = 0;
+            }
+            // ---- pass 2b: the reference's sums and NCC of each undecided view
+            // (matching.cpp:265-279, same order), one thread per view
+            const int nviews_u = nitems / NS;
+            for (int v = threadIdx.x; v < nviews_u; v += kTiledThreads) {
+                const int k0 = v * NS;
+                const int t = s_items[k0] & 0xFF;
+                const int ttx = t % kTW, tty = t / kTW;
+                double sb = 0.0, sbb = 0.0, sab = 0.0;
+                for (int q = 0; q < NS; ++q) {
+                    const int i = q / WW, j = q - (q / WW) * WW;
+                    const double val = s_vals[k0 + q];
+                    sb = add(sb, val);
+                    sbb = add(sbb, mul(val, val));
+                    sab = add(sab, mul(double(s_ref[(tty + i) * SW + ttx + j]), val));
+                }
+                s_vcost[v] = ncc_tail<NS>(sb, sbb, sab, s_rmean[t], s_rvar[t]);
+            }
+            __syncthreads();  // B
+            // ---- pass 3: pending entries -> final costs
+            for (int e = threadIdx.x; e < npend; e += kTiledThreads) {
+                const uint2 pe = s_pend[e];
+                if (pe.y == 0xFFFFFFFFu)
+                    continue;
+                const int t = pe.y & 0xFF, sl = (pe.y >> 8) & 7;
+                int vi = static_cast<int>(pe.y >> 19);
+                int sum_l = static_cast<int>(pe.x & 0xFFFFu), sum_r = static_cast<int>(pe.x >> 16);
+                for (uint32_t u = (pe.y >> 11) & 0xFFu; u; u &= u - 1) {
+                    const int c = s_vcost[vi++];
+                    if (__ffs(u) - 1 < a.nleft)
+                        sum_l += c;
+                    else
+                        sum_r += c;
+                }
+                const uint16_t v = static_cast<uint16_t>(min(sum_l, sum_r));
+                if (a.plane_slicing) {
+                    s_run[t * (kRunNcc + 2) + sl] = v;
+                } else {
+                    const int xt = x0 + t % kTW, yt = y0 + t / kTW;
+                    const VolMeta mt = a.meta[static_cast<size_t>(yt) * a.w + xt];
+                    a.costs[a.row_base[yt] + mt.rel + static_cast<uint64_t>(pb + sl - meta_first(mt.fc))] = v;
+                }
+            }
+            if (a.plane_slicing) {
+                __syncthreads();  // R: the run is complete
+                flush_run<kRunNcc>(a.costs, s_run + threadIdx.x * (kRunNcc + 2), pb, p, first, count, base);
+            }
+        }
     }
 }
 
