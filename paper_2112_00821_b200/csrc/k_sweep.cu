@@ -1465,9 +1465,10 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             __syncthreads();
         }
         // Two barriers per plane: tile complete (T), box costs complete (C);
-        // at the end of each batch of kRunNcc planes: exact-sample lists
-        // complete (I), exact samples taken (P), view costs resolved (B) and,
-        // on dense levels, the staged run complete (R).
+        // at the end of each run of kRunNcc planes (or earlier when the lists
+        // fill up): exact-sample lists complete (I), exact samples taken (P),
+        // view costs resolved (B) and, on dense levels, the staged run
+        // complete (R).
         // ---- tile build: each thread serves one view (parameters in
         // registers); quantised samples, the tile's max sample bound
         if (threadIdx.x < NM * kTPV) {
@@ -1493,7 +1494,10 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             s_emax[(p + 1) & 1][threadIdx.x] = 0u;
         // per-view flags of this pixel for pass 1 (s_tp and s_in are rewritten
         // by the next planes before pass 1 of this one may run)
-        const int bslot = (p - pmin) % kRunNcc;  // plane's slot in its batch
+        const int bslot = (p - pmin) % kRunNcc;  // plane's slot in its run
+        // lists already half full (appended by planes < p, reset before T):
+        // resolve at the end of this plane instead of the run's end
+        const bool early = s_count >= kNccItemCap / 2 || s_npend >= kNccPend / 2;
         uint32_t view_in = 0, view_exact = 0;
         if (need) {
 #pragma unroll
@@ -1655,8 +1659,9 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
                     a.costs[base + static_cast<uint64_t>(p - first)] = v;
             }
         }
-        if (bslot == kRunNcc - 1 || p == pmax) {
-            const int pb = p - bslot;  // first plane of the batch
+        const bool run_end = bslot == kRunNcc - 1 || p == pmax;
+        if (run_end || early) {
+            const int pb = p - bslot;  // first plane of the run
             __syncthreads();  // I: item and pending lists complete
             const int total = s_count;
             const int npend = min(s_npend, kNccPend);
@@ -1719,7 +1724,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
                     a.costs[a.row_base[yt] + mt.rel + static_cast<uint64_t>(pb + sl - meta_first(mt.fc))] = v;
                 }
             }
-            if (a.plane_slicing) {
+            if (a.plane_slicing && run_end) {
                 __syncthreads();  // R: the run is complete
                 flush_run<kRunNcc>(a.costs, s_run + threadIdx.x * (kRunNcc + 2), pb, p, first, count, base);
             }
