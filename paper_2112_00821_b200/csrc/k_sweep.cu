@@ -1321,18 +1321,25 @@ __device__ __forceinline__ int ncc_certify(const NccSums& S, int rsum, float rho
     return k_lo == k_hi ? k_lo : -1;
 }
 
-template <int WW, int WH, int NM>
-__global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) sweep_ncc_tiled(SweepArgs a) {
+// TH: tile height (8: 256 threads; 16: 512 threads, fewer halo samples per
+// pixel: 36 x 20 / 512 = 1.41 instead of 36 x 12 / 256 = 1.69)
+template <int WW, int WH, int NM, int TH>
+__global__ void __launch_bounds__(32 * TH, TH == 16 ? 2 : FMVS_NCC_MINB_OF(WW * WH, NM))
+    sweep_ncc_tiled(SweepArgs a) {
     using namespace dev;
+    constexpr int NT = kTW * TH;           // threads = tile pixels
+    constexpr int TB = NT > 256 ? 9 : 8;   // bits of a thread index in the item / pending words
+    constexpr uint32_t TM = (1u << TB) - 1;
     constexpr int RX = WW / 2, RY = WH / 2, NS = WW * WH;
-    constexpr int SW = kTW + WW - 1, SH = kTH + WH - 1, SN = SW * SH;
+    constexpr int SW = kTW + WW - 1, SH = TH + WH - 1, SN = SW * SH;
     constexpr int kRows = 4;                       // pixel rows per box-sum thread
-    static_assert(kTH == 2 * kRows, "box-sum thread map");
+    constexpr int kQ = TH / kRows;                 // box-sum row groups per column
+    static_assert(TH == kQ * kRows, "box-sum thread map");
     extern __shared__ int s_F[];  // [NM][SH][SW] quantised samples F = rint(f * 2^16)
     // certified cost per (view, pixel) or -1, then the certified inside flag
     // of each tile sample as a window centre (general tiles only)
-    int16_t* s_cost = reinterpret_cast<int16_t*>(s_F + NM * SN);  // [NM][kTiledThreads]
-    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_cost + NM * kTiledThreads);
+    int16_t* s_cost = reinterpret_cast<int16_t*>(s_F + NM * SN);  // [NM][NT]
+    uint8_t* s_in = reinterpret_cast<uint8_t*>(s_cost + NM * NT);
     // dense levels: staged runs (after the inside flags, 16-byte aligned)
     uint16_t* s_run = reinterpret_cast<uint16_t*>(
         (reinterpret_cast<uintptr_t>(s_in + NM * SN) + 15) & ~static_cast<uintptr_t>(15));
@@ -1345,24 +1352,24 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
     // max sample bound of the tile (float bits), by plane parity: reset for
     // plane p + 1 between barriers T and C of plane p
     __shared__ unsigned s_emax[2][NM];
-    __shared__ int s_rsum[kTiledThreads];            // sum r of each pixel's window
-    __shared__ float s_rho[kTiledThreads];           // sqrt(ref_var), 0 if ref_var <= 0
-    __shared__ uint32_t s_items[kNccItemCap];        // t | m << 8 | pos << 12 | slot << 19
+    __shared__ int s_rsum[NT];            // sum r of each pixel's window
+    __shared__ float s_rho[NT];           // sqrt(ref_var), 0 if ref_var <= 0
+    __shared__ uint32_t s_items[kNccItemCap];        // t | m << TB | pos << TB+4 | slot << TB+11
     __shared__ double s_vals[kNccItemCap];
-    // (sum_l | sum_r << 16, t | slot << 8 | undecided views << 11 | first view index << 19)
+    // (sum_l | sum_r << 16, t | slot << TB | undecided views << TB+3 | first view index << TB+11)
     __shared__ uint2 s_pend[kNccPend];
     int* s_first = reinterpret_cast<int*>(s_vals);  // prologue only (aliases s_vals)
-    int* s_cnt = s_first + kTiledThreads;
+    int* s_cnt = s_first + NT;
     __shared__ int s_vcost[kNccItemCap / NS + 1];  // pass 2b results
-    __shared__ double s_rmean[kTiledThreads], s_rvar[kTiledThreads];
-    constexpr int kTPV = kTiledThreads / NM;  // tile-build threads per view
+    __shared__ double s_rmean[NT], s_rvar[NT];
+    constexpr int kTPV = NT / NM;  // tile-build threads per view
 
     const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
-    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
+    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * TH;
     const int x = x0 + tx, y = y0 + ty;
     const bool in_img = x < a.w && y < a.h;
 
-    for (int r = threadIdx.x; r < SN; r += kTiledThreads) {
+    for (int r = threadIdx.x; r < SN; r += NT) {
         const int dv = r / SW, du = r - dv * SW;
         const int xx = min(max(x0 - RX + du, 0), a.w - 1);
         const int yy = min(max(y0 - RY + dv, 0), a.h - 1);
@@ -1430,12 +1437,12 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
     const int pmax = min(s_pmax, static_cast<int>(blockIdx.z + 1) * slice - 1);
     const double xd = double(x), yd = double(y);
     // plane union of the 4 pixels of each box-sum job this thread serves
-    constexpr int kJobs = (NM * 2 * kTW + kTiledThreads - 1) / kTiledThreads;
+    constexpr int kJobs = (NM * kQ * kTW + NT - 1) / NT;
     int job_lo[kJobs], job_hi[kJobs];
 #pragma unroll
     for (int jj = 0; jj < kJobs; ++jj) {
-        const int job = threadIdx.x + jj * kTiledThreads;
-        const int bc = job % kTW, bh = (job / kTW) & 1;
+        const int job = threadIdx.x + jj * NT;
+        const int bc = job % kTW, bh = (job / kTW) % kQ;
         job_lo[jj] = 0x7FFFFFFF;
         job_hi[jj] = -1;
 #pragma unroll
@@ -1455,7 +1462,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             // tile parameters of the next kPlaneChunk planes x NM views (the
             // previous chunk's were last read in the box pass of the previous
             // plane, before its barrier C)
-            for (int k = threadIdx.x; k < kPlaneChunk * NM; k += kTiledThreads) {
+            for (int k = threadIdx.x; k < kPlaneChunk * NM; k += NT) {
                 const int pp = p + k / NM, m = k % NM;
                 if (pp <= pmax)
                     s_tp[k / NM][m] = make_tile_params64(s_vc[m].homs + static_cast<size_t>(pp) * 9,
@@ -1521,10 +1528,10 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
         // pixel rows bh*4 .. bh*4+3)
 #pragma unroll
         for (int jj = 0; jj < kJobs; ++jj) {
-            const int job = threadIdx.x + jj * kTiledThreads;
-            if (job >= NM * 2 * kTW)
+            const int job = threadIdx.x + jj * NT;
+            if (job >= NM * kQ * kTW)
                 break;
-            const int m = job / (2 * kTW), bc = job % kTW, bh = (job / kTW) & 1;
+            const int m = job / (kQ * kTW), bc = job % kTW, bh = (job / kTW) % kQ;
             const int tpe = s_tp[slot][m].exact;
             // (a pixel of the job needing another plane inside the union
             // only costs a wasted certification)
@@ -1566,7 +1573,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
                     }
                     const int pix = (row0 + k) * kTW + bc;
                     const float rho = s_rho[pix];
-                    s_cost[m * kTiledThreads + pix] = static_cast<int16_t>(
+                    s_cost[m * NT + pix] = static_cast<int16_t>(
                         rho > 0.0f ? ncc_certify<NS>(S, s_rsum[pix], rho, e_norm) : -1);
                 }
             }
@@ -1589,7 +1596,7 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
                                                s_ref + ty * SW + tx, SW, s_rmean[threadIdx.x],
                                                s_rvar[threadIdx.x], a.census_lut);
                 } else if (((view_in >> m) & 1u) && !flat) {
-                    c = s_cost[m * kTiledThreads + threadIdx.x];
+                    c = s_cost[m * NT + threadIdx.x];
                     if (a.stats) {
                         atomicAdd(a.stats + 0, 1ull);
                         if (c < 0)
@@ -1610,23 +1617,23 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             if (!done) {
                 const int e = atomicAdd(&s_npend, 1);
                 const int off = e < kNccPend ? atomicAdd(&s_count, nun * NS) : kNccItemCap;
-                const uint32_t tag = threadIdx.x | (bslot << 19);
+                const uint32_t tag = threadIdx.x | (bslot << (TB + 11));
                 if (off + nun * NS <= kNccItemCap) {
                     int k = off;
                     for (uint32_t u = unsure; u; u &= u - 1) {
-                        const uint32_t mt = tag | ((__ffs(u) - 1) << 8);
+                        const uint32_t mt = tag | ((__ffs(u) - 1) << TB);
                         for (int q = 0; q < NS; ++q)
-                            s_items[k++] = mt | (q << 12);
+                            s_items[k++] = mt | (q << (TB + 4));
                     }
                     s_pend[e] = make_uint2(static_cast<uint32_t>(sum_l) | (static_cast<uint32_t>(sum_r) << 16),
-                                           threadIdx.x | (bslot << 8) | (unsure << 11) |
-                                               (static_cast<uint32_t>(off / NS) << 19));
+                                           threadIdx.x | (bslot << TB) | (unsure << (TB + 3)) |
+                                               (static_cast<uint32_t>(off / NS) << (TB + 11)));
                 } else {
                     // list overflow (pathological inputs): the owner walks its
                     // views; reserved slots get harmless dummy items
                     if (e < kNccPend) {
                         for (int k = off; k < min(off + nun * NS, kNccItemCap); ++k)
-                            s_items[k] = tag | ((__ffs(unsure) - 1) << 8);
+                            s_items[k] = tag | ((__ffs(unsure) - 1) << TB);
                         s_pend[e] = make_uint2(0u, 0xFFFFFFFFu);
                     }
                     for (uint32_t u = unsure; u; u &= u - 1) {
@@ -1669,11 +1676,11 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             if (a.stats && threadIdx.x == 0)
                 atomicAdd(a.stats + 6, static_cast<unsigned long long>(total));
             // ---- pass 2: the exact samples, one per thread
-            for (int it = threadIdx.x; it < nitems; it += kTiledThreads) {
+            for (int it = threadIdx.x; it < nitems; it += NT) {
                 const uint32_t item = s_items[it];
-                const int t = item & 0xFF, m = (item >> 8) & 0xF, pos = (item >> 12) & 0x7F;
+                const int t = item & TM, m = (item >> TB) & 0xF, pos = (item >> (TB + 4)) & 0x7F;
                 const ViewConst& vc = s_vc[m];
-                s_vals[it] = exact_window_sample(vc.homs + static_cast<size_t>(pb + (item >> 19)) * 9, vc.quad,
+                s_vals[it] = exact_window_sample(vc.homs + static_cast<size_t>(pb + (item >> (TB + 11))) * 9, vc.quad,
                                                  vc.w, vc.h, double(x0 + t % kTW), double(y0 + t / kTW), RX, RY,
                                                  pos / WW, pos % WW);
             }
@@ -1685,9 +1692,9 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             // ---- pass 2b: the reference's sums and NCC of each undecided view
             // (matching.cpp:265-279, same order), one thread per view
             const int nviews_u = nitems / NS;
-            for (int v = threadIdx.x; v < nviews_u; v += kTiledThreads) {
+            for (int v = threadIdx.x; v < nviews_u; v += NT) {
                 const int k0 = v * NS;
-                const int t = s_items[k0] & 0xFF;
+                const int t = s_items[k0] & TM;
                 const int ttx = t % kTW, tty = t / kTW;
                 double sb = 0.0, sbb = 0.0, sab = 0.0;
                 for (int q = 0; q < NS; ++q) {
@@ -1701,14 +1708,14 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
             }
             __syncthreads();  // B
             // ---- pass 3: pending entries -> final costs
-            for (int e = threadIdx.x; e < npend; e += kTiledThreads) {
+            for (int e = threadIdx.x; e < npend; e += NT) {
                 const uint2 pe = s_pend[e];
                 if (pe.y == 0xFFFFFFFFu)
                     continue;
-                const int t = pe.y & 0xFF, sl = (pe.y >> 8) & 7;
-                int vi = static_cast<int>(pe.y >> 19);
+                const int t = pe.y & TM, sl = (pe.y >> TB) & 7;
+                int vi = static_cast<int>(pe.y >> (TB + 11));
                 int sum_l = static_cast<int>(pe.x & 0xFFFFu), sum_r = static_cast<int>(pe.x >> 16);
-                for (uint32_t u = (pe.y >> 11) & 0xFFu; u; u &= u - 1) {
+                for (uint32_t u = (pe.y >> (TB + 3)) & 0xFFu; u; u &= u - 1) {
                     const int c = s_vcost[vi++];
                     if (__ffs(u) - 1 < a.nleft)
                         sum_l += c;
@@ -1732,28 +1739,46 @@ __global__ void __launch_bounds__(kTiledThreads, FMVS_NCC_MINB_OF(WW * WH, NM)) 
     }
 }
 
-template <int WW, int WH, int NM>
-void launch_ncc_nm(const SweepArgs& a, dim3 grid, cudaStream_t s) {
-    const size_t smem = (sizeof(int) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1) +
-                        sizeof(int16_t) * NM * kTiledThreads + 16 +
-                        (a.plane_slicing ? sizeof(uint16_t) * kTiledThreads * (kRunNcc + 2) : 0);
+template <int WW, int WH, int NM, int TH>
+void launch_ncc_nm(const SweepArgs& a, int slices, cudaStream_t s) {
+    constexpr int NT = kTW * TH;
+    const size_t smem = (sizeof(int) + 1) * NM * (kTW + WW - 1) * (TH + WH - 1) +
+                        sizeof(int16_t) * NM * NT + 16 +
+                        (a.plane_slicing ? sizeof(uint16_t) * NT * (kRunNcc + 2) : 0);
     // attribute: the largest size (with the dense-level run staging), a
     // constant -- contexts on other host threads launch the same kernel
-    const int smem_max = static_cast<int>((sizeof(int) + 1) * NM * (kTW + WW - 1) * (kTH + WH - 1) +
-                                          sizeof(int16_t) * NM * kTiledThreads + 16 +
-                                          sizeof(uint16_t) * kTiledThreads * (kRunNcc + 2));
-    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_ncc_tiled<WW, WH, NM>,
+    const int smem_max = static_cast<int>((sizeof(int) + 1) * NM * (kTW + WW - 1) * (TH + WH - 1) +
+                                          sizeof(int16_t) * NM * NT + 16 +
+                                          sizeof(uint16_t) * NT * (kRunNcc + 2));
+    FMVS_CUDA_CHECK(cudaFuncSetAttribute(sweep_ncc_tiled<WW, WH, NM, TH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-    sweep_ncc_tiled<WW, WH, NM><<<grid, kTiledThreads, smem, s>>>(a);
+    const dim3 grid((a.w + kTW - 1) / kTW, (a.h + TH - 1) / TH, slices);
+    sweep_ncc_tiled<WW, WH, NM, TH><<<grid, NT, smem, s>>>(a);
 }
 
+// Dense levels (every pixel sweeps the whole stack) with 5x5 windows and <= 4
+// matching views use 32 x 16 tiles (512 threads, 2 CTAs per SM at 64
+// registers; same threads per slice). Refined levels keep 32 x 8: a taller
+// tile widens the plane union its pixels iterate (measured: C2-NCC L0 1.98
+// -> 2.25 ms with 32 x 16). 9x9 windows and more views: their register budgets.
 template <int WW, int WH>
-bool launch_ncc(const SweepArgs& a, dim3 grid, cudaStream_t s) {
+bool launch_ncc(const SweepArgs& a, int slices, cudaStream_t s) {
+    const bool tall = WW * WH == 25 && a.plane_slicing;
     switch (a.nmatch) {
-        case 2: launch_ncc_nm<WW, WH, 2>(a, grid, s); return true;
-        case 4: launch_ncc_nm<WW, WH, 4>(a, grid, s); return true;
-        case 6: launch_ncc_nm<WW, WH, 6>(a, grid, s); return true;
-        case 8: launch_ncc_nm<WW, WH, 8>(a, grid, s); return true;
+        case 2:
+            if (tall)
+                launch_ncc_nm<WW, WH, 2, 16>(a, slices, s);
+            else
+                launch_ncc_nm<WW, WH, 2, 8>(a, slices, s);
+            return true;
+        case 4:
+            if (tall)
+                launch_ncc_nm<WW, WH, 4, 16>(a, slices, s);
+            else
+                launch_ncc_nm<WW, WH, 4, 8>(a, slices, s);
+            return true;
+        case 6: launch_ncc_nm<WW, WH, 6, 8>(a, slices, s); return true;
+        case 8: launch_ncc_nm<WW, WH, 8, 8>(a, slices, s); return true;
         default: return false;
     }
 }
@@ -1820,9 +1845,9 @@ int sweep(const SweepArgs& a_in, cudaStream_t s) {
     else if (a.kind == FMVS_COST_CENSUS)
         launch_tiled<9, 7>(a, tgrid, s);
     else if (a.ww == 5)
-        launch_ncc<5, 5>(a, tgrid, s);
+        launch_ncc<5, 5>(a, slices, s);
     else
-        launch_ncc<9, 9>(a, tgrid, s);
+        launch_ncc<9, 9>(a, slices, s);
     FMVS_CUDA_CHECK(cudaGetLastError());
     return 2;  // exact (wide pixels) + tiled
 }
