@@ -710,6 +710,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         wa.nz = nz;
         wa.planes = d_planes;
         wa.nplanes = np;
+        wa.wide = !have_prior && np >= 64;  // uniform level: every pixel scans the whole stack
         const bool capture = ctx->cap.level == l;
         if (capture)
             wa.winners = ctx->buf("cap_winners").as<int32_t>(static_cast<size_t>(P.w) * P.h);

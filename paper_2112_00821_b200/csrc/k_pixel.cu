@@ -42,6 +42,38 @@ __device__ double parabola_dev(double d_prev, double d_win, double d_next, doubl
     return v < d_prev ? d_prev : (d_next < v ? d_next : v);
 }
 
+// Winner of pixel p (plane f + best) -> winners / refined depth
+// (pipeline.cpp:263-288).
+__device__ __forceinline__ void wta_finish(const WtaArgs& a, int x, int y, size_t p, uint64_t e0, int f,
+                                           int c, int best) {
+    using namespace dev;
+    const uint32_t* v32 = a.agg + e0;
+    const uint16_t* v16 = reinterpret_cast<const uint16_t*>(a.agg) + e0;
+    auto val = [&](int i) -> uint32_t { return a.agg16 ? v16[i] : v32[i]; };
+    const int win = f + best;
+    if (a.winners)
+        a.winners[p] = win;
+    if (!a.depth)
+        return;
+    const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject_px(a.intr, x, y));
+    const double d_win = depth_from_plane_dev(denom, a.planes[win]);
+    float out = 0.0f;
+    if (d_win > 0.0) {
+        double d = d_win;
+        if (win - 1 >= f && win + 1 < f + c) {
+            const double d_lo = depth_from_plane_dev(denom, a.planes[win + 1]);
+            const double d_hi = depth_from_plane_dev(denom, a.planes[win - 1]);
+            if (d_lo > 0.0 && d_hi > 0.0 && d_lo < d_win && d_win < d_hi)
+                d = parabola_dev(d_lo, d_win, d_hi, double(val(best + 1)), double(val(best)),
+                                 double(val(best - 1)));
+        }
+        out = __double2float_rn(d);
+    }
+    a.depth[p] = out;
+}
+
+// One thread per pixel, a sequential scan of its entries (the reference's
+// first minimum): refined levels, where ranges are short.
 __global__ void wta_depth_kernel(WtaArgs a) {
     using namespace dev;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -71,27 +103,77 @@ __global__ void wta_depth_kernel(WtaArgs a) {
             best = i;
         }
     }
-    const int win = f + best;
-    if (a.winners)
-        a.winners[p] = win;
-    if (!a.depth)
-        return;
-    // pipeline.cpp:263-288
-    const double denom = dot3(D3{a.nx, a.ny, a.nz}, unproject_px(a.intr, x, y));
-    const double d_win = depth_from_plane_dev(denom, a.planes[win]);
-    float out = 0.0f;
-    if (d_win > 0.0) {
-        double d = d_win;
-        if (win - 1 >= f && win + 1 < f + c) {
-            const double d_lo = depth_from_plane_dev(denom, a.planes[win + 1]);
-            const double d_hi = depth_from_plane_dev(denom, a.planes[win - 1]);
-            if (d_lo > 0.0 && d_hi > 0.0 && d_lo < d_win && d_win < d_hi)
-                d = parabola_dev(d_lo, d_win, d_hi, double(val(best + 1)), double(val(best)),
-                                 double(val(best - 1)));
+    wta_finish(a, x, y, p, e0, f, c, best);
+}
+
+// Lane i scans entries i, i + 32, ... of one pixel (strict <: each lane's
+// first minimum); (value, index) reduced with ties to the lower index.
+template <typename T>
+__device__ __forceinline__ int warp_argmin_first(const T* __restrict__ v, int c, int lane) {
+    uint32_t bv = 0xFFFFFFFFu;
+    int bi = 0x7FFFFFFF;
+    for (int i = lane; i < c; i += 32) {
+        const uint32_t vi = v[i];
+        if (vi < bv) {
+            bv = vi;
+            bi = i;
         }
-        out = __double2float_rn(d);
     }
-    a.depth[p] = out;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const uint32_t ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+        const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+        if (ov < bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    return bi;
+}
+
+// Uniform (dense) levels: a warp per 32 consecutive pixels of a row; the
+// warp scans each pixel's entries coalesced and finds the same first minimum
+// as the sequential scan, then every lane refines its own pixel.
+constexpr int kWtaWarps = 8;
+__global__ void __launch_bounds__(32 * kWtaWarps) wta_depth_warp_kernel(WtaArgs a) {
+    using namespace dev;
+    const int lane = threadIdx.x & 31;
+    const int x0 = (blockIdx.x * kWtaWarps + (threadIdx.x >> 5)) * 32;
+    const int y = blockIdx.y;
+    if (x0 >= a.w)
+        return;  // warp-uniform
+    const int x = x0 + lane;
+    const bool valid = x < a.w;
+    const size_t p = static_cast<size_t>(y) * a.w + x;
+    int f = 0, c = 0;
+    uint64_t e0 = 0;
+    if (valid) {
+        const VolMeta m = a.meta[p];
+        f = meta_first(m.fc);
+        c = meta_count(m.fc);
+        e0 = a.row_base[y] + m.rel;
+    }
+    int best = 0;
+    for (int j = 0; j < 32; ++j) {
+        const int cj = __shfl_sync(0xFFFFFFFFu, c, j);
+        if (cj == 0)
+            continue;
+        const uint64_t ej = __shfl_sync(0xFFFFFFFFu, e0, j);
+        const int bj = a.agg16 ? warp_argmin_first(reinterpret_cast<const uint16_t*>(a.agg) + ej, cj, lane)
+                               : warp_argmin_first(a.agg + ej, cj, lane);
+        if (lane == j)
+            best = bj;
+    }
+    if (!valid)
+        return;
+    if (c == 0) {
+        if (a.winners)
+            a.winners[p] = -1;
+        if (a.depth)
+            a.depth[p] = 0.0f;
+        return;
+    }
+    wta_finish(a, x, y, p, e0, f, c, best);
 }
 
 // median_filter_5x5 (pipeline.cpp:175-198): element valid/2 of the sorted
@@ -400,7 +482,11 @@ inline dim3 grid2(int w, int h) { return dim3((w + 31) / 32, (h + 7) / 8); }
 }  // namespace
 
 void wta_depth(const WtaArgs& a, cudaStream_t s) {
-    wta_depth_kernel<<<dim3((a.w + 127) / 128, a.h), 128, 0, s>>>(a);
+    if (a.wide)
+        wta_depth_warp_kernel<<<dim3((a.w + 32 * kWtaWarps - 1) / (32 * kWtaWarps), a.h), 32 * kWtaWarps, 0,
+                                s>>>(a);
+    else
+        wta_depth_kernel<<<dim3((a.w + 127) / 128, a.h), 128, 0, s>>>(a);
     FMVS_CUDA_CHECK(cudaGetLastError());
 }
 

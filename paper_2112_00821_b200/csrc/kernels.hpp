@@ -178,6 +178,7 @@ struct WtaArgs {
     double nx, ny, nz;
     const double* planes;
     int nplanes;
+    int wide;                        // long ranges (dense levels): warp-cooperative scan
 };
 void wta_depth(const WtaArgs& a, cudaStream_t s);
 
