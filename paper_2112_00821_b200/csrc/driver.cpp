@@ -612,6 +612,7 @@ void run_bundle(fmvs_ctx* ctx, const fmvs_view* views, int n, const fmvs_config&
         sa.disable_tiled = ctx->sweep_exact;
         sa.plane_slicing = l == L - 1;  // uniform ranges: every pixel sweeps the whole stack
         sa.narrow_max = l == L - 1 ? 65535 : 0;
+        sa.small_lists = std::getenv("FMVS_NCC_SMALL_LISTS") != nullptr;
         if (ctx->sweep_stats == 1 || ctx->sweep_stats == 2 + l)
             sa.stats = ctx->buf("sweep_stats").as<unsigned long long>(8);
         ctx->timed(l == 0 ? "sweep_l0" : "sweep", [&] { launches += k::sweep(sa, s); });
@@ -1317,6 +1318,7 @@ int fmvs_sweep_cost_volume(fmvs_ctx* ctx, const fmvs_view* views, int32_t n, int
         sa.plane_slicing = 1;
         if (const char* e = std::getenv("FMVS_SWEEP_NARROW"))
             sa.narrow_max = std::atoi(e);
+        sa.small_lists = std::getenv("FMVS_NCC_SMALL_LISTS") != nullptr;
         k::sweep(sa, s);
         std::vector<fmvs::dev::VolMeta> meta(px);
         FMVS_CUDA_CHECK(cudaMemcpyAsync(meta.data(), ra.meta, px * 8, cudaMemcpyDeviceToHost, s));

@@ -1362,7 +1362,10 @@ __global__ void __launch_bounds__(32 * TH, TH == 16 ? 2 : FMVS_NCC_MINB_OF(WW * 
     int* s_cnt = s_first + NT;
     __shared__ int s_vcost[kNccItemCap / NS + 1];  // pass 2b results
     __shared__ double s_rmean[NT], s_rvar[NT];
-    constexpr int kTPV = NT / NM;  // tile-build threads per view
+    constexpr int kTPV = NT / NM;
+    // capacities of the exact lists (the test hook shrinks them)
+    const int icap = a.small_lists ? 2 * NS : kNccItemCap;
+    const int pcap = a.small_lists ? 2 : kNccPend;  // tile-build threads per view
 
     const int tx = threadIdx.x % kTW, ty = threadIdx.x / kTW;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * TH;
@@ -1504,7 +1507,7 @@ __global__ void __launch_bounds__(32 * TH, TH == 16 ? 2 : FMVS_NCC_MINB_OF(WW * 
         const int bslot = (p - pmin) % kRunNcc;  // plane's slot in its run
         // lists already half full (appended by planes < p, reset before T):
         // resolve at the end of this plane instead of the run's end
-        const bool early = s_count >= kNccItemCap / 2 || s_npend >= kNccPend / 2;
+        const bool early = s_count >= icap / 2 || s_npend >= pcap / 2;
         uint32_t view_in = 0, view_exact = 0;
         if (need) {
 #pragma unroll
@@ -1616,9 +1619,9 @@ __global__ void __launch_bounds__(32 * TH, TH == 16 ? 2 : FMVS_NCC_MINB_OF(WW * 
             bool done = unsure == 0;
             if (!done) {
                 const int e = atomicAdd(&s_npend, 1);
-                const int off = e < kNccPend ? atomicAdd(&s_count, nun * NS) : kNccItemCap;
+                const int off = e < pcap ? atomicAdd(&s_count, nun * NS) : icap;
                 const uint32_t tag = threadIdx.x | (bslot << (TB + 11));
-                if (off + nun * NS <= kNccItemCap) {
+                if (off + nun * NS <= icap) {
                     int k = off;
                     for (uint32_t u = unsure; u; u &= u - 1) {
                         const uint32_t mt = tag | ((__ffs(u) - 1) << TB);
@@ -1631,8 +1634,8 @@ __global__ void __launch_bounds__(32 * TH, TH == 16 ? 2 : FMVS_NCC_MINB_OF(WW * 
                 } else {
                     // list overflow (pathological inputs): the owner walks its
                     // views; reserved slots get harmless dummy items
-                    if (e < kNccPend) {
-                        for (int k = off; k < min(off + nun * NS, kNccItemCap); ++k)
+                    if (e < pcap) {
+                        for (int k = off; k < min(off + nun * NS, icap); ++k)
                             s_items[k] = tag | ((__ffs(unsure) - 1) << TB);
                         s_pend[e] = make_uint2(0u, 0xFFFFFFFFu);
                     }
@@ -1671,8 +1674,8 @@ __global__ void __launch_bounds__(32 * TH, TH == 16 ? 2 : FMVS_NCC_MINB_OF(WW * 
             const int pb = p - bslot;  // first plane of the run
             __syncthreads();  // I: item and pending lists complete
             const int total = s_count;
-            const int npend = min(s_npend, kNccPend);
-            const int nitems = min(total, kNccItemCap);
+            const int npend = min(s_npend, pcap);
+            const int nitems = min(total, icap);
             if (a.stats && threadIdx.x == 0)
                 atomicAdd(a.stats + 6, static_cast<unsigned long long>(total));
             // ---- pass 2: the exact samples, one per thread

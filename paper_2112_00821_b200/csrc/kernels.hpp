@@ -89,6 +89,8 @@ struct SweepArgs {
                                      // tiled kernels then stage each pixel's costs of 16
                                      // planes and write them as one 32-byte run
     int narrow_max;                  // pixels with more hypotheses take the exact kernel (0: default)
+    int small_lists;                 // test hook (FMVS_NCC_SMALL_LISTS): NCC exact lists of 2 views / 2
+                                     // pending entries, to exercise the overflow paths
     unsigned long long* stats;       // optional diagnostics (fmvs_ctx_sweep_stats)
 };
 // returns the number of kernels launched

@@ -560,6 +560,44 @@ def test_estimate_bundle_bitexact(b200, oracle, name, scene, cfg, group, arena, 
     assert (b.depth > 0).mean() > 0.5
 
 
+@pytest.mark.parametrize("cost", ["ncc5", "ncc9"])
+@pytest.mark.parametrize("texture", ["scene", "quantized"])
+def test_ncc_exact_list_overflow(b200, oracle, rng, cost, texture, monkeypatch):
+    """The NCC sweep's batched exact resolution with its lists shrunk to two
+    views / two pending entries (FMVS_NCC_SMALL_LISTS, read per call): the
+    early resolution, the owner's serial walk on overflow and the dummy items
+    of reserved slots all run, results bit-identical."""
+    monkeypatch.setenv("FMVS_NCC_SMALL_LISTS", "1")
+    bundle, stack = _level_inputs(oracle, w=96, h=64)
+    if texture == "quantized":
+        for v in bundle:
+            v.image = ((v.image // 48) * 48).astype(np.uint8)
+    h, w = bundle[2].image.shape
+    lo = np.full((h, w), 6.0, np.float32)
+    hi = np.full((h, w), 16.0, np.float32)
+    spec = {"ncc5": (CostKind.NccTruncated, 5, 5), "ncc9": (CostKind.NccTruncated, 9, 9)}[cost]
+    cf = CostFunctionSpec(*spec)
+    a = b200.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    b = oracle.sweep_cost_volume(bundle, 2, stack, lo, hi, cf)
+    assert_same(a.costs, b.costs, "costs")
+
+
+@pytest.mark.parametrize("name", ["c4_fronto_ncc_pi", "ncc9_sn_7views"])
+def test_estimate_bundle_ncc_small_lists(b200, oracle, name, monkeypatch):
+    """Whole bundles (dense and refined levels) through the shrunk NCC lists."""
+    monkeypatch.setenv("FMVS_NCC_SMALL_LISTS", "1")
+    _, scene, cfg = next(e for e in E2E if e[0] == name)
+    scene = dict(scene)
+    kind = scene.pop("kind")
+    bundle, _, _ = render(oracle, kind, **scene)
+    c = config(**cfg)
+    a = b200.estimate_bundle(bundle, c)
+    b = oracle.estimate_bundle(bundle, c)
+    assert_same(a.depth, b.depth, "depth")
+    assert_same(a.normals, b.normals, "normals")
+    assert_same(a.confidence, b.confidence, "confidence")
+
+
 @pytest.mark.parametrize("name", ["dense_216_planes", "c4_fronto_ncc_pi", "census_sn_3lvl", "c5_slanted_pg"])
 def test_estimate_bundle_packed_aggregate(oracle, name, monkeypatch):
     """The packed u16 SGM aggregate (two entries per 32-bit RED word), which
